@@ -1,0 +1,169 @@
+// common.cuh -- shared device-side building blocks of the B200 engine.
+//
+//  * tiled scenario layout   [w/32][row][w%32]: a warp of 32 consecutive
+//    scenarios reads one 128-byte line per row, for any tour order;
+//  * counter-based SplitMix64 (scenario.hpp:12-57): row r of column w is
+//    mix64(s_w + r*gamma), s_w = derive_stream(seed, kStreamScenario, w);
+//  * exact fixed-point aggregate (scendp_cuda.h "aggregates"): order- and
+//    shard-invariant sums of finite costs.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "scendp_cuda.h"
+
+namespace scendp_dev {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kStreamScenario = 0x5343454eULL;  // scenario.hpp:49
+constexpr int kTile = 32;                            // scenarios per tile
+constexpr int kAggWords = 16;                        // scendp_agg_raw / u64
+constexpr int kAggSlots = 17;  // 13 digits (12 + always-zero guard) + 4 counts
+constexpr int kDigitFinite = 13, kDigitInfeasible = 14, kDigitError = 15,
+              kDigitRange = 16;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += kGamma;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t derive_stream(uint64_t seed,
+                                                           uint64_t tag,
+                                                           uint64_t index) {
+  return mix64(mix64(mix64(seed) ^ tag) ^ index);
+}
+
+// Element index of (scenario w, row r) in the tiled layout.
+__host__ __device__ __forceinline__ uint64_t tiled_index(uint64_t w, uint64_t r,
+                                                         uint64_t rows) {
+  return ((w >> 5) * rows + r) * kTile + (w & 31);
+}
+
+// Generator parameters shared by the fused (in-DP) and materializing paths.
+struct GenParams {
+  int32_t kind;        // SCENDP_DIST_*
+  int64_t lo;
+  uint64_t span;       // uniform: hi - lo + 1
+  const double* cdf;   // poisson: P[0..cdf_len-1], device
+  int32_t cdf_len;
+  uint64_t seed;
+  uint64_t first_index;
+};
+
+// One counter-based draw: DistributionSpec::sample for the kinds that use
+// exactly one next() per value (scenario.cpp:23-26; poisson: SURVEY App. A).
+__device__ __forceinline__ uint32_t draw_counter(const GenParams& g,
+                                                 uint64_t stream, uint64_t row) {
+  const uint64_t x = mix64(stream + row * kGamma);
+  if (g.kind == SCENDP_DIST_UNIFORM) {
+    return static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
+  }
+  // next_unit: ((x >> 11) + 1) * 2^-53, exact in fp64
+  const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
+  int32_t k = 0;
+  while (u > __ldg(g.cdf + k)) ++k;  // cdf[len-1] == 1.0 terminates
+  return static_cast<uint32_t>(k);
+}
+
+// ---------------------------------------------------------------------------
+// Exact aggregate.  A finite cost v >= 0 is v = M * 2^E (M < 2^53); it adds
+// M << (E + 192) into a 384-bit integer held as 32-bit digits d[0..11] (one
+// u64 word each, weight 2^(32j-192)).  Bits below 2^-192 are truncated
+// (deterministically); v >= 2^192 counts as a range error.
+struct AggPieces {
+  uint32_t p0, p1, p2;
+  int32_t li;       // digit index of p0
+  int32_t kind;     // 0 finite, 1 infeasible(+inf), 2 error, 3 range, 4 none
+};
+
+__device__ __forceinline__ AggPieces agg_pieces(double v, bool evaluated) {
+  AggPieces a{0u, 0u, 0u, 0, 4};
+  if (!evaluated) { a.kind = 2; return a; }
+  if (!(v < __longlong_as_double(0x7ff0000000000000LL))) { a.kind = 1; return a; }
+  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+  const int be = static_cast<int>((bits >> 52) & 0x7ff);
+  uint64_t M = bits & ((1ULL << 52) - 1);
+  int E;
+  if (be == 0) { E = -1074; } else { M |= (1ULL << 52); E = be - 1075; }
+  int pos = E + 192;
+  if (pos + 53 > 384) { a.kind = 3; return a; }
+  if (pos < 0) {
+    M = (-pos >= 64) ? 0ULL : (M >> (-pos));
+    pos = 0;
+  }
+  const int sub = pos & 31;
+  const uint32_t lo = static_cast<uint32_t>(M);
+  const uint32_t hi = static_cast<uint32_t>(M >> 32);
+  a.li = pos >> 5;
+  a.p0 = lo << sub;
+  a.p1 = __funnelshift_l(lo, hi, sub);
+  a.p2 = sub ? (hi >> (32 - sub)) : 0u;
+  a.kind = 0;
+  return a;
+}
+
+// Warp-cooperative accumulation into a CTA accumulator in shared memory
+// (kAggSlots u64).  Must be called by all 32 lanes of the warp, converged;
+// lanes without a value pass valid = false.
+__device__ __forceinline__ void agg_warp_add(unsigned long long* cta_acc,
+                                             AggPieces a, bool valid) {
+  const unsigned full = 0xffffffffu;
+  if (!valid) a.kind = 4;
+  const int lane = threadIdx.x & 31;
+  const unsigned fin = __ballot_sync(full, a.kind == 0);
+  const unsigned inf = __ballot_sync(full, a.kind == 1);
+  const unsigned err = __ballot_sync(full, a.kind == 2);
+  const unsigned rng = __ballot_sync(full, a.kind == 3);
+  const int leader = __ffs(full) - 1;
+  if (lane == leader) {
+    if (fin) atomicAdd(cta_acc + kDigitFinite, static_cast<unsigned long long>(__popc(fin)));
+    if (inf) atomicAdd(cta_acc + kDigitInfeasible, static_cast<unsigned long long>(__popc(inf)));
+    if (err) atomicAdd(cta_acc + kDigitError, static_cast<unsigned long long>(__popc(err)));
+    if (rng) atomicAdd(cta_acc + kDigitRange, static_cast<unsigned long long>(__popc(rng)));
+  }
+  if (!fin) return;
+  if (a.kind == 0) {
+    // lanes with the same digit index reduce together (one group in the
+    // common case of costs of similar magnitude)
+    const unsigned grp = __match_any_sync(fin, a.li);
+    const unsigned s0l = __reduce_add_sync(grp, a.p0 & 0xffffu);
+    const unsigned s0h = __reduce_add_sync(grp, a.p0 >> 16);
+    const unsigned s1l = __reduce_add_sync(grp, a.p1 & 0xffffu);
+    const unsigned s1h = __reduce_add_sync(grp, a.p1 >> 16);
+    const unsigned s2l = __reduce_add_sync(grp, a.p2 & 0xffffu);
+    const unsigned s2h = __reduce_add_sync(grp, a.p2 >> 16);
+    if (lane == __ffs(grp) - 1) {
+      atomicAdd(cta_acc + a.li, static_cast<unsigned long long>(s0l) +
+                                    (static_cast<unsigned long long>(s0h) << 16));
+      atomicAdd(cta_acc + a.li + 1, static_cast<unsigned long long>(s1l) +
+                                        (static_cast<unsigned long long>(s1h) << 16));
+      if (s2l | s2h)
+        atomicAdd(cta_acc + a.li + 2, static_cast<unsigned long long>(s2l) +
+                                          (static_cast<unsigned long long>(s2h) << 16));
+    }
+  }
+}
+
+// CTA epilogue: add the CTA accumulator into the global raw aggregate of one
+// candidate (scendp_agg_raw layout: 12 digits, finite, infeasible, error,
+// range).  Integer atomics: associative, hence deterministic.
+__device__ __forceinline__ void agg_cta_flush(const unsigned long long* cta_acc,
+                                              unsigned long long* global_raw) {
+  const int t = threadIdx.x;
+  if (t < 12) {
+    const unsigned long long v = cta_acc[t];
+    if (v) atomicAdd(global_raw + t, v);
+  } else if (t >= 13 && t < kAggSlots) {
+    const unsigned long long v = cta_acc[t];
+    if (v) atomicAdd(global_raw + (t - 1), v);
+  }
+}
+
+__device__ __forceinline__ void agg_cta_init(unsigned long long* cta_acc) {
+  for (int t = threadIdx.x; t < kAggSlots; t += blockDim.x) cta_acc[t] = 0ULL;
+}
+
+}  // namespace scendp_dev

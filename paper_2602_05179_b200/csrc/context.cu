@@ -1,0 +1,439 @@
+// context.cu -- C-ABI: contexts, memory, timing, aggregates, NCCL.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+using namespace scendp_host;
+
+namespace scendp_host {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- NCCL, loaded at run time ----------------------------------------------
+// Minimal ABI of nccl.h (2.x): opaque comm, 128-byte unique id, enums.
+typedef struct { char internal[SCENDP_NCCL_UNIQUE_ID_BYTES]; } NcclUniqueId;
+typedef int NcclResult;
+struct NcclApi {
+  void* handle = nullptr;
+  NcclResult (*GetUniqueId)(NcclUniqueId*) = nullptr;
+  NcclResult (*CommInitRank)(void**, int, NcclUniqueId, int) = nullptr;
+  NcclResult (*CommInitAll)(void**, int, const int*) = nullptr;
+  NcclResult (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  NcclResult (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(NcclResult) = nullptr;
+};
+constexpr int kNcclUint64 = 5, kNcclSum = 0;
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.handle = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.handle) break;
+    }
+    if (!api.handle) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(dlsym(api.handle, "ncclCommInitAll"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
+  });
+  if (!api.handle || !api.AllReduce)
+    fail(SCENDP_ERR_NCCL, "NCCL not available (dlopen libnccl.so.2 failed)");
+  return api;
+}
+
+static void nccl_check(NcclResult r, const char* what) {
+  if (r == 0) return;
+  fail(SCENDP_ERR_NCCL, std::string(what) + ": " +
+                            (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+}
+
+// ---- exact aggregate finalization -----------------------------------------
+// The device accumulates 32-bit digits d[j] (weight 2^(32j-192)) in u64
+// words.  Carry-propagate into 32-bit words and round once to the nearest
+// double (ties to even) -> the correctly rounded sum.
+static double digits_to_double(const unsigned __int128* dsum) {
+  uint32_t w[18] = {};
+  unsigned __int128 carry = 0;
+  for (int j = 0; j < 18; ++j) {
+    unsigned __int128 t = carry + (j < SCENDP_AGG_DIGITS ? dsum[j] : 0);
+    w[j] = static_cast<uint32_t>(t);
+    carry = t >> 32;
+  }
+  int J = 17;
+  while (J >= 0 && w[J] == 0) --J;
+  if (J < 0) return 0.0;
+  unsigned __int128 T = 0;
+  int base = J - 2;  // word index of T's lowest word
+  for (int j = J; j >= J - 2; --j) T = (T << 32) | (j >= 0 ? w[j] : 0u);
+  bool sticky = false;
+  for (int j = 0; j < base; ++j) sticky |= (w[j] != 0);
+  int nbits = 0;
+  for (unsigned __int128 x = T; x; x >>= 1) ++nbits;
+  uint64_t mant;
+  int shift = 0;
+  if (nbits <= 53) {
+    mant = static_cast<uint64_t>(T);
+  } else {
+    shift = nbits - 53;
+    mant = static_cast<uint64_t>(T >> shift);
+    const unsigned __int128 rem = T & ((static_cast<unsigned __int128>(1) << shift) - 1);
+    const unsigned __int128 half = static_cast<unsigned __int128>(1) << (shift - 1);
+    const bool up = rem > half || (rem == half && (sticky || (mant & 1)));
+    if (up) {
+      ++mant;
+      if (mant == (1ULL << 53)) { mant >>= 1; ++shift; }
+    }
+  }
+  return std::ldexp(static_cast<double>(mant), shift + 32 * base - 192);
+}
+
+void finalize_agg(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
+                  scendp_agg* out) {
+  for (uint32_t c = 0; c < k; ++c) {
+    unsigned __int128 d[SCENDP_AGG_DIGITS] = {};
+    scendp_agg a{};
+    for (uint32_t r = 0; r < n; ++r) {
+      const scendp_agg_raw& x = raw[static_cast<uint64_t>(r) * k + c];
+      for (int j = 0; j < SCENDP_AGG_DIGITS; ++j) d[j] += x.digits[j];
+      a.finite_count += x.finite_count;
+      a.infeasible_count += x.infeasible_count;
+      a.error_count += x.error_count;
+      a.range_errors += x.range_errors;
+    }
+    a.sum = digits_to_double(d);
+    a.mean = a.finite_count ? a.sum / static_cast<double>(a.finite_count)
+                            : std::numeric_limits<double>::quiet_NaN();
+    out[c] = a;
+  }
+}
+
+}  // namespace scendp_host
+
+// ---- scendp_ctx members ------------------------------------------------------
+void* scendp_ctx::scratch_get(int slot, uint64_t bytes) {
+  if (bytes == 0) bytes = 256;
+  if (scratch_bytes[slot] >= bytes) return scratch[slot];
+  if (scratch[slot]) {
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    CUDA_CHECK(cudaFree(scratch[slot]));
+    scratch[slot] = nullptr;
+    scratch_bytes[slot] = 0;
+  }
+  const uint64_t want = (bytes + (bytes >> 3) + 4095) & ~uint64_t{4095};
+  CUDA_CHECK(cudaMalloc(&scratch[slot], want));
+  scratch_bytes[slot] = want;
+  return scratch[slot];
+}
+
+void* scendp_ctx::pinned_agg(uint64_t bytes) {
+  if (agg_pinned_bytes >= bytes) return agg_pinned;
+  if (agg_pinned) CUDA_CHECK(cudaFreeHost(agg_pinned));
+  agg_pinned = nullptr;
+  CUDA_CHECK(cudaMallocHost(&agg_pinned, bytes));
+  agg_pinned_bytes = bytes;
+  return agg_pinned;
+}
+
+int scendp_ctx::timing_begin(int kind) {
+  if (!(opts.flags & SCENDP_CTX_KERNEL_TIMING)) return -1;
+  const int idx = static_cast<int>(pending.size());
+  if (idx >= static_cast<int>(event_pool.size())) {
+    cudaEvent_t a, b;
+    CUDA_CHECK(cudaEventCreate(&a));
+    CUDA_CHECK(cudaEventCreate(&b));
+    event_pool.emplace_back(a, b);
+  }
+  CUDA_CHECK(cudaEventRecord(event_pool[idx].first, stream));
+  pending.push_back({idx, kind});
+  return idx;
+}
+
+void scendp_ctx::timing_end(int token) {
+  if (token < 0) return;
+  CUDA_CHECK(cudaEventRecord(event_pool[token].second, stream));
+}
+
+void scendp_ctx::timing_resolve() {
+  for (const Pending& p : pending) {
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, event_pool[p.pool_index].first,
+                                    event_pool[p.pool_index].second));
+    if (p.kind == 0) {
+      stats.dp_launches += 1;
+      stats.dp_ms += ms;
+    } else {
+      stats.gen_launches += 1;
+      stats.gen_ms += ms;
+    }
+  }
+  pending.clear();
+}
+
+void scendp_ctx::sync() {
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  timing_resolve();
+}
+
+void scendp_ctx::allreduce_agg(void* dev_raw, uint64_t words) {
+  if (!nccl_comm || nranks <= 1) return;
+  nccl_check(nccl().AllReduce(dev_raw, dev_raw, words, kNcclUint64, kNcclSum,
+                              nccl_comm, stream),
+             "ncclAllReduce");
+}
+
+// ---- C-ABI -------------------------------------------------------------------
+extern "C" {
+
+const char* scendp_last_error(void) { return g_last_error.c_str(); }
+
+int32_t scendp_abi_version(void) { return SCENDP_ABI_VERSION; }
+
+scendp_status scendp_ctx_create(const scendp_opts* opts, scendp_ctx** out) {
+  return guard([&] {
+    if (!out) fail(SCENDP_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    int ndev = 0;
+    const cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      fail(SCENDP_ERR_NO_DEVICE,
+           std::string("no CUDA device available (the engine has no CPU fallback): ") +
+               cudaGetErrorString(e));
+    scendp_opts o{};
+    o.device = -1;
+    if (opts) o = *opts;
+    int dev = o.device;
+    if (dev < 0) CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev >= ndev) fail(SCENDP_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    CUDA_CHECK(cudaSetDevice(dev));
+    cudaDeviceProp prop{};
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+      fail(SCENDP_ERR_NO_DEVICE, "this build targets sm_100a (B200); device is sm_" +
+                                     std::to_string(prop.major * 10 + prop.minor));
+    auto* ctx = new scendp_ctx();
+    ctx->device = dev;
+    ctx->sm_count = prop.multiProcessorCount;
+    ctx->opts = o;
+    ctx->opts.device = dev;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreate(&ctx->t0));
+    CUDA_CHECK(cudaEventCreate(&ctx->t1));
+    *out = ctx;
+  });
+}
+
+void scendp_ctx_destroy(scendp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->nccl_comm) scendp_comm_destroy(ctx);
+  for (int s = 0; s < kScrCount; ++s)
+    if (ctx->scratch[s]) cudaFree(ctx->scratch[s]);
+  if (ctx->agg_pinned) cudaFreeHost(ctx->agg_pinned);
+  for (auto& p : ctx->event_pool) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  cudaEventDestroy(ctx->t0);
+  cudaEventDestroy(ctx->t1);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+scendp_status scendp_ctx_info(scendp_ctx* ctx, int32_t* device, int32_t* sm_count,
+                              void** cuda_stream) {
+  return guard([&] {
+    if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
+    if (device) *device = ctx->device;
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (cuda_stream) *cuda_stream = ctx->stream;
+  });
+}
+
+scendp_status scendp_ctx_sync(scendp_ctx* ctx) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->sync();
+  });
+}
+
+scendp_status scendp_ctx_set_max_batch(scendp_ctx* ctx, uint64_t max_batch) {
+  return guard([&] {
+    if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
+    ctx->opts.max_batch = max_batch;
+  });
+}
+
+scendp_status scendp_device_alloc(scendp_ctx* ctx, uint64_t bytes, void** ptr) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    CUDA_CHECK(cudaMalloc(ptr, bytes ? bytes : 1));
+  });
+}
+
+scendp_status scendp_device_free(scendp_ctx* ctx, void* ptr) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    CUDA_CHECK(cudaFree(ptr));
+  });
+}
+
+scendp_status scendp_host_alloc_pinned(uint64_t bytes, void** ptr) {
+  return guard([&] { CUDA_CHECK(cudaMallocHost(ptr, bytes ? bytes : 1)); });
+}
+
+scendp_status scendp_host_free_pinned(void* ptr) {
+  return guard([&] { CUDA_CHECK(cudaFreeHost(ptr)); });
+}
+
+scendp_status scendp_memcpy(scendp_ctx* ctx, void* dst, const void* src,
+                            uint64_t bytes, int32_t kind, uint32_t flags) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                             : kind == 1 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream));
+    if (!(flags & SCENDP_ASYNC)) ctx->sync();
+  });
+}
+
+scendp_status scendp_memset(scendp_ctx* ctx, void* dst, int32_t value, uint64_t bytes) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    CUDA_CHECK(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  });
+}
+
+scendp_status scendp_agg_finalize(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
+                                  scendp_agg* out) {
+  return guard([&] {
+    if (!raw || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "null aggregate pointer");
+    finalize_agg(raw, n, k, out);
+  });
+}
+
+int64_t scendp_best_candidate(const scendp_agg* agg, uint32_t k) {
+  int64_t best = -1;
+  double bv = std::numeric_limits<double>::infinity();
+  for (uint32_t c = 0; c < k; ++c) {
+    if (agg[c].finite_count == 0) continue;
+    if (agg[c].mean < bv) {
+      bv = agg[c].mean;
+      best = c;
+    }
+  }
+  return best;
+}
+
+scendp_status scendp_nccl_unique_id(uint8_t out[SCENDP_NCCL_UNIQUE_ID_BYTES]) {
+  return guard([&] {
+    NcclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, SCENDP_NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+scendp_status scendp_comm_init_rank(scendp_ctx* ctx,
+                                    const uint8_t id[SCENDP_NCCL_UNIQUE_ID_BYTES],
+                                    int32_t nranks, int32_t rank) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "bad rank / nranks");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    NcclUniqueId uid;
+    std::memcpy(uid.internal, id, SCENDP_NCCL_UNIQUE_ID_BYTES);
+    void* comm = nullptr;
+    nccl_check(nccl().CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
+    ctx->nccl_comm = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+scendp_status scendp_comm_init_all(scendp_ctx** ctxs, int32_t n) {
+  return guard([&] {
+    if (n < 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one context");
+    std::vector<int> devs(n);
+    for (int i = 0; i < n; ++i) devs[i] = ctxs[i]->device;
+    std::vector<void*> comms(n, nullptr);
+    nccl_check(nccl().CommInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
+    for (int i = 0; i < n; ++i) {
+      ctxs[i]->nccl_comm = comms[i];
+      ctxs[i]->nranks = n;
+      ctxs[i]->rank = i;
+    }
+  });
+}
+
+scendp_status scendp_comm_destroy(scendp_ctx* ctx) {
+  return guard([&] {
+    if (ctx->nccl_comm) nccl().CommDestroy(ctx->nccl_comm);
+    ctx->nccl_comm = nullptr;
+    ctx->nranks = 1;
+    ctx->rank = 0;
+  });
+}
+
+scendp_status scendp_timer_start(scendp_ctx* ctx) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    CUDA_CHECK(cudaEventRecord(ctx->t0, ctx->stream));
+  });
+}
+
+scendp_status scendp_timer_stop(scendp_ctx* ctx, double* ms) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    CUDA_CHECK(cudaEventRecord(ctx->t1, ctx->stream));
+    ctx->sync();
+    float f = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
+    *ms = f;
+  });
+}
+
+scendp_status scendp_kernel_stats_get(scendp_ctx* ctx, scendp_kernel_stats* s,
+                                      int32_t reset) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->sync();
+    if (s) *s = ctx->stats;
+    if (reset) ctx->stats = scendp_kernel_stats{};
+  });
+}
+
+}  // extern "C"
+
+// L2 flush: overwrite a buffer twice the L2 size.
+__global__ void scendp_flush_kernel(uint4* buf, uint64_t n16, uint32_t salt) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n16;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    buf[i] = make_uint4(salt, static_cast<uint32_t>(i), 0u, 0u);
+}
+
+extern "C" scendp_status scendp_flush_l2(scendp_ctx* ctx) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    const uint64_t bytes = uint64_t{256} << 20;
+    void* p = ctx->scratch_get(kScrFlush, bytes);
+    static uint32_t salt = 1;
+    scendp_flush_kernel<<<ctx->sm_count * 4, 512, 0, ctx->stream>>>(
+        static_cast<uint4*>(p), bytes / 16, salt++);
+    CUDA_CHECK(cudaGetLastError());
+  });
+}

@@ -1,0 +1,515 @@
+// dsirp.cu -- K3: the DSIRP order-up-to inventory DP over (customer, scenario).
+//
+// Reference (paths under /root/reference/proj):
+//   forward_pass          src/oudp.cpp:40-87    dense frontier, two scans/day
+//   pick_terminal         src/oudp.cpp:94-106   smallest state, first minimum
+//   assemble_schedule     src/oudp.cpp:108-132
+//   batched_expected_cost src/oudp.cpp:398-438  one customer, rows == H
+//   validators            src/oudp.cpp:136-207
+//
+// B200 formulation.  Starting from the single state I0, day t maps every
+// reachable state i to max(0, i-d) (no delivery) and adds exactly one new
+// state max(0, U-d) (order-up-to delivery), so at most t+1 states are
+// reachable after day t.  Each thread keeps that sparse frontier in
+// registers as slots; slot e is created on day e and all slots shift by the
+// same demand, so slot order == state order (equal states only at 0, where
+// the first strict minimum survives, exactly like the reference's ascending
+// strict-< scan into b[0]).  The delivery candidate is the first minimum over
+// (r outer, state inner) of a[i] + (F(t,r,U-i) + hold(j1,s1)), merged into the
+// no-delivery value at j1 with strict <.  Schedules are tracked forward: a
+// per-slot delivery bitmask plus one route option per day (only one delivery
+// target exists per day), then replayed from I0.
+//
+// One thread per (customer, scenario); a CTA = one customer x 128 scenarios,
+// so customer parameters are CTA-uniform (shared memory) and demand rows
+// c*H+t are coalesced 128-byte lines of the tiled layout.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+using namespace scendp_dev;
+using namespace scendp_host;
+
+namespace scendp_host {
+template <typename T>
+void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst);
+}
+
+namespace {
+
+constexpr double kInfD = __builtin_huge_val();
+constexpr int kDsirpThreads = 128;
+
+struct CustDev {
+  int32_t U, I0, H, R;
+  double h, rh;            // rh = rho * h, same rounding as the reference
+  int32_t del_tab, hold_tab;
+  uint64_t off_fixed, off_unit, off_dtable, off_htable;  // into the pool
+};
+
+struct DsirpArgs {
+  const CustDev* cust;   // [nc]
+  const double* pool;
+  uint32_t nc;
+  int32_t H;
+  uint64_t rows;         // nc * H
+  uint64_t m_wave, w_base, m_total;
+  const uint32_t* tiled; // wave-local tiled demands
+  GenParams gen;
+  double* totals;        // [nc][m_total] or null
+  uint8_t* evaluated;    // [nc][m_total] or null
+  uint8_t* deliver;      // FULL tiled [nc][m/32][H][32]
+  int32_t* quantity;
+  int32_t* end_inventory;
+  int32_t* route_option;
+  unsigned long long* agg;  // [nc][16]
+};
+
+template <int K>
+__device__ __forceinline__ double sel_d(const double (&a)[K], int idx) {
+  double r = a[0];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
+  return r;
+}
+template <int K>
+__device__ __forceinline__ uint32_t sel_u(const uint32_t (&a)[K], int idx) {
+  uint32_t r = a[0];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
+  return r;
+}
+
+template <int HMAX, bool FULL, int SRC>
+__global__ void __launch_bounds__(kDsirpThreads)
+dsirp_kernel(DsirpArgs a) {
+  constexpr int K = HMAX + 1;
+  extern __shared__ __align__(16) double s_fu[];  // fixed [H][R], unit [H][R]
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t c = blockIdx.y;
+  const CustDev cd = a.cust[c];
+  const int U = cd.U, H = cd.H, R = cd.R;
+  const int HR = H * R;
+  double* s_fixed = s_fu;
+  double* s_unit = s_fu + HR;
+  if (!cd.del_tab) {
+    for (int x = threadIdx.x; x < HR; x += blockDim.x) {
+      s_fixed[x] = a.pool[cd.off_fixed + x];
+      s_unit[x] = a.pool[cd.off_unit + x];
+    }
+  }
+  agg_cta_init(s_agg);
+  __syncthreads();
+
+  const double h = cd.h, rh = cd.rh;
+  const double* dtable = a.pool + cd.off_dtable;  // [H][U+1]
+  const double* htable = a.pool + cd.off_htable;  // [U+1]
+  const bool dtab = cd.del_tab != 0, htab = cd.hold_tab != 0;
+
+  const int tid = threadIdx.x;
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + tid;
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;
+
+  // HoldingPenaltyModel::cost (oudp.hpp:58-62): h*J + (rho*h)*s, or table[J]
+  auto hold = [&](int j, int s) -> double {
+    if (htab) return __ldg(htable + j);
+    return __dadd_rn(__dmul_rn(h, static_cast<double>(j)), __dmul_rn(rh, static_cast<double>(s)));
+  };
+
+  double total = kInfD;
+  bool ok = false;
+  if (active) {
+    // demands of this (customer, scenario)
+    int dem[HMAX];
+    const uint64_t row0 = static_cast<uint64_t>(c) * H;
+    if (SRC == 0) {
+      const uint32_t* base = a.tiled + ((wl >> 5) * a.rows + row0) * kTile + (wl & 31);
+#pragma unroll
+      for (int t = 0; t < HMAX; ++t) dem[t] = t < H ? static_cast<int>(__ldg(base + t * kTile)) : 0;
+    } else {
+      const uint64_t stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+#pragma unroll
+      for (int t = 0; t < HMAX; ++t)
+        dem[t] = t < H ? static_cast<int>(draw_counter(a.gen, stream, row0 + t)) : 0;
+    }
+
+    int st[K];
+    double vl[K];
+    uint32_t dm[K];      // FULL: delivery-day bitmask per slot
+    int opt[HMAX];       // FULL: route option of the day's delivery target
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      st[e] = 0;
+      vl[e] = kInfD;
+      dm[e] = 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < HMAX; ++t) opt[t] = 0;
+    st[0] = cd.I0;
+    vl[0] = 0.0;
+    uint64_t live = 1ull;
+
+#pragma unroll
+    for (int t = 0; t < HMAX; ++t) {
+      if (t < H) {
+        const int d = dem[t];
+        const int j1 = max(0, U - d), s1 = max(0, d - U);
+        const double hold1 = hold(j1, s1);
+        // (1) delivery: first minimum over (r, state) of a[i] + (F + hold1)
+        double bv = kInfD;
+        int br = 0, be = -1;
+        for (int r = 0; r < R; ++r) {
+          const double fx = dtab ? 0.0 : s_fixed[t * R + r];
+          const double un = dtab ? 0.0 : s_unit[t * R + r];
+#pragma unroll
+          for (int e = 0; e <= t; ++e) {
+            if (((live >> e) & 1ull) && st[e] < U) {
+              const int q = U - st[e];
+              const double F = dtab ? __ldg(dtable + t * (U + 1) + q)
+                                    : __dadd_rn(fx, __dmul_rn(un, static_cast<double>(q)));
+              const double cand = __dadd_rn(vl[e], __dadd_rn(F, hold1));
+              if (cand < bv) {
+                bv = cand;
+                br = r;
+                be = e;
+              }
+            }
+          }
+        }
+        // (2) no delivery, in place; states <= d collapse onto 0 keeping the
+        // first strict minimum
+        double b0 = kInfD;
+        int k0 = -1, tgt = -1;
+#pragma unroll
+        for (int e = 0; e <= t; ++e) {
+          if ((live >> e) & 1ull) {
+            const int i = st[e];
+            const int j = max(0, i - d), s = max(0, d - i);
+            const double nv = __dadd_rn(vl[e], hold(j, s));
+            if (i == U && j1 > 0) tgt = e;
+            st[e] = j;
+            vl[e] = nv;
+            if (i <= d) {
+              if (nv < b0) {
+                if (k0 >= 0) live &= ~(1ull << k0);
+                b0 = nv;
+                k0 = e;
+              } else {
+                live &= ~(1ull << e);
+              }
+            } else if (!(nv < kInfD)) {
+              live &= ~(1ull << e);
+            }
+          }
+        }
+        if (j1 == 0) tgt = k0;
+        // (3) merge the delivery candidate into state j1 (strict <)
+        if (be >= 0) {
+          const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
+          if (tgt >= 0) {
+            const double tv = ((live >> tgt) & 1ull) ? sel_d<K>(vl, tgt) : kInfD;
+            if (bv < tv) {
+#pragma unroll
+              for (int e = 0; e <= t; ++e) {
+                if (e == tgt) {
+                  vl[e] = bv;
+                  if (FULL) dm[e] = nm;
+                }
+              }
+              live |= 1ull << tgt;
+              if (FULL) opt[t] = br;
+            }
+          } else {
+            st[t + 1] = j1;
+            vl[t + 1] = bv;
+            live |= 1ull << (t + 1);
+            if (FULL) {
+              dm[t + 1] = nm;
+              opt[t] = br;
+            }
+          }
+        }
+      }
+    }
+    // pick_terminal: smallest state with the minimal value
+    int ts = -1;
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      if (((live >> e) & 1ull) && vl[e] < total) {
+        total = vl[e];
+        ts = e;
+      }
+    }
+    ok = ts >= 0;
+    if (!ok) total = kInfD;  // logic_error slot: evaluated = 0
+    if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
+    if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+    if (FULL) {
+      const uint32_t mask = ok ? sel_u<K>(dm, ts) : 0u;
+      const uint64_t tiles = (a.m_total + 31) / 32;
+      const uint64_t ob = ((static_cast<uint64_t>(c) * tiles + (w >> 5)) * H) * kTile + (w & 31);
+      int inv = cd.I0;
+#pragma unroll
+      for (int t = 0; t < HMAX; ++t) {
+        if (t < H) {
+          const bool z = ok && ((mask >> t) & 1u);
+          const int q = z ? U - inv : 0;
+          const int j = max(0, inv + q - dem[t]);
+          a.deliver[ob + t * kTile] = z ? 1 : 0;
+          a.quantity[ob + t * kTile] = ok ? q : 0;
+          a.end_inventory[ob + t * kTile] = ok ? j : 0;
+          a.route_option[ob + t * kTile] = z ? opt[t] : 0;
+          inv = j;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(total, ok), active);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
+}
+
+// ---- host ----------------------------------------------------------------
+void validate_customer(const scendp_customer& s, int H) {
+  if (s.capacity < 0 || s.capacity > 65535)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "capacity U must be in [0, 65535]");
+  if (s.initial_inventory < 0 || s.initial_inventory > s.capacity)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "initial inventory must be in [0, U]");
+  if (s.horizon < 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "horizon H must be >= 1");
+  if (!(s.holding >= 0.0)) fail(SCENDP_ERR_INVALID_ARGUMENT, "holding cost must be >= 0");
+  if (!(s.stockout_multiplier > 1.0))
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "stockout multiplier rho must be > 1");
+  if (s.horizon != H)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "all customers of a call must share the horizon");
+  if (s.options < 1 || s.options > 256)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "route options R must be in [1, 256]");
+  const size_t HR = static_cast<size_t>(H) * s.options;
+  if (s.delivery_tabular) {
+    if (!s.delivery_table) fail(SCENDP_ERR_INVALID_ARGUMENT, "delivery table must be H x (U+1)");
+    for (int t = 0; t < H; ++t)
+      if (s.delivery_table[static_cast<size_t>(t) * (s.capacity + 1)] != 0.0)
+        fail(SCENDP_ERR_INVALID_ARGUMENT, "delivery table requires F_t(0) = 0");
+    for (size_t x = 0; x < static_cast<size_t>(H) * (s.capacity + 1); ++x) {
+      const double v = s.delivery_table[x];
+      if (!std::isfinite(v) || v < 0.0)
+        fail(SCENDP_ERR_INVALID_ARGUMENT, "delivery table entries must be finite and >= 0");
+    }
+  } else {
+    if (!s.fixed || !s.unit)
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "delivery model needs H x R fixed and unit costs");
+    for (size_t x = 0; x < HR; ++x)
+      if (!std::isfinite(s.fixed[x]) || s.fixed[x] < 0.0 || !std::isfinite(s.unit[x]) ||
+          s.unit[x] < 0.0)
+        fail(SCENDP_ERR_INVALID_ARGUMENT, "delivery costs must be finite and >= 0");
+  }
+  if (s.holding_tabular) {
+    if (!s.holding_table) fail(SCENDP_ERR_INVALID_ARGUMENT, "holding table must have U+1 entries");
+    for (int j = 0; j <= s.capacity; ++j)
+      if (!std::isfinite(s.holding_table[j]) || s.holding_table[j] < 0.0)
+        fail(SCENDP_ERR_INVALID_ARGUMENT, "holding table entries must be finite and >= 0");
+  }
+}
+
+template <int HMAX, bool FULL, int SRC>
+void launch_dsirp(scendp_ctx* ctx, const DsirpArgs& a, size_t smem) {
+  CUDA_CHECK(cudaFuncSetAttribute(dsirp_kernel<HMAX, FULL, SRC>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem, 16))));
+  dim3 grid(static_cast<unsigned>((a.m_wave + kDsirpThreads - 1) / kDsirpThreads), a.nc);
+  const int tok = ctx->timing_begin(0);
+  dsirp_kernel<HMAX, FULL, SRC><<<grid, kDsirpThreads, smem, ctx->stream>>>(a);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->timing_end(tok);
+  ctx->count_launch();
+}
+
+template <bool FULL, int SRC>
+void dispatch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem) {
+  if (a.H <= 4) launch_dsirp<4, FULL, SRC>(ctx, a, smem);
+  else if (a.H <= 8) launch_dsirp<8, FULL, SRC>(ctx, a, smem);
+  else if (a.H <= 16) launch_dsirp<16, FULL, SRC>(ctx, a, smem);
+  else launch_dsirp<32, FULL, SRC>(ctx, a, smem);
+}
+
+}  // namespace
+
+extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_customer* customers,
+                                           uint32_t n_customers, const scendp_scenarios* sc,
+                                           uint32_t flags, const scendp_dsirp_out* out) {
+  return guard([&] {
+    if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
+    if (!customers || n_customers == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one customer");
+    if (!sc || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenarios/out is null");
+    if (n_customers > 65535) fail(SCENDP_ERR_UNSUPPORTED, "at most 65535 customers per call");
+    const int H = customers[0].horizon;
+    for (uint32_t c = 0; c < n_customers; ++c) validate_customer(customers[c], H);
+    if (sc->rows != static_cast<uint64_t>(n_customers) * H)
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario batch rows must equal customers x horizon");
+    if (H > 32) fail(SCENDP_ERR_UNSUPPORTED, "horizon H > 32 is not supported by this build");
+    const bool full = (flags & SCENDP_DSIRP_FULL) != 0;
+    if (full && (!out->deliver || !out->quantity || !out->end_inventory || !out->route_option))
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "full mode needs deliver, quantity, end_inventory, route_option");
+    const uint64_t m = sc->count;
+    const uint32_t nc = n_customers;
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+
+    // customer records + parameter pool
+    std::vector<CustDev> cds(nc);
+    std::vector<double> pool;
+    int maxR = 1;
+    for (uint32_t c = 0; c < nc; ++c) {
+      const scendp_customer& s = customers[c];
+      CustDev& d = cds[c];
+      d.U = s.capacity;
+      d.I0 = s.initial_inventory;
+      d.H = H;
+      d.R = s.options;
+      d.h = s.holding;
+      d.rh = s.stockout_multiplier * s.holding;
+      d.del_tab = s.delivery_tabular;
+      d.hold_tab = s.holding_tabular;
+      maxR = std::max(maxR, s.options);
+      const size_t HR = static_cast<size_t>(H) * s.options;
+      d.off_fixed = pool.size();
+      if (!s.delivery_tabular) pool.insert(pool.end(), s.fixed, s.fixed + HR);
+      d.off_unit = pool.size();
+      if (!s.delivery_tabular) pool.insert(pool.end(), s.unit, s.unit + HR);
+      d.off_dtable = pool.size();
+      if (s.delivery_tabular)
+        pool.insert(pool.end(), s.delivery_table, s.delivery_table + static_cast<size_t>(H) * (s.capacity + 1));
+      d.off_htable = pool.size();
+      if (s.holding_tabular) pool.insert(pool.end(), s.holding_table, s.holding_table + s.capacity + 1);
+    }
+    if (pool.empty()) pool.push_back(0.0);
+    char* dcust = static_cast<char*>(ctx->scratch_get(kScrCustomers, nc * sizeof(CustDev) + 16 + pool.size() * 8));
+    CustDev* d_cust = reinterpret_cast<CustDev*>(dcust);
+    double* d_pool = reinterpret_cast<double*>(dcust + ((nc * sizeof(CustDev) + 15) & ~size_t(15)));
+    CUDA_CHECK(cudaMemcpyAsync(d_cust, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    const size_t smem = static_cast<size_t>(H) * maxR * 2 * sizeof(double);
+
+    auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, nc * sizeof(scendp_agg_raw)));
+    CUDA_CHECK(cudaMemsetAsync(d_agg, 0, nc * sizeof(scendp_agg_raw), ctx->stream));
+
+    const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
+    const bool out_dev_ref = out->mem_kind == SCENDP_MEM_DEVICE;
+    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+    const bool dev_out = out_dev_tiled || out_dev_ref;
+    double* d_totals = nullptr;
+    uint8_t* d_eval = nullptr;
+    if (out->totals)
+      d_totals = dev_out ? out->totals : static_cast<double*>(ctx->scratch_get(kScrTotals, nc * m * 8));
+    if (out->evaluated)
+      d_eval = dev_out ? out->evaluated : static_cast<uint8_t*>(ctx->scratch_get(kScrOut5, nc * m));
+    const uint64_t tiles = (m + 31) / 32;
+    const uint64_t fcount = static_cast<uint64_t>(nc) * tiles * 32 * H;
+    uint8_t* d_dl = nullptr;
+    int32_t *d_q = nullptr, *d_ei = nullptr, *d_ro = nullptr;
+    if (full) {
+      if (out_dev_tiled) {
+        d_dl = out->deliver;
+        d_q = out->quantity;
+        d_ei = out->end_inventory;
+        d_ro = out->route_option;
+      } else {
+        d_dl = static_cast<uint8_t*>(ctx->scratch_get(kScrOut1, fcount));
+        d_q = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, fcount * 4));
+        d_ei = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, fcount * 4));
+        d_ro = static_cast<int32_t*>(ctx->scratch_get(kScrOut4, fcount * 4));
+      }
+    }
+
+    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
+    for (uint64_t w0 = 0; w0 < m; w0 += wave) {
+      const uint64_t mw = std::min(wave, m - w0);
+      scendp_scenarios sw = *sc;
+      sw.count = mw;
+      sw.first_index = sc->first_index + w0;
+      if (sc->mem_kind == SCENDP_MEM_DEVICE_TILED) sw.data = sc->data + (w0 / 32) * sc->rows * 32;
+      else if (sc->mem_kind == SCENDP_MEM_HOST || sc->mem_kind == SCENDP_MEM_DEVICE)
+        sw.data = sc->data + w0 * sc->rows;
+      GenParams gp{};
+      bool fused = false;
+      const uint32_t* tiled = stage_scenarios(ctx, &sw, true, &gp, &fused);
+      DsirpArgs a{};
+      a.cust = d_cust;
+      a.pool = d_pool;
+      a.nc = nc;
+      a.H = H;
+      a.rows = sc->rows;
+      a.m_wave = mw;
+      a.w_base = w0;
+      a.m_total = m;
+      a.tiled = tiled;
+      a.gen = gp;
+      a.totals = d_totals;
+      a.evaluated = d_eval;
+      a.deliver = d_dl;
+      a.quantity = d_q;
+      a.end_inventory = d_ei;
+      a.route_option = d_ro;
+      a.agg = d_agg;
+      if (full) {
+        if (fused) dispatch_h<true, 1>(ctx, a, smem);
+        else dispatch_h<true, 0>(ctx, a, smem);
+      } else {
+        if (fused) dispatch_h<false, 1>(ctx, a, smem);
+        else dispatch_h<false, 0>(ctx, a, smem);
+      }
+    }
+
+    ctx->allreduce_agg(d_agg, static_cast<uint64_t>(nc) * kAggWords);
+
+    if (host_out) {
+      if (out->totals)
+        CUDA_CHECK(cudaMemcpyAsync(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (out->evaluated)
+        CUDA_CHECK(cudaMemcpyAsync(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (full && !out_dev_tiled) {
+      // tiled [c][m/32][H][32] -> [c][m][H]
+      uint8_t* r_dl = out_dev_ref ? out->deliver : static_cast<uint8_t*>(ctx->scratch_get(kScrStaging, nc * m * H));
+      int32_t* r_q = out_dev_ref ? out->quantity : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, nc * m * H * 4));
+      int32_t* r_ei = out_dev_ref ? out->end_inventory : static_cast<int32_t*>(ctx->scratch_get(kScrFallback, nc * m * H * 4));
+      int32_t* r_ro = out_dev_ref ? out->route_option : static_cast<int32_t*>(ctx->scratch_get(kScrOverflow, nc * m * H * 4));
+      for (uint32_t c = 0; c < nc; ++c) {
+        const uint64_t src = static_cast<uint64_t>(c) * tiles * 32 * H;
+        const uint64_t dst = static_cast<uint64_t>(c) * m * H;
+        launch_from_tiled<uint8_t>(ctx, d_dl + src, H, m, r_dl + dst);
+        launch_from_tiled<int32_t>(ctx, d_q + src, H, m, r_q + dst);
+        launch_from_tiled<int32_t>(ctx, d_ei + src, H, m, r_ei + dst);
+        launch_from_tiled<int32_t>(ctx, d_ro + src, H, m, r_ro + dst);
+        if (m % 32 == 0) {
+          // [c][m/32][H][32] is [(c*m)/32][H][32]: one launch covered all
+          // customers only if we had passed count = nc*m; keep per-customer
+          // launches for clarity when m is ragged
+        }
+      }
+      if (host_out) {
+        CUDA_CHECK(cudaMemcpyAsync(out->deliver, r_dl, nc * m * H, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(out->quantity, r_q, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(out->end_inventory, r_ei, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(out->route_option, r_ro, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    const bool want_agg = out->agg || out->agg_raw;
+    scendp_agg_raw* h_raw = nullptr;
+    if (want_agg) {
+      h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(nc * sizeof(scendp_agg_raw)));
+      CUDA_CHECK(cudaMemcpyAsync(h_raw, d_agg, nc * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    }
+    if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
+    if (want_agg) {
+      if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, nc * sizeof(scendp_agg_raw));
+      if (out->agg) finalize_agg(h_raw, 1, nc, out->agg);
+    }
+  });
+}

@@ -1,0 +1,71 @@
+// runtime.hpp -- internal glue between the C++ drop-in facade and the C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <vector>
+
+#include "scendp/engine.hpp"
+#include "scendp/scenario.hpp"
+#include "scendp_cuda.h"
+
+namespace scendp::detail {
+
+// Map a C-ABI status to the reference's exception types (invalid_argument,
+// logic_error, runtime_error; OOM -> std::bad_alloc).
+void check(scendp_status s);
+
+// Lazily created, cached context per CUDA device (+ its call mutex).
+struct DeviceSlot {
+  scendp_ctx* ctx = nullptr;
+  std::mutex mu;
+};
+DeviceSlot& device_slot(int device);
+
+std::vector<int> devices_of(const BackendConfig& cfg);
+
+struct Shard {
+  std::size_t lo = 0, hi = 0;
+  int device = 0;
+};
+
+// Contiguous scenario ranges [g*m/G, (g+1)*m/G) per device.
+std::vector<Shard> make_shards(std::size_t m, const std::vector<int>& devs);
+
+// Run fn(shard, ctx) on every shard, one host thread per device, holding the
+// device's call mutex.  Rethrows the first exception.
+void run_shards(const std::vector<Shard>& shards,
+                const std::function<void(const Shard&, scendp_ctx*)>& fn);
+
+// BackendConfig::batch_size / memory_budget -> per-call wave size
+// (adjust_batch_size, engine.cpp:7-20); appends the reference's warning.
+std::size_t wave_size(const BackendConfig& cfg, std::size_t count,
+                      std::uint64_t per_scenario_bytes,
+                      std::vector<std::string>* warnings);
+
+scendp_dist to_c(const DistributionSpec& d);
+
+// Fixed-order aggregate of run_batched (engine.hpp:195-211).
+template <typename R, typename CostOf>
+void sequential_aggregate(BatchResultSet<R>& out, CostOf cost_of) {
+  double sum = 0.0;
+  for (std::size_t w = 0; w < out.per_scenario.size(); ++w) {
+    if (!out.evaluated[w]) continue;
+    const double c = cost_of(out.per_scenario[w]);
+    if (c < std::numeric_limits<double>::infinity()) {
+      sum += c;
+      ++out.finite_count;
+    } else {
+      ++out.infeasible_count;
+    }
+  }
+  if (out.finite_count > 0) out.mean_cost = sum / static_cast<double>(out.finite_count);
+}
+
+ExactAggregate to_exact(const scendp_agg& a);
+
+double ms_since(std::uint64_t t0_ns);
+std::uint64_t now_ns();
+
+}  // namespace scendp::detail

@@ -1,0 +1,115 @@
+// internal.hpp -- host-side context shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "scendp_cuda.h"
+
+namespace scendp_host {
+
+// Thrown inside the library, converted to a status at the C-ABI boundary.
+struct Error {
+  scendp_status status;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(scendp_status s, std::string msg) {
+  throw Error{s, std::move(msg)};
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation)
+    fail(SCENDP_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+  fail(SCENDP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_CHECK(x) ::scendp_host::cuda_check((x), #x)
+
+void set_last_error(const std::string& msg);
+
+// Named, growable device scratch buffers owned by a context.
+enum ScratchSlot {
+  kScrScenarios = 0,   // tiled scenarios (converted or generated)
+  kScrStaging,         // reference-layout staging for host/device inputs
+  kScrTours,           // per-tour position tables
+  kScrAgg,             // raw aggregates [k]
+  kScrTotals,          // per-scenario totals when the caller wants host copies
+  kScrOut1, kScrOut2, kScrOut3, kScrOut4, kScrOut5, kScrOut6,
+  kScrOverflow,        // split deque overflow list
+  kScrFallback,        // overflow-path deques
+  kScrCdf,             // poisson table
+  kScrCustomers,       // dsirp customer records
+  kScrFlush,           // L2 flush buffer
+  kScrCount
+};
+
+struct NcclApi;
+
+}  // namespace scendp_host
+
+struct scendp_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  scendp_opts opts{};
+  void* scratch[scendp_host::kScrCount] = {};
+  uint64_t scratch_bytes[scendp_host::kScrCount] = {};
+  void* agg_pinned = nullptr;       // pinned staging for raw aggregates
+  uint64_t agg_pinned_bytes = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  // kernel timing
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
+  struct Pending { int pool_index; int kind; };  // kind 0 = dp, 1 = gen
+  std::vector<Pending> pending;
+  scendp_kernel_stats stats{};
+  // multi-GPU
+  void* nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  void* scratch_get(int slot, uint64_t bytes);
+  // kernel timing helpers (no-ops unless SCENDP_CTX_KERNEL_TIMING)
+  int timing_begin(int kind);
+  void timing_end(int token);
+  void timing_resolve();  // after a stream sync
+  void count_launch(uint64_t n = 1) { stats.launches += n; }
+  void sync();
+  void allreduce_agg(void* dev_raw, uint64_t words);  // NCCL, if attached
+  void* pinned_agg(uint64_t bytes);
+};
+
+namespace scendp_host {
+
+// Finalize raw aggregates (host): combine n shard records per candidate.
+void finalize_agg(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
+                  scendp_agg* out);
+
+// C-ABI wrapper: run `f`, translate exceptions to a status.
+template <typename F>
+scendp_status guard(F&& f) {
+  try {
+    f();
+    return SCENDP_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.status;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return SCENDP_ERR_RUNTIME;
+  }
+}
+
+// Make the scenario source available on the device in the tiled layout (or
+// report that the kernel generates it).  Returns the tiled device pointer or
+// nullptr for fused generation; fills `gen` for GENERATED sources.
+struct GenParamsHost;
+const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
+                                bool allow_fused, void* gen_params_out,
+                                bool* fused);
+
+}  // namespace scendp_host

@@ -1,0 +1,313 @@
+// scengen.cu -- K4 scenario generator + HBM layout conversions.
+//
+// Reference: generate_scenario_column / generate_scenarios
+// (proj/src/scenario.cpp:92-114), DistributionSpec::sample (22-40).
+// Column w draws sequentially from SplitMix64(derive_stream(seed,
+// kStreamScenario, w)).  For uniform and poisson every value consumes exactly
+// one next(), so row r of column w is a pure function of (w, r): the kernel
+// is element-parallel and writes the tiled layout with coalesced 128-byte
+// rows.  tnormal rejection-samples a variable number of draws per value and
+// is generated sequentially per column (one thread per scenario).
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+using namespace scendp_dev;
+using namespace scendp_host;
+
+namespace {
+
+constexpr int kGenThreads = 256;
+
+// Counter-based kinds: one thread per scenario, loop over rows; a warp writes
+// one 128-byte line per row of the tiled layout.
+__global__ void __launch_bounds__(kGenThreads)
+gen_counter_kernel(GenParams g, uint64_t rows, uint64_t count, uint32_t* out) {
+  extern __shared__ double s_cdf[];
+  if (g.kind == SCENDP_DIST_POISSON) {
+    for (int k = threadIdx.x; k < g.cdf_len; k += blockDim.x) s_cdf[k] = g.cdf[k];
+    __syncthreads();
+  }
+  const uint64_t w = blockIdx.x * uint64_t(kGenThreads) + threadIdx.x;
+  if (w >= count) return;
+  const uint64_t stream = derive_stream(g.seed, kStreamScenario, g.first_index + w);
+  uint32_t* dst = out + (w >> 5) * rows * kTile + (w & 31);
+  if (g.kind == SCENDP_DIST_UNIFORM) {
+    uint64_t st = stream;
+    for (uint64_t r = 0; r < rows; ++r) {
+      const uint64_t x = mix64(st);
+      st += kGamma;
+      dst[r * kTile] = static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
+    }
+  } else {
+    uint64_t st = stream;
+    for (uint64_t r = 0; r < rows; ++r) {
+      const uint64_t x = mix64(st);
+      st += kGamma;
+      const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
+      int k = 0;
+      while (u > s_cdf[k]) ++k;
+      dst[r * kTile] = static_cast<uint32_t>(k);
+    }
+  }
+}
+
+// tnormal (scenario.cpp:30-39): Box-Muller, llround, <= 64 rejections, then
+// clamp(llround(mean)).  No FMA contraction (built with -fmad=false).
+__global__ void __launch_bounds__(kGenThreads)
+gen_tnormal_kernel(int64_t lo, int64_t hi, double mean, double stddev,
+                   uint64_t seed, uint64_t first_index, uint64_t rows,
+                   uint64_t count, uint32_t* out) {
+  const uint64_t w = blockIdx.x * uint64_t(kGenThreads) + threadIdx.x;
+  if (w >= count) return;
+  uint64_t st = derive_stream(seed, kStreamScenario, first_index + w);
+  uint32_t* dst = out + (w >> 5) * rows * kTile + (w & 31);
+  const double two_pi = 2.0 * 0x1.921fb54442d18p+1;  // 2.0 * std::numbers::pi
+  for (uint64_t r = 0; r < rows; ++r) {
+    uint32_t v = 0;
+    bool done = false;
+    for (int attempt = 0; attempt < 64 && !done; ++attempt) {
+      const uint64_t x1 = mix64(st);
+      st += kGamma;
+      const uint64_t x2 = mix64(st);
+      st += kGamma;
+      const double u1 = static_cast<double>((x1 >> 11) + 1) * 0x1.0p-53;
+      const double u2 = static_cast<double>((x2 >> 11) + 1) * 0x1.0p-53;
+      const double z = sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+      const long long rr = llround(mean + stddev * z);
+      if (rr >= lo && rr <= hi) {
+        v = static_cast<uint32_t>(rr);
+        done = true;
+      }
+    }
+    if (!done) {
+      long long rr = llround(mean);
+      rr = rr < lo ? lo : (rr > hi ? hi : rr);
+      v = static_cast<uint32_t>(rr);
+    }
+    dst[r * kTile] = v;
+  }
+}
+
+// Reference layout [count][rows] -> tiled [count/32][rows][32] (32x32 smem
+// transpose, both sides coalesced).  Element type is 4 bytes.
+template <typename T>
+__global__ void __launch_bounds__(256)
+to_tiled_kernel(const T* __restrict__ src, uint64_t rows, uint64_t count,
+                T* __restrict__ dst) {
+  __shared__ T tile[32][33];
+  const uint64_t w0 = blockIdx.x * uint64_t(32);
+  const uint64_t r0 = blockIdx.y * uint64_t(32);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int s = ty; s < 32; s += 8) {
+    const uint64_t w = w0 + s, r = r0 + tx;
+    if (w < count && r < rows) tile[s][tx] = src[w * rows + r];
+  }
+  __syncthreads();
+  for (int rr = ty; rr < 32; rr += 8) {
+    const uint64_t r = r0 + rr, w = w0 + tx;
+    if (w < count && r < rows) dst[tiled_index(w, r, rows)] = tile[tx][rr];
+  }
+}
+
+// Tiled [count/32][rows][32] -> reference [count][rows].
+template <typename T>
+__global__ void __launch_bounds__(256)
+from_tiled_kernel(const T* __restrict__ src, uint64_t rows, uint64_t count,
+                  T* __restrict__ dst) {
+  __shared__ T tile[32][33];
+  const uint64_t w0 = blockIdx.x * uint64_t(32);
+  const uint64_t r0 = blockIdx.y * uint64_t(32);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const uint64_t r = r0 + rr, w = w0 + tx;
+    if (w < count && r < rows) tile[rr][tx] = src[tiled_index(w, r, rows)];
+  }
+  __syncthreads();
+  for (int s = ty; s < 32; s += 8) {
+    const uint64_t w = w0 + s, r = r0 + tx;
+    if (w < count && r < rows) dst[w * rows + r] = tile[tx][s];
+  }
+}
+
+void check_dist(const scendp_dist* d) {
+  if (!d) fail(SCENDP_ERR_INVALID_ARGUMENT, "distribution is null");
+  if (d->lo > d->hi) fail(SCENDP_ERR_INVALID_ARGUMENT, "distribution bounds: lo > hi");
+  if (d->lo < 0)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "demands are nonnegative: lo must be >= 0");
+  if (d->hi > 0xffffffffLL)
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "demands are u32: hi must be < 2^32");
+  if (d->kind == SCENDP_DIST_TNORMAL && !(d->stddev > 0.0))
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "truncated normal: std must be > 0");
+  if (d->kind == SCENDP_DIST_POISSON) {
+    if (!(d->mean > 0.0)) fail(SCENDP_ERR_INVALID_ARGUMENT, "poisson: lambda must be > 0");
+    if (d->lo != 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "poisson: lo must be 0");
+    if (d->hi > (1 << 20)) fail(SCENDP_ERR_UNSUPPORTED, "poisson: hi must be <= 2^20");
+  }
+  if (d->kind < 0 || d->kind > 2) fail(SCENDP_ERR_INVALID_ARGUMENT, "unknown distribution kind");
+}
+
+}  // namespace
+
+namespace scendp_host {
+
+// Host CDF table, summed in index order; P[hi] = 1.
+std::vector<double> poisson_table(double lambda, int64_t hi) {
+  std::vector<double> p(static_cast<size_t>(hi) + 1);
+  double term = std::exp(-lambda), acc = 0.0;
+  for (int64_t k = 0; k <= hi; ++k) {
+    if (k > 0) term = term * lambda / static_cast<double>(k);
+    acc = acc + term;
+    p[k] = acc;
+  }
+  p[hi] = 1.0;
+  return p;
+}
+
+GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_index) {
+  check_dist(d);
+  GenParams g{};
+  g.kind = d->kind;
+  g.lo = d->lo;
+  g.span = static_cast<uint64_t>(d->hi - d->lo) + 1;
+  g.seed = d->seed;
+  g.first_index = first_index;
+  if (d->kind == SCENDP_DIST_POISSON) {
+    std::vector<double> cdf = poisson_table(d->mean, d->hi);
+    g.cdf_len = static_cast<int32_t>(cdf.size());
+    double* dev = static_cast<double*>(ctx->scratch_get(kScrCdf, cdf.size() * sizeof(double)));
+    CUDA_CHECK(cudaMemcpyAsync(dev, cdf.data(), cdf.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    g.cdf = dev;
+  }
+  return g;
+}
+
+void launch_generate_tiled(scendp_ctx* ctx, const scendp_dist* d, uint64_t rows,
+                           uint64_t w0, uint64_t count, uint32_t* out) {
+  if (count == 0) return;
+  const unsigned blocks = static_cast<unsigned>((count + kGenThreads - 1) / kGenThreads);
+  const int tok = ctx->timing_begin(1);
+  if (d->kind == SCENDP_DIST_TNORMAL) {
+    check_dist(d);
+    gen_tnormal_kernel<<<blocks, kGenThreads, 0, ctx->stream>>>(
+        d->lo, d->hi, d->mean, d->stddev, d->seed, w0, rows, count, out);
+  } else {
+    GenParams g = make_gen_params(ctx, d, w0);
+    const size_t smem = g.kind == SCENDP_DIST_POISSON ? g.cdf_len * sizeof(double) : 0;
+    if (smem > 48 * 1024)
+      CUDA_CHECK(cudaFuncSetAttribute(gen_counter_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    gen_counter_kernel<<<blocks, kGenThreads, smem, ctx->stream>>>(g, rows, count, out);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  ctx->timing_end(tok);
+  ctx->count_launch();
+}
+
+template <typename T>
+void launch_to_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst) {
+  if (count == 0 || rows == 0) return;
+  dim3 grid(static_cast<unsigned>((count + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  to_tiled_kernel<T><<<grid, 256, 0, ctx->stream>>>(src, rows, count, dst);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->count_launch();
+}
+
+template <typename T>
+void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst) {
+  if (count == 0 || rows == 0) return;
+  dim3 grid(static_cast<unsigned>((count + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  from_tiled_kernel<T><<<grid, 256, 0, ctx->stream>>>(src, rows, count, dst);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->count_launch();
+}
+
+template void launch_from_tiled<double>(scendp_ctx*, const double*, uint64_t, uint64_t, double*);
+template void launch_from_tiled<int32_t>(scendp_ctx*, const int32_t*, uint64_t, uint64_t, int32_t*);
+template void launch_from_tiled<uint8_t>(scendp_ctx*, const uint8_t*, uint64_t, uint64_t, uint8_t*);
+template void launch_from_tiled<uint32_t>(scendp_ctx*, const uint32_t*, uint64_t, uint64_t, uint32_t*);
+
+const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
+                                bool allow_fused, void* gen_params_out, bool* fused) {
+  *fused = false;
+  const uint64_t rows = sc->rows, count = sc->count;
+  const uint64_t tiled_bytes = scendp_tiled_bytes(rows, count);
+  switch (sc->mem_kind) {
+    case SCENDP_MEM_DEVICE_TILED:
+      if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
+      return sc->data;
+    case SCENDP_MEM_GENERATED: {
+      if (!sc->dist) fail(SCENDP_ERR_INVALID_ARGUMENT, "generated scenarios need a dist");
+      if (allow_fused && sc->dist->kind != SCENDP_DIST_TNORMAL) {
+        *static_cast<GenParams*>(gen_params_out) = make_gen_params(ctx, sc->dist, sc->first_index);
+        *fused = true;
+        return nullptr;
+      }
+      uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
+      launch_generate_tiled(ctx, sc->dist, rows, sc->first_index, count, dst);
+      return dst;
+    }
+    case SCENDP_MEM_HOST: {
+      if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
+      uint32_t* stg = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, rows * count * 4));
+      CUDA_CHECK(cudaMemcpyAsync(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+      uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
+      launch_to_tiled<uint32_t>(ctx, stg, rows, count, dst);
+      return dst;
+    }
+    case SCENDP_MEM_DEVICE: {
+      if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
+      uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
+      launch_to_tiled<uint32_t>(ctx, sc->data, rows, count, dst);
+      return dst;
+    }
+    default:
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "unknown scenario mem_kind");
+  }
+}
+
+}  // namespace scendp_host
+
+extern "C" {
+
+uint64_t scendp_tiled_bytes(uint64_t rows, uint64_t count) {
+  return ((count + 31) / 32) * rows * 32 * sizeof(uint32_t);
+}
+
+scendp_status scendp_gen_scenarios(scendp_ctx* ctx, const scendp_dist* dist, uint64_t rows,
+                                   uint64_t w0, uint64_t count, uint32_t layout,
+                                   uint32_t* out) {
+  return guard([&] {
+    if (!ctx || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "null ctx or output");
+    check_dist(dist);
+    if (rows == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario grid must have at least one cell");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    if (layout == SCENDP_MEM_DEVICE_TILED) {
+      launch_generate_tiled(ctx, dist, rows, w0, count, out);
+    } else if (layout == SCENDP_MEM_DEVICE) {
+      uint32_t* tmp = static_cast<uint32_t*>(
+          ctx->scratch_get(kScrScenarios, scendp_tiled_bytes(rows, count)));
+      launch_generate_tiled(ctx, dist, rows, w0, count, tmp);
+      launch_from_tiled<uint32_t>(ctx, tmp, rows, count, out);
+    } else {
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "layout must be SCENDP_MEM_DEVICE or DEVICE_TILED");
+    }
+    ctx->sync();
+  });
+}
+
+scendp_status scendp_scenarios_to_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows,
+                                        uint64_t count, uint32_t* dst) {
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    launch_to_tiled<uint32_t>(ctx, src, rows, count, dst);
+    ctx->sync();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,782 @@
+// split.cu -- K1/K2/K6: the CVRPSD split DP over scenario batches.
+//
+// Reference (paths under /root/reference/proj):
+//   fill_prefixes         src/split.cpp:24-39   (load by customer id, dist
+//                                               summed sequentially)
+//   split_core_quadratic  src/split.cpp:45-75   (penalized / forced)
+//   split_core_linear     src/split.cpp:77-118  (hard capacities)
+//   finalize_solution     src/split.cpp:120-126
+//   batched_*             src/split.cpp:303-388
+//
+// Execution model (B200): one thread per (tour, scenario); a CTA holds T
+// scenarios of one tour.  Tour-only constants (dist prefix, depot legs,
+// customer rows) are computed once on the host in the reference's order and
+// staged in shared memory; demands are read from the tiled HBM layout (one
+// 128-byte line per warp and tour position, any tour order) or generated in
+// registers (fused).  The hard-mode deque lives in a 16-entry shared-memory
+// ring per thread (occupancy <= 9 observed on every BASELINE shape); a
+// scenario whose deque would overflow is re-run by the generic fallback
+// kernel, which also serves very large n.
+//
+// Exactness: every double op is a single IEEE op in the reference's
+// association (built with -fmad=false; no FMA contraction): f(p) =
+// (V(p) + c(0,s_{p+1})) - dist[p+1], V(i) = (f(front) + dist[i]) + c(s_i,n+1),
+// penalized cand = ((f + dist[i]) + ret) + beta*(double)excess.  Ties keep
+// the earliest predecessor (strict <), as the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+using namespace scendp_dev;
+using namespace scendp_host;
+
+namespace scendp_host {
+GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_index);
+template <typename T>
+void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst);
+}  // namespace scendp_host
+
+namespace {
+
+constexpr int kRing = 16;  // deque ring entries per thread (power of two)
+constexpr double kInfD = __builtin_huge_val();
+
+enum Src { kSrcTiled = 0, kSrcGen = 1 };
+
+struct SplitArgs {
+  int32_t n;
+  int64_t Q;
+  int32_t hard;
+  int32_t linear;      // 1: deque form (hard mode), 0: quadratic form
+  double beta;
+  uint32_t k;          // tours
+  uint64_t m_wave;     // scenarios in this launch
+  uint64_t w_base;     // offset of this wave inside the call
+  uint64_t m_total;    // scenarios in the call (output stride)
+  // per-tour tables, [k][n+1]
+  const double* dist;  // dist[i], i = 0..n (dist[0] = dist[1] = 0)
+  const double* ret;   // c(s_i, n+1), i = 1..n
+  const double* c0;    // c(0, s_{i+1}), i = 0..n-1
+  const uint32_t* col; // s_i - 1, i = 1..n
+  // scenarios
+  const uint32_t* tiled;  // wave-local tiled demands (kSrcTiled)
+  GenParams gen;          // kSrcGen (first_index already includes w_base)
+  // outputs
+  double* totals;       // [k][m_total] or null
+  double* V;            // FULL, tiled [m/32][n+1][32]
+  int32_t* cuts;        // FULL, tiled
+  int32_t* route_count; // FULL, [m]
+  uint8_t* feasible;    // FULL, [m]
+  unsigned long long* agg;  // [k][16]
+  // overflow list: items (k << 40 | w_wave)
+  unsigned int* ovf_count;
+  unsigned long long* ovf_items;
+  uint32_t ovf_cap;
+};
+
+__device__ __forceinline__ uint32_t demand_at(const SplitArgs& a, int src, uint64_t stream,
+                                              const uint32_t* tile_base, uint32_t row) {
+  if (src == kSrcTiled) return __ldg(tile_base + static_cast<uint64_t>(row) * kTile);
+  return draw_counter(a.gen, stream, row);
+}
+
+// Shared memory: tour tables + per-thread rings.
+struct TourSmem {
+  double* dist;
+  double* ret;
+  double* c0;
+  uint32_t* col;
+};
+
+__device__ __forceinline__ TourSmem load_tour(const SplitArgs& a, uint32_t k, char* smem) {
+  const int n1 = a.n + 1;
+  TourSmem t;
+  t.dist = reinterpret_cast<double*>(smem);
+  t.ret = t.dist + n1;
+  t.c0 = t.ret + n1;
+  t.col = reinterpret_cast<uint32_t*>(t.c0 + n1);
+  const uint64_t off = static_cast<uint64_t>(k) * n1;
+  for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+    t.dist[i] = a.dist[off + i];
+    t.ret[i] = a.ret[off + i];
+    t.c0[i] = a.c0[off + i];
+    t.col[i] = a.col[off + i];
+  }
+  return t;
+}
+
+__host__ __device__ constexpr size_t tour_smem_bytes(int n) {
+  return static_cast<size_t>(n + 1) * (3 * sizeof(double) + sizeof(uint32_t));
+}
+
+__device__ __forceinline__ void push_overflow(const SplitArgs& a, uint32_t k, uint64_t wl) {
+  const unsigned int slot = atomicAdd(a.ovf_count, 1u);
+  if (slot < a.ovf_cap) a.ovf_items[slot] = (static_cast<unsigned long long>(k) << 40) | wl;
+}
+
+// ---------------------------------------------------------------------------
+// K1: hard capacities, O(n) monotone deque (split.cpp:77-118).
+template <bool FULL, int SRC>
+__global__ void __launch_bounds__(128)
+split_linear_kernel(SplitArgs a) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t k = blockIdx.y;
+  const int T = blockDim.x;
+  const int n = a.n;
+  TourSmem tour = load_tour(a, k, smem);
+  char* ring_base = smem + ((tour_smem_bytes(n) + 15) & ~size_t(15));
+  double* rf = reinterpret_cast<double*>(ring_base);         // [kRing][T]
+  uint32_t* rl = reinterpret_cast<uint32_t*>(rf + kRing * T);  // [kRing][T]
+  int32_t* ri = reinterpret_cast<int32_t*>(rl + kRing * T);   // FULL: [kRing][T]
+  int32_t* rr = ri + kRing * T;                               // FULL: route counts
+  agg_cta_init(s_agg);
+  __syncthreads();
+
+  const int tid = threadIdx.x;
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;  // wave-local
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;                                  // call-level
+  const uint32_t Qc = static_cast<uint32_t>(a.Q);  // host guarantees Q < 2^31
+
+  double v = 0.0;
+  bool overflow = false;
+  if (active) {
+    const uint32_t* tile_base = nullptr;
+    uint64_t stream = 0;
+    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+
+    int head = 0, tail = 0;
+    uint32_t load = 0;
+    // p = 0: f(0) = (0.0 + c(0, s_1)) - dist[1]
+    rf[tid] = (0.0 + tour.c0[0]) - tour.dist[1];
+    rl[tid] = 0u;
+    if (FULL) { ri[tid] = 0; rr[tid] = 0; }
+    tail = 1;
+    double* Vout = nullptr;
+    int32_t* Cout = nullptr;
+    if (FULL) {
+      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+      Vout = a.V + base;
+      Cout = a.cuts + base;
+      Vout[0] = 0.0;
+      Cout[0] = 0;
+    }
+    int32_t rc = 0;
+    // software prefetch of the next demands
+    uint32_t d1 = demand_at(a, SRC, stream, tile_base, tour.col[1]);
+    uint32_t d2 = n >= 2 ? demand_at(a, SRC, stream, tile_base, tour.col[2]) : 0u;
+    uint32_t d3 = n >= 3 ? demand_at(a, SRC, stream, tile_base, tour.col[3]) : 0u;
+    for (int i = 1; i <= n; ++i) {
+      const uint32_t d = d1;
+      d1 = d2;
+      d2 = d3;
+      if (i + 3 <= n) d3 = demand_at(a, SRC, stream, tile_base, tour.col[i + 3]);
+      load += d;
+      // evict predecessors whose route (p, i] exceeds Q
+      if (d > Qc) {
+        head = tail;
+      } else {
+        while (head != tail && load - rl[(head & (kRing - 1)) * T + tid] > Qc) ++head;
+      }
+      int32_t cut = -1;
+      if (head == tail) {
+        v = kInfD;
+      } else {
+        const int hs = (head & (kRing - 1)) * T + tid;
+        v = __dadd_rn(__dadd_rn(rf[hs], tour.dist[i]), tour.ret[i]);
+        if (FULL) {
+          const bool fin = v < kInfD;
+          cut = fin ? ri[hs] : -1;
+          rc = fin ? rr[hs] + 1 : 0;
+        }
+      }
+      if (FULL) {
+        Vout[static_cast<uint64_t>(i) * kTile] = v;
+        Cout[static_cast<uint64_t>(i) * kTile] = cut;
+      }
+      if (i < n) {
+        const double fi = __dsub_rn(__dadd_rn(v, tour.c0[i]), tour.dist[i + 1]);
+        // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113)
+        while (tail != head && rf[((tail - 1) & (kRing - 1)) * T + tid] > fi) --tail;
+        if (tail - head == kRing) {
+          overflow = true;
+          break;
+        }
+        const int ts = (tail & (kRing - 1)) * T + tid;
+        rf[ts] = fi;
+        rl[ts] = load;
+        if (FULL) {
+          ri[ts] = i;
+          rr[ts] = rc;
+        }
+        ++tail;
+      }
+    }
+    if (overflow) {
+      push_overflow(a, k, wl);
+    } else {
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
+      if (FULL) {
+        const bool fin = v < kInfD;
+        a.route_count[w] = fin ? rc : 0;
+        a.feasible[w] = fin ? 1 : 0;
+      }
+    }
+  }
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(v, true), active && !overflow);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
+}
+
+// ---------------------------------------------------------------------------
+// K2: O(n^2) Bellman min (split.cpp:45-75), penalized (or forced) mode.
+// Per-thread f(p) and load(p) in shared memory, [p][T] (conflict-free).
+template <bool FULL, int SRC>
+__global__ void __launch_bounds__(256)
+split_quadratic_kernel(SplitArgs a) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t k = blockIdx.y;
+  const int T = blockDim.x;
+  const int n = a.n;
+  TourSmem tour = load_tour(a, k, smem);
+  char* arr_base = smem + ((tour_smem_bytes(n) + 15) & ~size_t(15));
+  double* sf = reinterpret_cast<double*>(arr_base);        // [n][T] f(p)
+  uint32_t* sl = reinterpret_cast<uint32_t*>(sf + static_cast<size_t>(n) * T);  // [n][T]
+  int32_t* sr = reinterpret_cast<int32_t*>(sl + static_cast<size_t>(n) * T);    // FULL rc
+  agg_cta_init(s_agg);
+  __syncthreads();
+
+  const int tid = threadIdx.x;
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;
+  const bool hard = a.hard != 0;
+  const double beta = a.beta;
+  const int64_t Q = a.Q;
+
+  double v = 0.0;
+  bool overflow = false;
+  if (active) {
+    const uint32_t* tile_base = nullptr;
+    uint64_t stream = 0;
+    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+    double* Vout = nullptr;
+    int32_t* Cout = nullptr;
+    if (FULL) {
+      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+      Vout = a.V + base;
+      Cout = a.cuts + base;
+      Vout[0] = 0.0;
+      Cout[0] = 0;
+    }
+    // p = 0 entry
+    sf[tid] = __dsub_rn(__dadd_rn(0.0, tour.c0[0]), tour.dist[1]);
+    sl[tid] = 0u;
+    if (FULL) sr[tid] = 0;
+    uint32_t load = 0;
+    int32_t rc = 0;
+    uint32_t dnext = demand_at(a, SRC, stream, tile_base, tour.col[1]);
+    for (int i = 1; i <= n; ++i) {
+      const uint32_t d = dnext;
+      if (i < n) dnext = demand_at(a, SRC, stream, tile_base, tour.col[i + 1]);
+      const uint32_t nl = load + d;
+      if (nl < load) { overflow = true; break; }  // u32 load wrapped: 64-bit fallback
+      load = nl;
+      const double di = tour.dist[i];
+      const double ret = tour.ret[i];
+      double best = kInfD;
+      int32_t bestp = -1;
+      for (int p = 0; p < i; ++p) {
+        const double fp = sf[p * T + tid];
+        if (!(fp < kInfD)) continue;  // V(p) = +inf  <=>  f(p) = +inf
+        const int64_t excess = static_cast<int64_t>(load - sl[p * T + tid]) - Q;
+        double cand = __dadd_rn(__dadd_rn(fp, di), ret);
+        if (excess > 0) {
+          if (hard) continue;
+          cand = __dadd_rn(cand, __dmul_rn(beta, static_cast<double>(excess)));
+        }
+        if (cand < best) {
+          best = cand;
+          bestp = p;
+        }
+      }
+      v = best;
+      if (FULL) {
+        Vout[static_cast<uint64_t>(i) * kTile] = best;
+        Cout[static_cast<uint64_t>(i) * kTile] = bestp;
+        rc = bestp >= 0 ? sr[bestp * T + tid] + 1 : 0;
+      }
+      if (i < n) {
+        sf[i * T + tid] = __dsub_rn(__dadd_rn(best, tour.c0[i]), tour.dist[i + 1]);
+        sl[i * T + tid] = load;
+        if (FULL) sr[i * T + tid] = rc;
+      }
+    }
+    if (overflow) {
+      push_overflow(a, k, wl);
+    } else {
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
+      if (FULL) {
+        const bool fin = v < kInfD;
+        a.route_count[w] = fin ? rc : 0;
+        a.feasible[w] = fin ? 1 : 0;
+      }
+    }
+  }
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(v, true), active && !overflow);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
+}
+
+// ---------------------------------------------------------------------------
+// Generic path: one thread per item with O(n) global-memory scratch and
+// 64-bit loads -- the reference algorithm verbatim for any n, Q or demand
+// magnitude.  Items come from the overflow list (list mode) or are all
+// (tour, scenario) pairs of the wave (range mode, used for very large n).
+template <bool FULL, int SRC>
+__global__ void __launch_bounds__(64)
+split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
+                     char* scratch, uint64_t scratch_stride) {
+  __shared__ unsigned long long s_agg[kAggSlots];
+  agg_cta_init(s_agg);
+  __syncthreads();
+  const int n = a.n;
+  const uint64_t n_items = list_mode ? min(static_cast<uint64_t>(*a.ovf_count),
+                                           static_cast<uint64_t>(a.ovf_cap))
+                                     : n_range_items;
+  const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  char* my = scratch + gtid * scratch_stride;
+  double* f = reinterpret_cast<double*>(my);             // [n+1]
+  int64_t* ld = reinterpret_cast<int64_t*>(f + n + 1);    // [n+1]
+  int32_t* dq = reinterpret_cast<int32_t*>(ld + n + 1);   // [n+1]
+  int32_t* rcs = dq + n + 1;                              // [n+1]
+  // round-robin over items; every lane runs the same number of rounds so the
+  // warp-level aggregate stays convergent
+  const uint64_t rounds = (n_items + nthreads - 1) / nthreads;
+  for (uint64_t rd = 0; rd < rounds; ++rd) {
+    const uint64_t item = rd * nthreads + gtid;
+    const bool active = item < n_items;
+    double v = 0.0;
+    uint32_t k = 0;
+    if (active) {
+      uint64_t wl;
+      if (list_mode) {
+        const unsigned long long it = a.ovf_items[item];
+        k = static_cast<uint32_t>(it >> 40);
+        wl = it & ((1ULL << 40) - 1);
+      } else {
+        k = static_cast<uint32_t>(item / a.m_wave);
+        wl = item % a.m_wave;
+      }
+      const uint64_t w = a.w_base + wl;
+      const uint64_t toff = static_cast<uint64_t>(k) * (n + 1);
+      const double* dist = a.dist + toff;
+      const double* ret = a.ret + toff;
+      const double* c0 = a.c0 + toff;
+      const uint32_t* col = a.col + toff;
+      const uint32_t* tile_base = nullptr;
+      uint64_t stream = 0;
+      if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+      else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+      double* Vout = nullptr;
+      int32_t* Cout = nullptr;
+      if (FULL) {
+        const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+        Vout = a.V + base;
+        Cout = a.cuts + base;
+        Vout[0] = 0.0;
+        Cout[0] = 0;
+      }
+      ld[0] = 0;
+      for (int i = 1; i <= n; ++i)
+        ld[i] = ld[i - 1] + static_cast<int64_t>(demand_at(a, SRC, stream, tile_base, col[i]));
+      f[0] = __dsub_rn(__dadd_rn(0.0, c0[0]), dist[1]);
+      rcs[0] = 0;
+      if (a.linear) {
+        int head = 0, tail = 0;
+        dq[tail++] = 0;
+        for (int i = 1; i <= n; ++i) {
+          while (head < tail && ld[i] - ld[dq[head]] > a.Q) ++head;
+          int32_t cut = -1;
+          if (head >= tail) {
+            v = kInfD;
+            rcs[i] = 0;
+          } else {
+            const int p = dq[head];
+            v = __dadd_rn(__dadd_rn(f[p], dist[i]), ret[i]);
+            cut = v < kInfD ? p : -1;
+            rcs[i] = v < kInfD ? rcs[p] + 1 : 0;
+          }
+          if (FULL) {
+            Vout[static_cast<uint64_t>(i) * kTile] = v;
+            Cout[static_cast<uint64_t>(i) * kTile] = cut;
+          }
+          if (i < n) {
+            const double fi = __dsub_rn(__dadd_rn(v, c0[i]), dist[i + 1]);
+            while (tail > head && f[dq[tail - 1]] > fi) --tail;
+            dq[tail++] = i;
+            f[i] = fi;
+          }
+        }
+      } else {
+        for (int i = 1; i <= n; ++i) {
+          double best = kInfD;
+          int32_t bestp = -1;
+          for (int p = 0; p < i; ++p) {
+            const double fp = f[p];
+            if (!(fp < kInfD)) continue;
+            const int64_t excess = ld[i] - ld[p] - a.Q;
+            double cand = __dadd_rn(__dadd_rn(fp, dist[i]), ret[i]);
+            if (excess > 0) {
+              if (a.hard) continue;
+              cand = __dadd_rn(cand, __dmul_rn(a.beta, static_cast<double>(excess)));
+            }
+            if (cand < best) {
+              best = cand;
+              bestp = p;
+            }
+          }
+          v = best;
+          rcs[i] = bestp >= 0 ? rcs[bestp] + 1 : 0;
+          if (FULL) {
+            Vout[static_cast<uint64_t>(i) * kTile] = best;
+            Cout[static_cast<uint64_t>(i) * kTile] = bestp;
+          }
+          if (i < n) f[i] = __dsub_rn(__dadd_rn(best, c0[i]), dist[i + 1]);
+        }
+      }
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
+      if (FULL) {
+        const bool fin = v < kInfD;
+        a.route_count[w] = fin ? rcs[n] : 0;
+        a.feasible[w] = fin ? 1 : 0;
+      }
+    }
+    // per-item aggregate straight to global (items of one warp may belong to
+    // different tours; integer atomics keep the sum exact)
+    const AggPieces pc = agg_pieces(v, true);
+    if (active) {
+      unsigned long long* g = a.agg + static_cast<uint64_t>(k) * kAggWords;
+      if (pc.kind == 0) {
+        atomicAdd(g + pc.li, static_cast<unsigned long long>(pc.p0));
+        atomicAdd(g + pc.li + 1, static_cast<unsigned long long>(pc.p1));
+        if (pc.p2) atomicAdd(g + pc.li + 2, static_cast<unsigned long long>(pc.p2));
+        atomicAdd(g + 12, 1ULL);
+      } else if (pc.kind == 1) {
+        atomicAdd(g + 13, 1ULL);
+      } else if (pc.kind == 3) {
+        atomicAdd(g + 15, 1ULL);
+      }
+    }
+  }
+}
+
+// ---- host ----------------------------------------------------------------
+struct TourTables {
+  std::vector<double> dist, ret, c0;
+  std::vector<uint32_t> col;
+};
+
+void validate_instance(const scendp_routing* inst) {
+  if (!inst) fail(SCENDP_ERR_INVALID_ARGUMENT, "instance is null");
+  const int n = inst->n;
+  if (n < 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "instance needs at least one customer");
+  if (inst->capacity <= 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "capacity Q must be > 0");
+  if (!inst->costs) fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix must be (n+2) x (n+2)");
+  const size_t side = static_cast<size_t>(n) + 2;
+  for (size_t x = 0; x < side; ++x)
+    for (size_t y = 0; y < side; ++y) {
+      const double c = inst->costs[x * side + y];
+      if (!std::isfinite(c) || c < 0.0)
+        fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix entries must be finite and >= 0");
+      if (x == y && c != 0.0) fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix diagonal must be 0");
+    }
+  if (!inst->hard && !(inst->penalty_beta >= 0.0))
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "penalty beta must be >= 0");
+}
+
+void validate_tour(const int32_t* tour, int n) {
+  std::vector<char> seen(static_cast<size_t>(n) + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    const int c = tour[i];
+    if (c < 1 || c > n || seen[c])
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "tour is not a permutation of 1.." + std::to_string(n));
+    seen[c] = 1;
+  }
+}
+
+// Tour-only prefix constants, in the reference's sequential order
+// (fill_prefixes, split.cpp:24-39).
+void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, TourTables& t) {
+  const int n = inst->n, side = n + 2;
+  const size_t n1 = static_cast<size_t>(n) + 1;
+  t.dist.assign(k * n1, 0.0);
+  t.ret.assign(k * n1, 0.0);
+  t.c0.assign(k * n1, 0.0);
+  t.col.assign(k * n1, 0u);
+  const double* c = inst->costs;
+  for (uint32_t q = 0; q < k; ++q) {
+    const int32_t* s = tours + static_cast<size_t>(q) * n;
+    double* dist = t.dist.data() + q * n1;
+    dist[0] = 0.0;
+    dist[1] = 0.0;
+    for (int i = 2; i <= n; ++i) dist[i] = dist[i - 1] + c[s[i - 2] * side + s[i - 1]];
+    for (int i = 1; i <= n; ++i) {
+      t.ret[q * n1 + i] = c[s[i - 1] * side + (n + 1)];
+      t.col[q * n1 + i] = static_cast<uint32_t>(s[i - 1] - 1);
+    }
+    for (int i = 0; i < n; ++i) t.c0[q * n1 + i] = c[0 * side + s[i]];
+  }
+}
+
+constexpr int kLinearThreads = 128;
+constexpr int kMaxQuadSmem = 200 * 1024;
+constexpr int kGenericThreads = 64;
+constexpr int kGenericBlocksPerSm = 2;
+
+int quad_threads(int n) {
+  // largest multiple of 32 (<= 256) whose arrays fit in ~kMaxQuadSmem
+  const size_t per_thread = static_cast<size_t>(n) * (sizeof(double) + 2 * sizeof(uint32_t));
+  const size_t avail = kMaxQuadSmem - tour_smem_bytes(n) - 64;
+  int t = static_cast<int>(avail / per_thread / 32) * 32;
+  return std::min(t, 256);
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+}
+
+template <bool FULL, int SRC>
+void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic_scratch,
+                 uint64_t generic_stride, int generic_blocks) {
+  const int n = a.n;
+  // deque form needs Q < 2^31 (u32 window arithmetic); the quadratic form
+  // needs its per-thread arrays to fit in shared memory
+  const bool use_generic_range =
+      linear ? a.Q >= (int64_t{1} << 31) : quad_threads(n) < 32;
+  const bool small_tables = tour_smem_bytes(n) <= 48 * 1024;
+  const int tok = ctx->timing_begin(0);
+  if (use_generic_range || !small_tables) {
+    const uint64_t items = static_cast<uint64_t>(a.k) * a.m_wave;
+    split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
+        a, 0, items, generic_scratch, generic_stride);
+    CUDA_CHECK(cudaGetLastError());
+    ctx->count_launch();
+    ctx->timing_end(tok);
+    return;
+  }
+  if (linear) {
+    const int T = kLinearThreads;
+    const size_t smem = ((tour_smem_bytes(n) + 15) & ~size_t(15)) +
+                        static_cast<size_t>(kRing) * T * (FULL ? 20 : 12);
+    set_smem(split_linear_kernel<FULL, SRC>, smem);
+    dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
+    split_linear_kernel<FULL, SRC><<<grid, T, smem, ctx->stream>>>(a);
+  } else {
+    const int T = quad_threads(n);
+    const size_t smem = ((tour_smem_bytes(n) + 15) & ~size_t(15)) +
+                        static_cast<size_t>(n) * T * (sizeof(double) + 2 * sizeof(uint32_t));
+    set_smem(split_quadratic_kernel<FULL, SRC>, smem);
+    dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
+    split_quadratic_kernel<FULL, SRC><<<grid, T, smem, ctx->stream>>>(a);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  ctx->timing_end(tok);
+  ctx->count_launch();
+  // scenarios whose deque overflowed (or whose u32 load wrapped)
+  split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
+      a, 1, 0, generic_scratch, generic_stride);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->count_launch();
+}
+
+}  // namespace
+
+extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing* inst,
+                                           const int32_t* tours, uint32_t k_tours,
+                                           const scendp_scenarios* sc, uint32_t flags,
+                                           const scendp_split_out* out) {
+  return guard([&] {
+    if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
+    if (!sc || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenarios/out is null");
+    validate_instance(inst);
+    const int n = inst->n;
+    if (!tours || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one tour");
+    if (k_tours >= (1u << 23)) fail(SCENDP_ERR_UNSUPPORTED, "too many tours per call");
+    for (uint32_t q = 0; q < k_tours; ++q) validate_tour(tours + static_cast<size_t>(q) * n, n);
+    if (sc->rows != static_cast<uint64_t>(n))
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "demand column has " + std::to_string(sc->rows) +
+                                            " entries, instance has " + std::to_string(n) +
+                                            " customers");
+    const bool full = (flags & SCENDP_SPLIT_FULL) != 0;
+    if (full && k_tours != 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "full solutions need k_tours == 1");
+    if (full && (!out->values || !out->cuts || !out->route_count || !out->feasible))
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "full mode needs values, cuts, route_count, feasible");
+    if (sc->mem_kind == SCENDP_MEM_DEVICE_TILED && (sc->first_index & 31) && false)
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "tiled shards must start on a tile");
+    // hard mode follows the deque form (batched_expected_split, split.cpp:
+    // 316-318); penalized or SCENDP_QUADRATIC -> quadratic form
+    const bool linear = inst->hard && !(flags & SCENDP_QUADRATIC);
+    const uint64_t m = sc->count;
+    const uint32_t k = k_tours;
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+
+    // tour tables
+    TourTables tt;
+    build_tables(inst, tours, k, tt);
+    const size_t n1 = static_cast<size_t>(n) + 1;
+    const size_t tb = k * n1;
+    char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, tb * (3 * 8 + 4)));
+    double* d_dist = reinterpret_cast<double*>(dtab);
+    double* d_ret = d_dist + tb;
+    double* d_c0 = d_ret + tb;
+    uint32_t* d_col = reinterpret_cast<uint32_t*>(d_c0 + tb);
+    CUDA_CHECK(cudaMemcpyAsync(d_dist, tt.dist.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_ret, tt.ret.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_c0, tt.c0.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_col, tt.col.data(), tb * 4, cudaMemcpyHostToDevice, ctx->stream));
+
+    // aggregates
+    auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw)));
+    CUDA_CHECK(cudaMemsetAsync(d_agg, 0, k * sizeof(scendp_agg_raw), ctx->stream));
+
+    // outputs: device destinations (caller's device buffers when tiled/device
+    // layout matches, else scratch)
+    const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
+    const bool out_dev_ref = out->mem_kind == SCENDP_MEM_DEVICE;
+    double* d_totals = nullptr;
+    if (out->totals) {
+      d_totals = (out_dev_tiled || out_dev_ref) ? out->totals
+                                                : static_cast<double*>(ctx->scratch_get(kScrTotals, k * m * 8));
+    }
+    double* d_V = nullptr;
+    int32_t* d_cuts = nullptr;
+    int32_t* d_rc = nullptr;
+    uint8_t* d_feas = nullptr;
+    const uint64_t tiles = (m + 31) / 32;
+    if (full) {
+      if (out_dev_tiled) {
+        d_V = out->values;
+        d_cuts = out->cuts;
+      } else {
+        d_V = static_cast<double*>(ctx->scratch_get(kScrOut1, tiles * 32 * n1 * 8));
+        d_cuts = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, tiles * 32 * n1 * 4));
+      }
+      if (out_dev_tiled || out_dev_ref) {
+        d_rc = out->route_count;
+        d_feas = out->feasible;
+      } else {
+        d_rc = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, m * 4));
+        d_feas = static_cast<uint8_t*>(ctx->scratch_get(kScrOut4, m));
+      }
+    }
+
+    // overflow list + generic-path scratch
+    const uint32_t ovf_cap = 1u << 16;
+    char* ovf = static_cast<char*>(ctx->scratch_get(kScrOverflow, 16 + ovf_cap * 8ull));
+    auto* d_ovf_count = reinterpret_cast<unsigned int*>(ovf);
+    auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + 16);
+    const int generic_blocks = ctx->sm_count * kGenericBlocksPerSm;
+    const uint64_t generic_stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
+    char* gen_scratch = static_cast<char*>(
+        ctx->scratch_get(kScrFallback, generic_stride * generic_blocks * kGenericThreads));
+
+    // waves (BackendConfig::batch_size / memory_budget analogue)
+    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
+    if (wave == 0) wave = 32;
+    for (uint64_t w0 = 0; w0 < m || (m == 0 && w0 == 0); w0 += wave) {
+      if (m == 0) break;
+      const uint64_t mw = std::min(wave, m - w0);
+      scendp_scenarios sw = *sc;
+      sw.count = mw;
+      sw.first_index = sc->first_index + w0;
+      if (sc->mem_kind == SCENDP_MEM_DEVICE_TILED) sw.data = sc->data + (w0 / 32) * n * 32;
+      else if (sc->mem_kind == SCENDP_MEM_HOST || sc->mem_kind == SCENDP_MEM_DEVICE)
+        sw.data = sc->data + w0 * static_cast<uint64_t>(n);
+      GenParams gp{};
+      bool fused = false;
+      const uint32_t* tiled = stage_scenarios(ctx, &sw, true, &gp, &fused);
+      SplitArgs a{};
+      a.n = n;
+      a.Q = inst->capacity;
+      a.hard = inst->hard;
+      a.linear = linear;
+      a.beta = inst->penalty_beta;
+      a.k = k;
+      a.m_wave = mw;
+      a.w_base = w0;
+      a.m_total = m;
+      a.dist = d_dist;
+      a.ret = d_ret;
+      a.c0 = d_c0;
+      a.col = d_col;
+      a.tiled = tiled;
+      a.gen = gp;
+      a.totals = d_totals;
+      a.V = d_V;
+      a.cuts = d_cuts;
+      a.route_count = d_rc;
+      a.feasible = d_feas;
+      a.agg = d_agg;
+      a.ovf_count = d_ovf_count;
+      a.ovf_items = d_ovf_items;
+      a.ovf_cap = ovf_cap;
+      CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
+      if (full) {
+        if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        else launch_wave<true, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+      } else {
+        if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+      }
+    }
+
+    // the single collective: per-candidate raw aggregates, K x 16 u64
+    ctx->allreduce_agg(d_agg, static_cast<uint64_t>(k) * kAggWords);
+
+    // copies back
+    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+    if (out->totals && host_out)
+      CUDA_CHECK(cudaMemcpyAsync(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (full && !out_dev_tiled) {
+      // tiled -> reference layout [m][n+1]
+      double* V_ref = out_dev_ref ? out->values : static_cast<double*>(ctx->scratch_get(kScrOut5, m * n1 * 8));
+      launch_from_tiled<double>(ctx, d_V, n1, m, V_ref);
+      if (host_out) CUDA_CHECK(cudaMemcpyAsync(out->values, V_ref, m * n1 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      int32_t* C_ref = out_dev_ref ? out->cuts : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, m * n1 * 4));
+      launch_from_tiled<int32_t>(ctx, d_cuts, n1, m, C_ref);
+      if (host_out) {
+        CUDA_CHECK(cudaMemcpyAsync(out->cuts, C_ref, m * n1 * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(out->route_count, d_rc, m * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(out->feasible, d_feas, m, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    const bool want_agg = out->agg || out->agg_raw;
+    scendp_agg_raw* h_raw = nullptr;
+    if (want_agg) {
+      h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(k * sizeof(scendp_agg_raw)));
+      CUDA_CHECK(cudaMemcpyAsync(h_raw, d_agg, k * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    }
+    if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
+    if (want_agg) {
+      if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, k * sizeof(scendp_agg_raw));
+      if (out->agg) finalize_agg(h_raw, 1, k, out->agg);
+    }
+  });
+}

@@ -1,0 +1,130 @@
+"""GPU parity: DSIRP order-up-to DP (K3) against the real reference's
+batched_expected_cost (oracle/_ref) and the C restatement.
+
+Per-scenario totals and schedules (deliver, quantity, end inventory, route
+option) bit-exact; means within 1e-9 relative.  Multi-customer calls are
+checked against the composition oracle: batched_expected_cost per row slice
+[c*H, (c+1)*H).
+"""
+import numpy as np
+import pytest
+
+from oracle import Customer as OCustomer
+from oracle import UNIFORM
+from paper_2602_05179_b200 import Customer
+
+pytestmark = pytest.mark.gpu
+
+
+def random_customer(rng, U=None, H=None, R=None, integer=False, tab_hold=None, tab_del=None):
+    U = int(rng.integers(0, 120)) if U is None else U
+    H = int(rng.integers(1, 11)) if H is None else H
+    R = int(rng.integers(1, 5)) if R is None else R
+    I0 = int(rng.integers(0, U + 1))
+    if integer:
+        h, rho = float(rng.integers(1, 5)), float(rng.integers(2, 4))
+        fixed = rng.integers(0, 11, size=(H, R)).astype(float)
+        unit = rng.integers(0, 6, size=(H, R)).astype(float)
+    else:
+        h, rho = rng.random() * 2, 1.0 + rng.random() * 3
+        fixed, unit = rng.random((H, R)) * 50, rng.random((H, R)) * 2
+    tab_hold = rng.random() < 0.3 if tab_hold is None else tab_hold
+    tab_del = rng.random() < 0.2 if tab_del is None else tab_del
+    htab = rng.random(U + 1) * 10 if tab_hold else None
+    dtab = None
+    if tab_del:
+        dtab = rng.random((H, U + 1)) * 30
+        dtab[:, 0] = 0.0
+    kw = dict(U=U, I0=I0, H=H, h=h, rho=rho)
+    if dtab is not None:
+        g = Customer(**kw, delivery_table=dtab, holding_table=htab, R=R)
+        o = OCustomer(U, I0, H, h, rho, delivery_table=dtab, holding_table=htab, R=R)
+    else:
+        g = Customer(**kw, fixed=fixed, unit=unit, holding_table=htab)
+        o = OCustomer(U, I0, H, h, rho, fixed=fixed, unit=unit, holding_table=htab)
+    return g, o
+
+
+def compare_one(ctx, reference, g, o, dem):
+    got = ctx.dsirp_eval([g], dem, full=True)
+    tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, dem)
+    np.testing.assert_array_equal(got["evaluated"][0], ev)
+    np.testing.assert_array_equal(got["totals"][0], tot)
+    np.testing.assert_array_equal(got["deliver"][0], dl)
+    np.testing.assert_array_equal(got["quantity"][0], q)
+    np.testing.assert_array_equal(got["end_inventory"][0], ei)
+    np.testing.assert_array_equal(got["route_option"][0], ro)
+    a = got["agg"][0]
+    assert a["finite_count"] == fc
+    if mean is not None:
+        assert abs(a["mean"] - mean) <= 1e-9 * abs(mean) + 1e-300
+    return got
+
+
+def test_dsirp_random_instances_match_reference(ctx, reference):
+    rng = np.random.default_rng(2024)
+    for trial in range(60):
+        g, o = random_customer(rng, integer=(trial % 3 == 0))
+        m = int(rng.integers(1, 700))
+        dem = rng.integers(0, max(2, 2 * g.U // 3 + 3), size=(m, g.H)).astype(np.uint32)
+        compare_one(ctx, reference, g, o, dem)
+
+
+@pytest.mark.parametrize("H", [1, 4, 6, 8, 9, 16, 17, 32])
+def test_dsirp_horizons(ctx, reference, H):
+    rng = np.random.default_rng(H)
+    g, o = random_customer(rng, U=100, H=H, R=3)
+    dem = rng.integers(0, 40, size=(300, H)).astype(np.uint32)
+    compare_one(ctx, reference, g, o, dem)
+
+
+def test_dsirp_edge_states(ctx, reference):
+    rng = np.random.default_rng(5)
+    # U = 0 (no delivery possible), huge demands (all collapse to 0), zero demands
+    for U, lo, hi in ((0, 0, 3), (10, 20, 40), (50, 0, 1), (1, 0, 2)):
+        g, o = random_customer(rng, U=U, H=6, R=2, tab_hold=False, tab_del=False)
+        dem = rng.integers(lo, hi, size=(257, 6)).astype(np.uint32)
+        compare_one(ctx, reference, g, o, dem)
+
+
+def test_paper_golden_a4(ctx):
+    """PAPER.md App. A.4: U=2, I0=1, d=(1,1), F(q)=q, hold {0:5,1:1,2:0} -> 4."""
+    H, U = 2, 2
+    dtab = np.array([[0, 1, 2], [0, 1, 2]], np.float64)
+    g = Customer(U=U, I0=1, H=H, delivery_table=dtab, holding_table=np.array([5.0, 1.0, 0.0]))
+    got = ctx.dsirp_eval([g], np.array([[1, 1]], np.uint32), full=True)
+    assert got["totals"][0, 0] == 4.0
+    np.testing.assert_array_equal(got["deliver"][0, 0], [1, 1])
+    np.testing.assert_array_equal(got["quantity"][0, 0], [1, 1])
+
+
+def test_dsirp_multi_customer_composition(ctx, oracle, reference):
+    """rows c*H+t of one scenario column == per-customer reference calls."""
+    rng = np.random.default_rng(11)
+    nc, H, m = 12, 6, 2000
+    pairs = [random_customer(rng, U=int(rng.integers(20, 120)), H=H, R=3) for _ in range(nc)]
+    dem = oracle.generate(UNIFORM, 0, 33, 99, nc * H, m)
+    got = ctx.dsirp_eval([p[0] for p in pairs], dem, full=True)
+    for c, (g, o) in enumerate(pairs):
+        sl = np.ascontiguousarray(dem[:, c * H:(c + 1) * H])
+        tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, sl)
+        np.testing.assert_array_equal(got["totals"][c], tot)
+        np.testing.assert_array_equal(got["deliver"][c], dl)
+        np.testing.assert_array_equal(got["route_option"][c], ro)
+        np.testing.assert_array_equal(got["end_inventory"][c], ei)
+        assert abs(got["agg"][c]["mean"] - mean) <= 1e-9 * abs(mean)
+
+
+def test_dsirp_generated_matches_materialized(ctx):
+    from paper_2602_05179_b200 import Distribution
+    rng = np.random.default_rng(3)
+    nc, H, m = 5, 6, 5000
+    custs = [random_customer(rng, U=100, H=H, R=3, tab_hold=False, tab_del=False)[0]
+             for _ in range(nc)]
+    dist = Distribution("uniform", 0, 33, seed=1234)
+    buf = ctx.gen_scenarios(dist, nc * H, m)
+    a = ctx.dsirp_eval(custs, (buf, 2), count=m)
+    b = ctx.dsirp_eval(custs, dist, count=m)
+    np.testing.assert_array_equal(a["totals"], b["totals"])
+    assert a["agg"] == b["agg"]
+    buf.free()

@@ -1,0 +1,178 @@
+"""GPU parity: split evaluators (K1 linear, K2 quadratic, K6 multi-tour)
+against the real reference (oracle/_ref) and the C restatement (oracle/).
+
+Bar (BASELINE.json): per-scenario totals, V and cuts, route counts
+bit-exact; aggregate mean within 1e-9 relative (bit-exact for integer costs).
+"""
+import numpy as np
+import pytest
+
+from oracle import POISSON, TAG_SCENARIO, UNIFORM
+from paper_2602_05179_b200 import Distribution, RoutingInstance
+
+pytestmark = pytest.mark.gpu
+
+MEAN_RTOL = 1e-9
+
+
+def float_instance(n, Q, seed, hard=True, beta=0.0):
+    """random_float_instance (oracle.cpp:41-57 style): non-integral costs pin
+    the fp64 operation order."""
+    rng = np.random.default_rng(seed)
+    c = rng.random((n + 2, n + 2)) * 20.0
+    c = np.triu(c, 1)
+    c = c + c.T
+    return RoutingInstance(n, Q, hard, beta, c)
+
+
+def rand_tour(n, seed):
+    return (np.random.default_rng(seed).permutation(n) + 1).astype(np.int32)
+
+
+def check_mean(agg, ref_mean):
+    assert agg["mean"] is not None
+    assert abs(agg["mean"] - ref_mean) <= MEAN_RTOL * abs(ref_mean)
+
+
+@pytest.mark.parametrize("n,m", [(50, 1024), (200, 4096), (7, 333)])
+@pytest.mark.parametrize("costs", ["int", "float"])
+def test_split_costs_hard_matches_reference(ctx, oracle, reference, n, m, costs):
+    seed = oracle.derive_stream(1, TAG_SCENARIO, 0)
+    dem = oracle.generate(UNIFORM, 1, 10, seed, n, m)
+    if costs == "int":
+        inst = RoutingInstance(n, 100, True, 0.0, oracle.make_random_instance(n, 1))
+    else:
+        inst = float_instance(n, 100, n)
+    for tour in (np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 3)):
+        got = ctx.split_eval(inst, tour, dem)
+        ref_tot, (ref_mean, fc, ic) = reference.split_costs(n, 100, 1, 0.0, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], ref_tot)
+        a = got["agg"][0]
+        assert a["finite_count"] == fc and a["infeasible_count"] == ic
+        check_mean(a, ref_mean)
+        if costs == "int":
+            assert a["mean"] == ref_mean
+
+
+def test_split_costs_tiled_and_fused_match(ctx, oracle):
+    n, m = 200, 10_000
+    inst = RoutingInstance(n, 100, True, 0.0, oracle.make_random_instance(n, 1))
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    dist = Distribution("uniform", 1, 10, seed=oracle.derive_stream(1, TAG_SCENARIO, 0))
+    host = oracle.generate(UNIFORM, 1, 10, dist.seed, n, m)
+    want = oracle.split_batch(n, 100, 1, 0.0, inst.costs, tour, host)
+    tiled = ctx.gen_scenarios(dist, n, m)
+    got_t = ctx.split_eval(inst, tour, (tiled, 2), count=m)
+    got_g = ctx.split_eval(inst, tour, dist, count=m)
+    np.testing.assert_array_equal(got_t["totals"][0], want)
+    np.testing.assert_array_equal(got_g["totals"][0], want)
+    assert got_t["agg"][0] == got_g["agg"][0]
+    tiled.free()
+
+
+def test_split_full_matches_reference(ctx, oracle, reference):
+    n, m = 50, 1024
+    for costs in ("int", "float"):
+        inst = (RoutingInstance(n, 100, True, 0.0, oracle.make_random_instance(n, 1))
+                if costs == "int" else float_instance(n, 100, 5))
+        seed = oracle.derive_stream(2, TAG_SCENARIO, 0)
+        dem = oracle.generate(POISSON, 0, 47, seed, n, m, mean=5.0)
+        tour = rand_tour(n, 9)
+        got = ctx.split_eval(inst, tour, dem, full=True)
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+            n, 100, 1, 0.0, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
+        np.testing.assert_array_equal(got["feasible"], feas)
+        check_mean(got["agg"][0], mean)
+
+
+@pytest.mark.parametrize("n", [10, 50, 120])
+def test_split_penalized_matches_reference(ctx, oracle, reference, n):
+    m = 2048
+    seed = oracle.derive_stream(3, TAG_SCENARIO, 0)
+    dem = oracle.generate(UNIFORM, 1, 10, seed, n, m)
+    for inst in (RoutingInstance(n, 40, False, 10.0, oracle.make_random_instance(n, 4)),
+                 float_instance(n, 40, 11, hard=False, beta=2.75)):
+        tour = rand_tour(n, n)
+        got = ctx.split_eval(inst, tour, dem, full=True)
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+            n, 40, 0, inst.penalty_beta, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
+        check_mean(got["agg"][0], mean)
+
+
+def test_multi_tour_candidates_match_per_tour_calls(ctx, oracle, reference):
+    """K6: K tours in one launch == K reference calls; argmin = first min."""
+    n, m, K = 50, 1000, 33
+    inst = RoutingInstance(n, 100, False, 10.0, oracle.make_random_instance(n, 7))
+    seed = oracle.derive_stream(7, TAG_SCENARIO, 0)
+    dem = oracle.generate(UNIFORM, 1, 10, seed, n, m)
+    tours = np.stack([rand_tour(n, 100 + q) for q in range(K)])
+    tours[5] = tours[3]  # duplicate: ties resolve to the first index
+    got = ctx.split_eval(inst, tours, dem)
+    means = []
+    for q in range(K):
+        tot, (mean, fc, ic) = reference.split_costs(n, 100, 0, 10.0, inst.costs, tours[q], dem)
+        np.testing.assert_array_equal(got["totals"][q], tot)
+        assert got["agg"][q]["mean"] == mean  # integer costs -> exact
+        means.append(mean)
+    assert got["best"] == int(np.argmin(means))
+
+
+def test_edge_cases(ctx, oracle, reference):
+    # infeasible scenarios (demand > Q), zero demands (deque growth), n = 1
+    n = 30
+    inst = RoutingInstance(n, 10, True, 0.0, oracle.make_random_instance(n, 2))
+    tour = rand_tour(n, 1)
+    rng = np.random.default_rng(0)
+    dem = rng.integers(0, 4, size=(512, n)).astype(np.uint32)
+    dem[::7, 3] = 11  # > Q: infeasible
+    dem[1::5] = 0     # all-zero demand: one long window, deque overflow path
+    got = ctx.split_eval(inst, tour, dem, full=True)
+    tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+        n, 10, 1, 0.0, inst.costs, tour, dem)
+    np.testing.assert_array_equal(got["totals"][0], tot)
+    np.testing.assert_array_equal(got["V"], V)
+    np.testing.assert_array_equal(got["cuts"], cuts)
+    assert got["agg"][0]["infeasible_count"] == ic > 0
+    assert got["agg"][0]["finite_count"] == fc
+    # n = 1
+    inst1 = RoutingInstance(1, 5, True, 0.0, oracle.make_random_instance(1, 3))
+    d1 = np.array([[3], [6], [0]], np.uint32)
+    g1 = ctx.split_eval(inst1, [1], d1, full=True)
+    t1, V1, c1, *_ = reference.expected_split(1, 5, 1, 0.0, inst1.costs, np.array([1], np.int32), d1)
+    np.testing.assert_array_equal(g1["totals"][0], t1)
+    np.testing.assert_array_equal(g1["cuts"], c1)
+
+
+def test_paper_golden_a3(ctx):
+    """PAPER.md App. A.3: V = (0,4,4,8), routes [s1 s2], [s3]."""
+    c4 = np.array([[0, 1, 2, 3], [1, 0, 1, 2], [2, 1, 0, 1], [3, 2, 1, 0]], np.float64)
+    c = np.zeros((5, 5))
+    c[:4, :4] = c4
+    c[:4, 4] = [0, 3, 2, 1]
+    c[4, :4] = [0, 3, 2, 1]
+    inst = RoutingInstance(3, 5, True, 0.0, c)
+    got = ctx.split_eval(inst, [1, 2, 3], np.array([[2, 3, 4]], np.uint32), full=True)
+    np.testing.assert_array_equal(got["V"][0], [0, 4, 4, 8])
+    np.testing.assert_array_equal(got["cuts"][0], [0, 0, 0, 2])
+    assert got["route_count"][0] == 2
+
+
+def test_waves_do_not_change_results(oracle):
+    from paper_2602_05179_b200 import Context
+    n, m = 60, 3000
+    inst = RoutingInstance(n, 50, False, 3.0, oracle.make_random_instance(n, 9))
+    dem = oracle.generate(UNIFORM, 0, 12, 77, n, m)
+    tour = rand_tour(n, 4)
+    with Context(0) as a, Context(0, max_batch=96) as b:
+        ra = a.split_eval(inst, tour, dem)
+        rb = b.split_eval(inst, tour, dem)
+    np.testing.assert_array_equal(ra["totals"], rb["totals"])
+    assert ra["agg"] == rb["agg"]
