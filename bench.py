@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""bench.py -- scenario-batched DP throughput on B200 (contract in the task).
+
+Headline (BASELINE.json configs[1], "C2"): CVRPSD split, n=200, Q=100, hard
+capacities, identity giant tour, make_random_instance(200, seed=1) costs,
+uniform:1:10 demands (the reference default), 10^6 scenarios per GPU
+(weak scaling: rank r owns scenario indices [r*10^6, (r+1)*10^6)).
+
+  value  one step = one scendp_split_eval over the HBM-resident (tiled)
+         scenario set: K1 DP kernel + overflow pass (+ the NCCL all-reduce of
+         the aggregate when N > 1); device-timed with CUDA events, max over
+         ranks.  Inputs (800 MB) exceed the 126 MB L2, so no flush.
+  e2e    the reference's own benchmark call, batched_split_costs_generated
+         (saa.cpp:366-375), through the C-ABI: per step the host->device copy
+         of the step's inputs (instance/tour tables; the scenarios are the
+         distribution spec) and the device->host read of all 10^6 per-scenario
+         totals into pinned memory.  `e2e_host_batch` is the same metric with a
+         materialized host ScenarioBatch (800 MB pinned H2D per step).
+  --impl reference  the reference's own CPU implementation (oracle/_ref,
+         compiled from /root/reference sources) running the same call with all
+         host threads.
+
+Secondary lines (DSIRP C3/C4, SAA C5 candidate sweep, penalized and
+float-cost split) ride in the same JSON object under "secondary".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scenario DP evals/sec (split & DSIRP, 10^6 scen) at 1/2/4/8 B200 vs host CPU"
+UNIT = "scenario-evals/s"
+N_C2, Q_C2, M_C2 = 200, 100, 1_000_000
+TAG_SCENARIO = 0x5343454E
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--scenarios", type=int, default=M_C2, help="scenarios per GPU")
+    p.add_argument("--no-secondary", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---- distributed plumbing (gloo: barrier, id broadcast, max over ranks) -------
+class Dist:
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes) -> bytes:
+        if not self.pg:
+            return b
+        obj = [b]
+        self.pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---- clocks during the timed region --------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                try:
+                    rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        smax = max(r[1] for r in rows)
+        load = [r for r in rows if r[2] > 250.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(name: str):
+    """dram bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+# ---- reference (CPU) arm -------------------------------------------------------
+def reference_rate(m: int, threads: int, reps: int, warmup: int, budget_s: float = 60.0):
+    from oracle import UNIFORM, Reference
+    R = Reference()
+    costs = R.make_random_instance(N_C2, 1)
+    tour = np.arange(1, N_C2 + 1, dtype=np.int32)
+    seed = R.derive_stream(1, TAG_SCENARIO, 0)
+    # warm-up like run_scaling_benchmark (saa.cpp:364-368)
+    R.split_costs_generated(N_C2, Q_C2, 1, 0.0, costs, tour, UNIFORM, 1, 10, seed,
+                            min(m, 1000), threads, want_totals=False)
+    for _ in range(warmup):
+        R.split_costs_generated(N_C2, Q_C2, 1, 0.0, costs, tour, UNIFORM, 1, 10, seed, m,
+                                threads, want_totals=False)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        R.split_costs_generated(N_C2, Q_C2, 1, 0.0, costs, tour, UNIFORM, 1, 10, seed, m,
+                                threads, want_totals=True)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    return m / (sum(times) / len(times)), len(times)
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # bounded sample: the full 10^6 scenarios per step unless that would
+    # exceed ~60 s for the requested steps
+    probe, _ = reference_rate(100_000, threads, 1, 0)
+    m = args.scenarios
+    if args.steps * m / probe > 60.0:
+        m = max(10_000, int(60.0 * probe / max(1, args.steps)))
+    rate, done = reference_rate(m, threads, args.steps, min(args.warmup, 3))
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
+        "warmup": args.warmup, "ms_per_step": m / rate * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"batched_split_costs_generated, {m} scenarios per step, "
+                                   f"{threads} threads (BackendConfig::multi_thread)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {"workload": "C2: CVRPSD split n=200 Q=100 hard, identity giant tour, "
+                        "make_random_instance(200, seed=1), uniform:1:10 demands, "
+                        f"{args.scenarios} scenarios per GPU",
+            "n": N_C2, "Q": Q_C2, "scenarios_per_gpu": args.scenarios, "tours": 1,
+            "mode": "hard (linear deque)", "parallelism": f"scenario shards x{args.gpus}",
+            "l2": "inputs (4n B/scenario = 800 MB) exceed the 126 MB L2; no flush"}
+
+
+# ---- our arm -------------------------------------------------------------------
+def timed(ctx, d: Dist, fn, steps: int, warmup: int):
+    for _ in range(warmup):
+        fn()
+    ctx.sync()
+    ctx.kernel_stats(reset=True)
+    d.barrier()
+    ctx.sync()
+    ctx.timer_start()
+    for _ in range(steps):
+        fn()
+    ms = ctx.timer_stop()  # synchronizes
+    st = ctx.kernel_stats(reset=True)
+    d.barrier()
+    return d.max(ms), ms, st
+
+
+def run_ours(args, d: Dist):
+    from paper_2602_05179_b200 import (Context, Customer, Distribution, RoutingInstance,
+                                       derive_stream, make_random_instance, pinned_empty)
+    from paper_2602_05179_b200 import _capi as A
+    ctx = Context(d.local_rank, timing=True)
+    if d.world > 1:
+        uid = d.bcast_bytes(Context.nccl_unique_id() if d.rank == 0 else b"")
+        ctx.comm_init_rank(uid, d.world, d.rank)
+    hbm_peak, peak_src = peaks()
+    m = args.scenarios
+    n = N_C2
+    w0 = d.rank * m
+    inst = make_random_instance(n, 1, Q_C2, True)
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    dist = Distribution("uniform", 1, 10, seed=derive_stream(1, TAG_SCENARIO, 0))
+    scen = ctx.gen_scenarios(dist, n, m, w0=w0)          # HBM-resident, tiled
+    tot = ctx.alloc(m * 8)
+
+    def step():
+        ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m,
+                       out_kind="device_tiled", device_out={"totals": tot}, sync=False)
+
+    clocks = Clocks(d.local_rank)
+    clocks.start()
+    ms_max, ms_local, st = timed(ctx, d, step, args.steps, args.warmup)
+    clk = clocks.stop()
+    ms_step = ms_max / args.steps
+    value = d.world * m / (ms_step / 1e3)
+    k_ms = st["dp_ms"] / max(1, st["dp_launches"])
+    bytes_per_launch = m * (4 * n + 8)
+    achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
+    # correctness spot check of the timed path against the exact aggregate
+    chk = ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m, totals=False)
+
+    # ---- e2e: reference-facing call with host buffers ------------------------
+    host_tot = pinned_empty(m, np.float64)
+
+    def e2e_step():
+        ctx.split_eval(inst, tour, dist, count=m, first_index=w0, host_totals=host_tot)
+
+    e2e_steps = max(3, min(args.steps, 200))
+    e_ms_max, _, est = timed(ctx, d, e2e_step, e2e_steps, 2)
+    e2e_value = d.world * m / (e_ms_max / e2e_steps / 1e3)
+    e2e = {"value": e2e_value, "unit": UNIT,
+           "h2d_bytes_per_step": est["h2d_bytes"] // e2e_steps,
+           "d2h_bytes_per_step": est["d2h_bytes"] // e2e_steps,
+           "call": "scendp_split_eval(GENERATED uniform:1:10, host totals) == "
+                   "batched_split_costs_generated"}
+    # materialized host ScenarioBatch (reference layout, pinned)
+    ref_layout = ctx.gen_scenarios(dist, n, m, w0=w0, tiled=False)
+    host_batch = pinned_empty(m * n, np.uint32)
+    A.check(ctx.lib.scendp_memcpy(ctx.handle, host_batch.ctypes.data, ref_layout.ptr,
+                                  m * n * 4, 1, 0))
+    ref_layout.free()
+    hb = host_batch.reshape(m, n)
+
+    def host_step():
+        ctx.split_eval(inst, tour, hb, host_totals=host_tot)
+
+    h_steps = max(3, min(args.steps, 20))
+    h_ms_max, _, hst = timed(ctx, d, host_step, h_steps, 1)
+    e2e_host = {"value": d.world * m / (h_ms_max / h_steps / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": hst["h2d_bytes"] // h_steps,
+                "d2h_bytes_per_step": hst["d2h_bytes"] // h_steps,
+                "call": "scendp_split_eval(HOST ScenarioBatch) == batched_split_costs"}
+    scen_tot_check = float(np.sum(host_tot))  # keep the D2H result live
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 (exact int32 path: integral costs, bit-identical to fp64)",
+        "data": "synthetic (seeded generator, bit-identical to the reference's)",
+        "config": workload_config(args),
+        "gpu_launches": st["launches"],
+        "kernel_ms": k_ms,
+        "bellman_state_updates_per_s": value * n,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("split_linear_c2"),
+                     "kernel": "split_linear_kernel<cost-only, tiled, int32>",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "peak_source": peak_src},
+        "clocks": clk,
+        "e2e": e2e,
+        "e2e_host_batch": e2e_host,
+        "check": {"mean_cost": chk["agg"][0]["mean"], "finite": chk["agg"][0]["finite_count"],
+                  "host_totals_sum": scen_tot_check},
+    }
+    if d.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if not args.no_secondary:
+        line["secondary"] = secondary(ctx, d, args)
+    if d.rank == 0:
+        print(json.dumps(line), flush=True)
+    scen.free()
+    tot.free()
+    ctx.close()
+
+
+def cpu_baseline():
+    threads = os.cpu_count() or 1
+    try:
+        rate, reps = reference_rate(M_C2, threads, 20, 1, budget_s=15.0)
+        rate1, _ = reference_rate(50_000, 1, 3, 0, budget_s=10.0)
+    except Exception as e:  # reference library missing on this box
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"batched_split_costs_generated C2, {M_C2} scenarios x {reps} reps, "
+                      f"{threads} threads",
+            "single_thread_value": rate1}
+
+
+def secondary(ctx, d: Dist, args):
+    from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance, make_random_instance
+    from paper_2602_05179_b200 import _capi as A
+    out = {}
+    hbm_peak, _ = peaks()
+    n = N_C2
+
+    def kernel_rate(fn, steps, warm=2):
+        ms_max, ms, st = timed(ctx, d, fn, steps, warm)
+        return ms_max / steps, st["dp_ms"] / max(1, st["dp_launches"])
+
+    # float-cost twin of C2 (pure fp64 path) and full solutions
+    m = min(args.scenarios, 1_000_000)
+    dist = Distribution("uniform", 1, 10, seed=77)
+    scen = ctx.gen_scenarios(dist, n, m, w0=d.rank * m)
+    tot = ctx.alloc(m * 8)
+    rng = np.random.default_rng(1)
+    c = rng.random((n + 2, n + 2)) * 20.0
+    c = np.triu(c, 1)
+    c = c + c.T
+    finst = RoutingInstance(n, Q_C2, True, 0.0, c)
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
+        finst, tour, (scen, A.MEM_DEVICE_TILED), count=m, out_kind="device_tiled",
+        device_out={"totals": tot}, sync=False), 50)
+    out["split_c2_float_costs"] = {"value": d.world * m / (step_ms / 1e3), "unit": UNIT,
+                                   "kernel_ms": k_ms, "dtype": "f64",
+                                   "roofline_frac": m * (4 * n + 8) / (k_ms / 1e3) / 1e9 / hbm_peak}
+    iinst = make_random_instance(n, 1, Q_C2, True)
+    V = ctx.alloc(ctx.tiled_bytes(n + 1, m) * 2)
+    cuts = ctx.alloc(ctx.tiled_bytes(n + 1, m))
+    rc = ctx.alloc(m * 4)
+    fe = ctx.alloc(m)
+    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
+        iinst, tour, (scen, A.MEM_DEVICE_TILED), count=m, full=True, out_kind="device_tiled",
+        device_out={"totals": tot, "values": V, "cuts": cuts, "route_count": rc, "feasible": fe},
+        sync=False), 10)
+    out["split_c2_full_solution"] = {
+        "value": d.world * m / (step_ms / 1e3), "unit": UNIT, "kernel_ms": k_ms,
+        "roofline_frac": m * (4 * n + 8 + 12 * (n + 1)) / (k_ms / 1e3) / 1e9 / hbm_peak}
+    for b in (V, cuts, rc, fe):
+        b.free()
+    # penalized split (quadratic, FP64-bound), n = 200 and the SAA shape n = 50
+    pinst = make_random_instance(n, 1, Q_C2, False, 10.0)
+    mp = min(m, 200_000)
+    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
+        pinst, tour, (scen, A.MEM_DEVICE_TILED), count=mp, out_kind="device_tiled",
+        device_out={"totals": tot}, sync=False), 2, 1)
+    out["split_c2_penalized"] = {"value": d.world * mp / (step_ms / 1e3), "unit": UNIT,
+                                 "kernel_ms": k_ms, "scenarios": mp,
+                                 "dense_candidates_per_s": d.world * mp * n * (n + 1) / 2 / (step_ms / 1e3)}
+    scen.free()
+    tot.free()
+
+    # C5: 1000 giant tours x 10^5 scenarios, n = 50, penalized beta = 10, one launch
+    n5, m5, K5 = 50, 100_000, 1000
+    inst5 = make_random_instance(n5, 5, Q_C2, False, 10.0)
+    rng = np.random.default_rng(5)
+    tours5 = np.stack([rng.permutation(n5) + 1 for _ in range(K5)]).astype(np.int32)
+    scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, m5, w0=d.rank * m5)
+    res = {}
+
+    def c5():
+        res["r"] = ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=m5,
+                                  totals=False)
+
+    step_ms, k_ms = kernel_rate(c5, 2, 1)
+    out["saa_c5_candidates"] = {
+        "value": d.world * K5 * m5 / (step_ms / 1e3), "unit": "(tour, scenario)-evals/s",
+        "candidates_per_s": K5 / (step_ms / 1e3), "ms_per_launch": step_ms, "kernel_ms": k_ms,
+        "best_tour": res["r"]["best"], "config": "K=1000 tours x 1e5 scenarios, n=50, beta=10"}
+    scen5.free()
+
+    # DSIRP C3 (50 customers, H=6, 1e5) and C4 (200 customers, H=6, 1e6)
+    for name, nc, m3, steps in (("dsirp_c3", 50, 100_000, 20), ("dsirp_c4", 200, 1_000_000, 3)):
+        m3 = m3 // d.world if name == "dsirp_c4" else m3
+        H = 6
+        custs = [Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
+                          fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                          unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
+        sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m3,
+                               w0=d.rank * m3)
+        t3 = ctx.alloc(nc * m3 * 8)
+        step_ms, k_ms = kernel_rate(lambda: ctx.dsirp_eval(
+            custs, (sc, A.MEM_DEVICE_TILED), count=m3, out_kind="device_tiled",
+            device_out={"totals": t3}, sync=False), steps)
+        units = d.world * nc * m3
+        out[name] = {"value": units / (step_ms / 1e3), "unit": "(customer, scenario)-evals/s",
+                     "kernel_ms": k_ms, "customers": nc, "scenarios": d.world * m3,
+                     "bellman_state_updates_per_s": units * H * 101 / (step_ms / 1e3),
+                     "roofline_frac": nc * m3 * 32 / (k_ms / 1e3) / 1e9 / hbm_peak,
+                     "scaling": "strong" if name == "dsirp_c4" else "weak"}
+        sc.free()
+        t3.free()
+    return out
+
+
+def main():
+    args = parse()
+    d = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, d)
+        else:
+            run_ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

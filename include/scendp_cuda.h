@@ -290,6 +290,8 @@ typedef struct {
   double dp_ms;             /* summed event time of the DP kernels */
   uint64_t gen_launches;
   double gen_ms;
+  uint64_t h2d_bytes;       /* bytes this library copied host->device */
+  uint64_t d2h_bytes;       /* bytes this library copied device->host */
 } scendp_kernel_stats;
 scendp_status scendp_kernel_stats_get(scendp_ctx* ctx, scendp_kernel_stats* s,
                                       int32_t reset);

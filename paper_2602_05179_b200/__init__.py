@@ -265,7 +265,8 @@ class Context:
     def split_eval(self, inst: RoutingInstance, tours, scenarios, count: Optional[int] = None,
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    quadratic: bool = False, out_kind: str = "host",
-                   device_out: Optional[dict] = None, sync: bool = True) -> dict:
+                   device_out: Optional[dict] = None, sync: bool = True,
+                   host_totals: Optional[np.ndarray] = None) -> dict:
         """Evaluate tours (k x n, 1-based ids) on a scenario set.
 
         Returns totals [k][m] (host), V/cuts [m][n+1], route_count, feasible
@@ -285,7 +286,8 @@ class Context:
         if out_kind == "host":
             o = A.SplitOut(A.MEM_HOST, None, None, None, None, None, agg, None)
             if totals:
-                res["totals"] = np.empty((k, m), np.float64)
+                res["totals"] = (host_totals.reshape(k, m) if host_totals is not None
+                                 else np.empty((k, m), np.float64))
                 o.totals = res["totals"].ctypes.data
             if full:
                 res["V"] = np.empty((m, n + 1), np.float64)
@@ -360,7 +362,8 @@ class Context:
         s = A.KernelStats()
         A.check(self.lib.scendp_kernel_stats_get(self.handle, C.byref(s), 1 if reset else 0))
         return {"launches": s.launches, "dp_launches": s.dp_launches, "dp_ms": s.dp_ms,
-                "gen_launches": s.gen_launches, "gen_ms": s.gen_ms}
+                "gen_launches": s.gen_launches, "gen_ms": s.gen_ms,
+                "h2d_bytes": s.h2d_bytes, "d2h_bytes": s.d2h_bytes}
 
     def flush_l2(self):
         A.check(self.lib.scendp_flush_l2(self.handle))
@@ -379,6 +382,16 @@ class Context:
 
     def comm_destroy(self):
         A.check(self.lib.scendp_comm_destroy(self.handle))
+
+
+def pinned_empty(count: int, dtype) -> np.ndarray:
+    """numpy view of page-locked host memory (cudaMallocHost); freed at exit."""
+    lib = A.load()
+    dt = np.dtype(dtype)
+    p = C.c_void_p()
+    A.check(lib.scendp_host_alloc_pinned(max(1, count * dt.itemsize), C.byref(p)))
+    buf = (C.c_char * (count * dt.itemsize)).from_address(p.value)
+    return np.frombuffer(buf, dtype=dt, count=count)
 
 
 def agg_finalize(raws: List[A.AggRaw], k: int) -> List[dict]:

@@ -90,7 +90,8 @@ class DsirpOut(C.Structure):
 
 class KernelStats(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("dp_launches", C.c_uint64), ("dp_ms", C.c_double),
-                ("gen_launches", C.c_uint64), ("gen_ms", C.c_double)]
+                ("gen_launches", C.c_uint64), ("gen_ms", C.c_double),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 # Every symbol include/scendp_cuda.h declares, with its ctypes signature.

@@ -307,7 +307,7 @@ scendp_status scendp_memcpy(scendp_ctx* ctx, void* dst, const void* src,
     const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
                              : kind == 1 ? cudaMemcpyDeviceToHost
                                          : cudaMemcpyDeviceToDevice;
-    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream));
+    ctx->copy(dst, src, bytes, k);
     if (!(flags & SCENDP_ASYNC)) ctx->sync();
   });
 }

@@ -391,8 +391,8 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     char* dcust = static_cast<char*>(ctx->scratch_get(kScrCustomers, nc * sizeof(CustDev) + 16 + pool.size() * 8));
     CustDev* d_cust = reinterpret_cast<CustDev*>(dcust);
     double* d_pool = reinterpret_cast<double*>(dcust + ((nc * sizeof(CustDev) + 15) & ~size_t(15)));
-    CUDA_CHECK(cudaMemcpyAsync(d_cust, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->copy(d_cust, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice);
+    ctx->copy(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice);
     const size_t smem = static_cast<size_t>(H) * maxR * 2 * sizeof(double);
 
     auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, nc * sizeof(scendp_agg_raw)));
@@ -469,9 +469,9 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
 
     if (host_out) {
       if (out->totals)
-        CUDA_CHECK(cudaMemcpyAsync(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->copy(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost);
       if (out->evaluated)
-        CUDA_CHECK(cudaMemcpyAsync(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->copy(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost);
     }
     if (full && !out_dev_tiled) {
       // tiled [c][m/32][H][32] -> [c][m][H]
@@ -493,18 +493,17 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
         }
       }
       if (host_out) {
-        CUDA_CHECK(cudaMemcpyAsync(out->deliver, r_dl, nc * m * H, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(out->quantity, r_q, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(out->end_inventory, r_ei, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(out->route_option, r_ro, nc * m * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->copy(out->deliver, r_dl, nc * m * H, cudaMemcpyDeviceToHost);
+        ctx->copy(out->quantity, r_q, nc * m * H * 4, cudaMemcpyDeviceToHost);
+        ctx->copy(out->end_inventory, r_ei, nc * m * H * 4, cudaMemcpyDeviceToHost);
+        ctx->copy(out->route_option, r_ro, nc * m * H * 4, cudaMemcpyDeviceToHost);
       }
     }
     const bool want_agg = out->agg || out->agg_raw;
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
       h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(nc * sizeof(scendp_agg_raw)));
-      CUDA_CHECK(cudaMemcpyAsync(h_raw, d_agg, nc * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+      ctx->copy(h_raw, d_agg, nc * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost);
     }
     if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
     if (want_agg) {

@@ -78,6 +78,13 @@ struct scendp_ctx {
   void timing_end(int token);
   void timing_resolve();  // after a stream sync
   void count_launch(uint64_t n = 1) { stats.launches += n; }
+  // stream-ordered copy with H2D / D2H byte accounting (bench e2e bytes)
+  void copy(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind) {
+    if (bytes == 0) return;
+    scendp_host::cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, stream), "cudaMemcpyAsync");
+    if (kind == cudaMemcpyHostToDevice) stats.h2d_bytes += bytes;
+    else if (kind == cudaMemcpyDeviceToHost) stats.d2h_bytes += bytes;
+  }
   void sync();
   void allreduce_agg(void* dev_raw, uint64_t words);  // NCCL, if attached
   void* pinned_agg(uint64_t bytes);

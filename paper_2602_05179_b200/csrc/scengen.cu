@@ -178,8 +178,7 @@ GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_
     std::vector<double> cdf = poisson_table(d->mean, d->hi);
     g.cdf_len = static_cast<int32_t>(cdf.size());
     double* dev = static_cast<double*>(ctx->scratch_get(kScrCdf, cdf.size() * sizeof(double)));
-    CUDA_CHECK(cudaMemcpyAsync(dev, cdf.data(), cdf.size() * sizeof(double),
-                               cudaMemcpyHostToDevice, ctx->stream));
+    ctx->copy(dev, cdf.data(), cdf.size() * sizeof(double), cudaMemcpyHostToDevice);
     g.cdf = dev;
   }
   return g;
@@ -254,8 +253,7 @@ const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
     case SCENDP_MEM_HOST: {
       if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
       uint32_t* stg = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, rows * count * 4));
-      CUDA_CHECK(cudaMemcpyAsync(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice,
-                                 ctx->stream));
+      ctx->copy(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice);
       uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
       launch_to_tiled<uint32_t>(ctx, stg, rows, count, dst);
       return dst;

@@ -25,6 +25,7 @@
 // the earliest predecessor (strict <), as the reference.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -64,6 +65,13 @@ struct SplitArgs {
   const double* ret;   // c(s_i, n+1), i = 1..n
   const double* c0;    // c(0, s_{i+1}), i = 0..n-1
   const uint32_t* col; // s_i - 1, i = 1..n
+  // K1 chunked tables, [k][npad] per row; slot s = position s+1
+  int32_t npad;
+  const uint32_t* ccol;  // customer row of position s+1
+  const int32_t* itab;   // [k][2][npad]: A = dist+ret, B = c0 - dist_next (int path)
+  const double* dtab;    // [k][4][npad]: dist, ret, c0, dist_next
+  const double* f0d;     // [k] f(0) = (0.0 + c(0,s_1)) - dist[1]
+  const int32_t* f0i;    // [k] same, integer path
   // scenarios
   const uint32_t* tiled;  // wave-local tiled demands (kSrcTiled)
   GenParams gen;          // kSrcGen (first_index already includes w_base)
@@ -120,122 +128,7 @@ __device__ __forceinline__ void push_overflow(const SplitArgs& a, uint32_t k, ui
   if (slot < a.ovf_cap) a.ovf_items[slot] = (static_cast<unsigned long long>(k) << 40) | wl;
 }
 
-// ---------------------------------------------------------------------------
-// K1: hard capacities, O(n) monotone deque (split.cpp:77-118).
-template <bool FULL, int SRC>
-__global__ void __launch_bounds__(128)
-split_linear_kernel(SplitArgs a) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ unsigned long long s_agg[kAggSlots];
-  const uint32_t k = blockIdx.y;
-  const int T = blockDim.x;
-  const int n = a.n;
-  TourSmem tour = load_tour(a, k, smem);
-  char* ring_base = smem + ((tour_smem_bytes(n) + 15) & ~size_t(15));
-  double* rf = reinterpret_cast<double*>(ring_base);         // [kRing][T]
-  uint32_t* rl = reinterpret_cast<uint32_t*>(rf + kRing * T);  // [kRing][T]
-  int32_t* ri = reinterpret_cast<int32_t*>(rl + kRing * T);   // FULL: [kRing][T]
-  int32_t* rr = ri + kRing * T;                               // FULL: route counts
-  agg_cta_init(s_agg);
-  __syncthreads();
-
-  const int tid = threadIdx.x;
-  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;  // wave-local
-  const bool active = wl < a.m_wave;
-  const uint64_t w = a.w_base + wl;                                  // call-level
-  const uint32_t Qc = static_cast<uint32_t>(a.Q);  // host guarantees Q < 2^31
-
-  double v = 0.0;
-  bool overflow = false;
-  if (active) {
-    const uint32_t* tile_base = nullptr;
-    uint64_t stream = 0;
-    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
-    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
-
-    int head = 0, tail = 0;
-    uint32_t load = 0;
-    // p = 0: f(0) = (0.0 + c(0, s_1)) - dist[1]
-    rf[tid] = (0.0 + tour.c0[0]) - tour.dist[1];
-    rl[tid] = 0u;
-    if (FULL) { ri[tid] = 0; rr[tid] = 0; }
-    tail = 1;
-    double* Vout = nullptr;
-    int32_t* Cout = nullptr;
-    if (FULL) {
-      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
-      Vout = a.V + base;
-      Cout = a.cuts + base;
-      Vout[0] = 0.0;
-      Cout[0] = 0;
-    }
-    int32_t rc = 0;
-    // software prefetch of the next demands
-    uint32_t d1 = demand_at(a, SRC, stream, tile_base, tour.col[1]);
-    uint32_t d2 = n >= 2 ? demand_at(a, SRC, stream, tile_base, tour.col[2]) : 0u;
-    uint32_t d3 = n >= 3 ? demand_at(a, SRC, stream, tile_base, tour.col[3]) : 0u;
-    for (int i = 1; i <= n; ++i) {
-      const uint32_t d = d1;
-      d1 = d2;
-      d2 = d3;
-      if (i + 3 <= n) d3 = demand_at(a, SRC, stream, tile_base, tour.col[i + 3]);
-      load += d;
-      // evict predecessors whose route (p, i] exceeds Q
-      if (d > Qc) {
-        head = tail;
-      } else {
-        while (head != tail && load - rl[(head & (kRing - 1)) * T + tid] > Qc) ++head;
-      }
-      int32_t cut = -1;
-      if (head == tail) {
-        v = kInfD;
-      } else {
-        const int hs = (head & (kRing - 1)) * T + tid;
-        v = __dadd_rn(__dadd_rn(rf[hs], tour.dist[i]), tour.ret[i]);
-        if (FULL) {
-          const bool fin = v < kInfD;
-          cut = fin ? ri[hs] : -1;
-          rc = fin ? rr[hs] + 1 : 0;
-        }
-      }
-      if (FULL) {
-        Vout[static_cast<uint64_t>(i) * kTile] = v;
-        Cout[static_cast<uint64_t>(i) * kTile] = cut;
-      }
-      if (i < n) {
-        const double fi = __dsub_rn(__dadd_rn(v, tour.c0[i]), tour.dist[i + 1]);
-        // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113)
-        while (tail != head && rf[((tail - 1) & (kRing - 1)) * T + tid] > fi) --tail;
-        if (tail - head == kRing) {
-          overflow = true;
-          break;
-        }
-        const int ts = (tail & (kRing - 1)) * T + tid;
-        rf[ts] = fi;
-        rl[ts] = load;
-        if (FULL) {
-          ri[ts] = i;
-          rr[ts] = rc;
-        }
-        ++tail;
-      }
-    }
-    if (overflow) {
-      push_overflow(a, k, wl);
-    } else {
-      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
-      if (FULL) {
-        const bool fin = v < kInfD;
-        a.route_count[w] = fin ? rc : 0;
-        a.feasible[w] = fin ? 1 : 0;
-      }
-    }
-  }
-  __syncwarp();
-  agg_warp_add(s_agg, agg_pieces(v, true), active && !overflow);
-  __syncthreads();
-  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
-}
+#include "split_linear.cuh"
 
 // ---------------------------------------------------------------------------
 // K2: O(n^2) Bellman min (split.cpp:45-75), penalized (or forced) mode.
@@ -488,6 +381,12 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
 struct TourTables {
   std::vector<double> dist, ret, c0;
   std::vector<uint32_t> col;
+  // K1 chunked tables
+  int npad = 0;
+  bool intv = false;  // every tour admits the exact integer path
+  std::vector<uint32_t> ccol;
+  std::vector<int32_t> itab, f0i;
+  std::vector<double> dtab, f0d;
 };
 
 void validate_instance(const scendp_routing* inst) {
@@ -540,9 +439,58 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, 
     }
     for (int i = 0; i < n; ++i) t.c0[q * n1 + i] = c[0 * side + s[i]];
   }
+  // chunked K1 tables (slot s = position s+1) and the integer-path check:
+  // all tour costs integral and every partial sum < 2^29, so each fp64 op of
+  // the reference is exact and integer adds reproduce it bit for bit.
+  const int npad = ((n + 3) / 4) * 4 + 4;
+  t.npad = npad;
+  t.ccol.assign(static_cast<size_t>(k) * npad, 0u);
+  t.itab.assign(static_cast<size_t>(k) * 2 * npad, 0);
+  t.dtab.assign(static_cast<size_t>(k) * 4 * npad, 0.0);
+  t.f0d.assign(k, 0.0);
+  t.f0i.assign(k, 0);
+  bool intv = true;
+  for (uint32_t q = 0; q < k; ++q) {
+    const double* dist = t.dist.data() + q * n1;
+    const double* ret = t.ret.data() + q * n1;
+    const double* c0 = t.c0.data() + q * n1;
+    double bound = dist[n], cmax = 0.0;
+    bool integral = true;
+    for (int i = 0; i <= n; ++i) {
+      integral &= std::floor(dist[i]) == dist[i] && std::floor(ret[i]) == ret[i] &&
+                  std::floor(c0[i]) == c0[i];
+      bound += ret[i] + c0[i];
+      cmax = std::max(cmax, c0[i]);
+    }
+    bound += cmax;
+    intv &= integral && bound < static_cast<double>(1 << 29);
+    t.f0d[q] = (0.0 + c0[0]) - dist[1];
+    for (int i = 1; i <= n; ++i) {
+      const size_t sidx = static_cast<size_t>(i - 1);
+      t.ccol[q * npad + sidx] = t.col[q * n1 + i];
+      double* dt = t.dtab.data() + static_cast<size_t>(q) * 4 * npad;
+      dt[0 * npad + sidx] = dist[i];
+      dt[1 * npad + sidx] = ret[i];
+      dt[2 * npad + sidx] = c0[i];
+      dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
+    }
+  }
+  t.intv = intv;
+  if (intv) {
+    for (uint32_t q = 0; q < k; ++q) {
+      const double* dist = t.dist.data() + q * n1;
+      const double* ret = t.ret.data() + q * n1;
+      const double* c0 = t.c0.data() + q * n1;
+      t.f0i[q] = static_cast<int32_t>(t.f0d[q]);
+      int32_t* it = t.itab.data() + static_cast<size_t>(q) * 2 * npad;
+      for (int i = 1; i <= n; ++i) {
+        it[0 * npad + (i - 1)] = static_cast<int32_t>(dist[i] + ret[i]);
+        it[1 * npad + (i - 1)] = i < n ? static_cast<int32_t>(c0[i] - dist[i + 1]) : 0;
+      }
+    }
+  }
 }
 
-constexpr int kLinearThreads = 128;
 constexpr int kMaxQuadSmem = 200 * 1024;
 constexpr int kGenericThreads = 64;
 constexpr int kGenericBlocksPerSm = 2;
@@ -569,7 +517,8 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   // needs its per-thread arrays to fit in shared memory
   const bool use_generic_range =
       linear ? a.Q >= (int64_t{1} << 31) : quad_threads(n) < 32;
-  const bool small_tables = tour_smem_bytes(n) <= 48 * 1024;
+  const bool small_tables = tour_smem_bytes(n) <= 48 * 1024 &&
+                            static_cast<size_t>(a.npad) * 36 <= 96 * 1024;
   const int tok = ctx->timing_begin(0);
   if (use_generic_range || !small_tables) {
     const uint64_t items = static_cast<uint64_t>(a.k) * a.m_wave;
@@ -581,12 +530,19 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     return;
   }
   if (linear) {
-    const int T = kLinearThreads;
-    const size_t smem = ((tour_smem_bytes(n) + 15) & ~size_t(15)) +
-                        static_cast<size_t>(kRing) * T * (FULL ? 20 : 12);
-    set_smem(split_linear_kernel<FULL, SRC>, smem);
+    const int T = kK1Threads;
+    const bool intv = a.itab != nullptr;
+    const size_t vt = intv ? 4 : 8;
+    const size_t smem = static_cast<size_t>(a.npad) * (4 + (intv ? 2 : 4) * vt) +
+                        static_cast<size_t>(kRing) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
-    split_linear_kernel<FULL, SRC><<<grid, T, smem, ctx->stream>>>(a);
+    if (intv) {
+      set_smem(split_linear_kernel<FULL, SRC, true>, smem);
+      split_linear_kernel<FULL, SRC, true><<<grid, T, smem, ctx->stream>>>(a);
+    } else {
+      set_smem(split_linear_kernel<FULL, SRC, false>, smem);
+      split_linear_kernel<FULL, SRC, false><<<grid, T, smem, ctx->stream>>>(a);
+    }
   } else {
     const int T = quad_threads(n);
     const size_t smem = ((tour_smem_bytes(n) + 15) & ~size_t(15)) +
@@ -640,16 +596,29 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     TourTables tt;
     build_tables(inst, tours, k, tt);
     const size_t n1 = static_cast<size_t>(n) + 1;
-    const size_t tb = k * n1;
-    char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, tb * (3 * 8 + 4)));
-    double* d_dist = reinterpret_cast<double*>(dtab);
-    double* d_ret = d_dist + tb;
-    double* d_c0 = d_ret + tb;
-    uint32_t* d_col = reinterpret_cast<uint32_t*>(d_c0 + tb);
-    CUDA_CHECK(cudaMemcpyAsync(d_dist, tt.dist.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(d_ret, tt.ret.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(d_c0, tt.c0.data(), tb * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(d_col, tt.col.data(), tb * 4, cudaMemcpyHostToDevice, ctx->stream));
+    // one staging blob -> one H2D copy; sections 16-byte aligned
+    std::vector<char> blob;
+    auto put = [&blob](const void* src, size_t bytes) {
+      const size_t off = (blob.size() + 15) & ~size_t(15);
+      blob.resize(off + bytes);
+      if (bytes) std::memcpy(blob.data() + off, src, bytes);
+      return off;
+    };
+    const size_t o_dist = put(tt.dist.data(), tt.dist.size() * 8);
+    const size_t o_ret = put(tt.ret.data(), tt.ret.size() * 8);
+    const size_t o_c0 = put(tt.c0.data(), tt.c0.size() * 8);
+    const size_t o_col = put(tt.col.data(), tt.col.size() * 4);
+    const size_t o_ccol = put(tt.ccol.data(), tt.ccol.size() * 4);
+    const size_t o_itab = put(tt.itab.data(), tt.itab.size() * 4);
+    const size_t o_dtab = put(tt.dtab.data(), tt.dtab.size() * 8);
+    const size_t o_f0d = put(tt.f0d.data(), tt.f0d.size() * 8);
+    const size_t o_f0i = put(tt.f0i.data(), tt.f0i.size() * 4);
+    char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, blob.size()));
+    ctx->copy(dtab, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    const double* d_dist = reinterpret_cast<const double*>(dtab + o_dist);
+    const double* d_ret = reinterpret_cast<const double*>(dtab + o_ret);
+    const double* d_c0 = reinterpret_cast<const double*>(dtab + o_c0);
+    const uint32_t* d_col = reinterpret_cast<const uint32_t*>(dtab + o_col);
 
     // aggregates
     auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw)));
@@ -725,6 +694,12 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ret = d_ret;
       a.c0 = d_c0;
       a.col = d_col;
+      a.npad = tt.npad;
+      a.ccol = reinterpret_cast<const uint32_t*>(dtab + o_ccol);
+      a.itab = tt.intv ? reinterpret_cast<const int32_t*>(dtab + o_itab) : nullptr;
+      a.dtab = reinterpret_cast<const double*>(dtab + o_dtab);
+      a.f0d = reinterpret_cast<const double*>(dtab + o_f0d);
+      a.f0i = reinterpret_cast<const int32_t*>(dtab + o_f0i);
       a.tiled = tiled;
       a.gen = gp;
       a.totals = d_totals;
@@ -752,26 +727,25 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     // copies back
     const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
     if (out->totals && host_out)
-      CUDA_CHECK(cudaMemcpyAsync(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->copy(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost);
     if (full && !out_dev_tiled) {
       // tiled -> reference layout [m][n+1]
       double* V_ref = out_dev_ref ? out->values : static_cast<double*>(ctx->scratch_get(kScrOut5, m * n1 * 8));
       launch_from_tiled<double>(ctx, d_V, n1, m, V_ref);
-      if (host_out) CUDA_CHECK(cudaMemcpyAsync(out->values, V_ref, m * n1 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (host_out) ctx->copy(out->values, V_ref, m * n1 * 8, cudaMemcpyDeviceToHost);
       int32_t* C_ref = out_dev_ref ? out->cuts : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, m * n1 * 4));
       launch_from_tiled<int32_t>(ctx, d_cuts, n1, m, C_ref);
       if (host_out) {
-        CUDA_CHECK(cudaMemcpyAsync(out->cuts, C_ref, m * n1 * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(out->route_count, d_rc, m * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(out->feasible, d_feas, m, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->copy(out->cuts, C_ref, m * n1 * 4, cudaMemcpyDeviceToHost);
+        ctx->copy(out->route_count, d_rc, m * 4, cudaMemcpyDeviceToHost);
+        ctx->copy(out->feasible, d_feas, m, cudaMemcpyDeviceToHost);
       }
     }
     const bool want_agg = out->agg || out->agg_raw;
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
       h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(k * sizeof(scendp_agg_raw)));
-      CUDA_CHECK(cudaMemcpyAsync(h_raw, d_agg, k * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+      ctx->copy(h_raw, d_agg, k * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost);
     }
     if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
     if (want_agg) {

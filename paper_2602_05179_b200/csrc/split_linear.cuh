@@ -1,0 +1,298 @@
+// split_linear.cuh -- K1: hard capacities, O(n) monotone deque
+// (reference split_core_linear, proj/src/split.cpp:77-118).  Included by
+// split.cu (shares SplitArgs / demand_at / push_overflow).
+//
+// The kernel is issue-bound (its DRAM traffic equals the algorithmic 4n+8
+// bytes per scenario), so the step is written for instruction count:
+//  * tour constants arrive as 128-bit broadcast loads once per 4 positions
+//    (chunked SoA tables in shared memory);
+//  * the deque's front entry (f, load, idx, routes) and back f-value live in
+//    registers; the per-thread ring in shared memory is read only when an end
+//    moves (eviction / pop) and written once per push;
+//  * the deque is never empty at the start of a position (position i-1 was
+//    just pushed) and, unless d_i > Q, entry i-1 survives the eviction, so
+//    the common path carries no emptiness tests: the rare "window emptied"
+//    and "popped empty" cases are handled inside the eviction / pop bodies;
+//  * ring overflow is checked once per chunk (<= 11 entries before a chunk
+//    of 4 pushes cannot reach 16).
+//
+// Value type VT: double (the reference's arithmetic verbatim), or int32 when
+// the host proved every tour cost is an integer and every partial sum stays
+// below 2^29.  Then every fp64 operation of the reference is exact, and
+//   V(i) = f(front) + (dist_i + ret_i),  f(i) = V(i) + (c0_i - dist_{i+1})
+// reproduce its doubles bit for bit with one integer add each.  +inf is the
+// class of values >= 2^29 (an emptied window yields 2^30 and inf-class values
+// never decrease below 2^30 - dist_n).  Inf-class entries can
+// only occupy the back of the deque, so the finite prefix -- which alone
+// decides V and the cuts -- is identical to the reference's.
+#pragma once
+
+constexpr int32_t kIntInf = 1 << 30;      // value of an emptied window
+constexpr int32_t kIntFinite = 1 << 29;   // v < kIntFinite  <=>  finite
+constexpr int kK1Threads = 128;           // CTA size (ring stride)
+constexpr int kRingSpan = kRing * kK1Threads;  // slot counters are scaled by T
+
+template <typename VT>
+struct K1State {
+  uint32_t load;
+  int head, tail;  // slot * kK1Threads, unbounded (masked on access)
+  VT front_f, back_f, v;
+  uint32_t front_l;
+  int32_t front_i, front_rc, rc;
+};
+
+template <typename VT>
+__device__ __forceinline__ bool k1_finite(VT v) {
+  if constexpr (std::is_same<VT, int32_t>::value) return v < kIntFinite;
+  else return v < kInfD;
+}
+
+template <typename VT>
+__device__ __forceinline__ double k1_to_double(VT v) {
+  if constexpr (std::is_same<VT, int32_t>::value)
+    return v < kIntFinite ? static_cast<double>(v) : kInfD;
+  else return v;
+}
+
+template <typename VT>
+__device__ __forceinline__ VT k1_inf() {
+  if constexpr (std::is_same<VT, int32_t>::value) return kIntInf;
+  else return kInfD;
+}
+
+template <typename VT>
+__device__ __forceinline__ VT k1_neg_inf() {
+  if constexpr (std::is_same<VT, int32_t>::value) return INT32_MIN;
+  else return -kInfD;
+}
+
+// One DP position.  PUSH = (i < n).  Ring slot s of this thread lives at
+// rf[s & (kRingSpan-1)] (rf/rl/ri/rr are per-thread base pointers).
+template <typename VT, bool FULL, bool PUSH>
+__device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
+                                        VT t1, VT t2, VT t3, VT* __restrict__ rf,
+                                        uint32_t* __restrict__ rl, int32_t* __restrict__ ri,
+                                        int32_t* __restrict__ rr, double* Vout, int32_t* Cout) {
+  s.load += d;
+  // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96)
+  while (s.load - s.front_l > Qc) {
+    s.head += kK1Threads;
+    if (s.head == s.tail) {
+      // d_i > Q: the window is empty, V(i) = +inf.  The placeholder front
+      // (inf-class f, load of position i) stands in for entry i until it is
+      // pushed; the back is parked at -inf so nothing is popped.
+      s.front_f = k1_inf<VT>();
+      s.front_l = s.load;
+      s.front_i = -1;
+      s.front_rc = -1;
+      s.back_f = k1_neg_inf<VT>();
+      break;
+    }
+    const int hs = s.head & (kRingSpan - 1);
+    s.front_f = rf[hs];
+    s.front_l = rl[hs];
+    if (FULL) {
+      s.front_i = ri[hs];
+      s.front_rc = rr[hs];
+    }
+  }
+  if constexpr (std::is_same<VT, int32_t>::value) s.v = s.front_f + t0;
+  else s.v = __dadd_rn(__dadd_rn(s.front_f, t0), t1);
+  if (FULL) {
+    const bool fin = k1_finite(s.v);
+    s.rc = fin ? s.front_rc + 1 : 0;
+    Vout[static_cast<uint64_t>(i) * kTile] = k1_to_double(s.v);
+    Cout[static_cast<uint64_t>(i) * kTile] = fin ? s.front_i : -1;
+  }
+  if (PUSH) {
+    VT fi;
+    if constexpr (std::is_same<VT, int32_t>::value) fi = s.v + t1;
+    else fi = __dsub_rn(__dadd_rn(s.v, t2), t3);
+    // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113)
+    while (s.back_f > fi) {
+      s.tail -= kK1Threads;
+      if (s.tail == s.head) {
+        // popped empty: entry i becomes the front
+        s.back_f = k1_neg_inf<VT>();
+        s.front_f = fi;
+        s.front_l = s.load;
+        s.front_i = i;
+        s.front_rc = s.rc;
+        break;
+      }
+      s.back_f = rf[(s.tail - kK1Threads) & (kRingSpan - 1)];
+    }
+    const int ts = s.tail & (kRingSpan - 1);
+    rf[ts] = fi;
+    rl[ts] = s.load;
+    if (FULL) {
+      ri[ts] = i;
+      rr[ts] = s.rc;
+    }
+    s.tail += kK1Threads;
+    s.back_f = fi;
+  }
+}
+
+template <bool FULL, int SRC, bool INTV>
+__global__ void __launch_bounds__(kK1Threads)
+split_linear_kernel(SplitArgs a) {
+  using VT = typename std::conditional<INTV, int32_t, double>::type;
+  constexpr int T = kK1Threads;
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t k = blockIdx.y;
+  const int n = a.n;
+  const int npad = a.npad;  // multiple of 4, >= n + 4
+  // chunked tour tables, slot s = position s+1: col | t0..t3
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem);
+  VT* s_tab = reinterpret_cast<VT*>(s_col + npad);
+  constexpr int ntab = INTV ? 2 : 4;
+  {
+    const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
+    for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
+    if (INTV) {
+      const int32_t* g = a.itab + static_cast<uint64_t>(k) * 2 * npad;
+      for (int x = threadIdx.x; x < 2 * npad; x += T) reinterpret_cast<int32_t*>(s_tab)[x] = g[x];
+    } else {
+      const double* g = a.dtab + static_cast<uint64_t>(k) * 4 * npad;
+      for (int x = threadIdx.x; x < 4 * npad; x += T) reinterpret_cast<double*>(s_tab)[x] = g[x];
+    }
+  }
+  const int tid = threadIdx.x;
+  VT* rf = reinterpret_cast<VT*>(s_tab + ntab * npad) + tid;                 // [kRing][T]
+  uint32_t* rl = reinterpret_cast<uint32_t*>(rf - tid + kRingSpan) + tid;   // [kRing][T]
+  int32_t* ri = reinterpret_cast<int32_t*>(rl - tid + kRingSpan) + tid;     // FULL
+  int32_t* rr = ri + kRingSpan;                                             // FULL
+  agg_cta_init(s_agg);
+  __syncthreads();
+
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;  // wave-local
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;                                  // call-level
+  const uint32_t Qc = static_cast<uint32_t>(a.Q);  // host guarantees Q < 2^31
+
+  K1State<VT> s;
+  bool ok = true;
+  if (active) {
+    const uint32_t* tile_base = nullptr;
+    uint64_t stream = 0;
+    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+    double* Vout = nullptr;
+    int32_t* Cout = nullptr;
+    if (FULL) {
+      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+      Vout = a.V + base;
+      Cout = a.cuts + base;
+      Vout[0] = 0.0;
+      Cout[0] = 0;
+    }
+    // p = 0: f(0) = (0.0 + c(0, s_1)) - dist[1]
+    s.front_f = INTV ? static_cast<VT>(a.f0i[k]) : static_cast<VT>(a.f0d[k]);
+    s.back_f = s.front_f;
+    s.front_l = 0u;
+    s.front_i = 0;
+    s.front_rc = 0;
+    s.rc = 0;
+    s.v = VT(0);
+    s.load = 0u;
+    s.head = 0;
+    s.tail = T;
+    rf[0] = s.front_f;
+    rl[0] = 0u;
+    if (FULL) {
+      ri[0] = 0;
+      rr[0] = 0;
+    }
+
+    // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
+    const int npush = n - 1;
+    const int nfull = npush >> 2;
+    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dc3 = 0;
+    if (nfull > 0) {
+      const uint4 c = *reinterpret_cast<const uint4*>(s_col);
+      dc0 = demand_at(a, SRC, stream, tile_base, c.x);
+      dc1 = demand_at(a, SRC, stream, tile_base, c.y);
+      dc2 = demand_at(a, SRC, stream, tile_base, c.z);
+      dc3 = demand_at(a, SRC, stream, tile_base, c.w);
+    }
+    int cidx = 0;
+    for (; cidx < nfull; ++cidx) {
+      // a chunk pushes 4 entries: with <= kRing-5 live entries it cannot
+      // overflow the ring; otherwise the scenario takes the generic path
+      if (s.tail - s.head > (kRing - 5) * T) {
+        ok = false;
+        break;
+      }
+      const int s0 = cidx * 4;
+      uint32_t dn0 = 0, dn1 = 0, dn2 = 0, dn3 = 0;
+      if (cidx + 1 < nfull) {
+        const uint4 c = *reinterpret_cast<const uint4*>(s_col + s0 + 4);
+        dn0 = demand_at(a, SRC, stream, tile_base, c.x);
+        dn1 = demand_at(a, SRC, stream, tile_base, c.y);
+        dn2 = demand_at(a, SRC, stream, tile_base, c.z);
+        dn3 = demand_at(a, SRC, stream, tile_base, c.w);
+      }
+      VT t0[4], t1[4], t2[4], t3[4];
+      if constexpr (INTV) {
+        const int4 x0 = *reinterpret_cast<const int4*>(s_tab + s0);
+        const int4 x1 = *reinterpret_cast<const int4*>(s_tab + npad + s0);
+        t0[0] = x0.x; t0[1] = x0.y; t0[2] = x0.z; t0[3] = x0.w;
+        t1[0] = x1.x; t1[1] = x1.y; t1[2] = x1.z; t1[3] = x1.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t2[j] = t3[j] = 0;
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 y0 = *reinterpret_cast<const double2*>(s_tab + 0 * npad + s0 + 2 * h);
+          const double2 y1 = *reinterpret_cast<const double2*>(s_tab + 1 * npad + s0 + 2 * h);
+          const double2 y2 = *reinterpret_cast<const double2*>(s_tab + 2 * npad + s0 + 2 * h);
+          const double2 y3 = *reinterpret_cast<const double2*>(s_tab + 3 * npad + s0 + 2 * h);
+          t0[2 * h] = y0.x; t0[2 * h + 1] = y0.y;
+          t1[2 * h] = y1.x; t1[2 * h + 1] = y1.y;
+          t2[2 * h] = y2.x; t2[2 * h + 1] = y2.y;
+          t3[2 * h] = y3.x; t3[2 * h + 1] = y3.y;
+        }
+      }
+      k1_step<VT, FULL, true>(s, s0 + 1, dc0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 2, dc1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 3, dc2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 4, dc3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+      dc0 = dn0;
+      dc1 = dn1;
+      dc2 = dn2;
+      dc3 = dn3;
+    }
+    // remaining pushing positions (< 4), then position n (no push)
+    for (int i = nfull * 4 + 1; ok && i <= n; ++i) {
+      if (s.tail - s.head >= (kRing - 1) * T) {
+        ok = false;
+        break;
+      }
+      const int sl = i - 1;
+      const uint32_t d = demand_at(a, SRC, stream, tile_base, s_col[sl]);
+      const VT x0 = s_tab[sl], x1 = s_tab[npad + sl];
+      const VT x2 = INTV ? VT(0) : s_tab[(ntab > 2 ? 2 : 0) * npad + sl];
+      const VT x3 = INTV ? VT(0) : s_tab[(ntab > 3 ? 3 : 0) * npad + sl];
+      if (i < n) k1_step<VT, FULL, true>(s, i, d, Qc, x0, x1, x2, x3, rf, rl, ri, rr, Vout, Cout);
+      else k1_step<VT, FULL, false>(s, i, d, Qc, x0, x1, x2, x3, rf, rl, ri, rr, Vout, Cout);
+    }
+    if (!ok) {
+      push_overflow(a, k, wl);
+    } else {
+      const double vd = k1_to_double(s.v);
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = vd;
+      if (FULL) {
+        const bool fin = vd < kInfD;
+        a.route_count[w] = fin ? s.rc : 0;
+        a.feasible[w] = fin ? 1 : 0;
+      }
+    }
+  }
+  const double vout = active && ok ? k1_to_double(s.v) : 0.0;
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(vout, true), active && ok);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
+}
