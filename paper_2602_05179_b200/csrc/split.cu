@@ -67,6 +67,7 @@ struct SplitArgs {
   const uint32_t* col; // s_i - 1, i = 1..n
   // K1 chunked tables, [k][npad] per row; slot s = position s+1
   int32_t npad;
+  int32_t ident;         // every tour is the identity 1..n
   const uint32_t* ccol;  // customer row of position s+1
   const int32_t* itab;   // [k][2][npad]: A = dist+ret, B = c0 - dist_next (int path)
   const double* dtab;    // [k][4][npad]: dist, ret, c0, dist_next
@@ -384,6 +385,7 @@ struct TourTables {
   // K1 chunked tables
   int npad = 0;
   bool intv = false;  // every tour admits the exact integer path
+  bool ident = false; // every tour is the identity (contiguous demand rows)
   std::vector<uint32_t> ccol;
   std::vector<int32_t> itab, f0i;
   std::vector<double> dtab, f0d;
@@ -476,6 +478,13 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, 
     }
   }
   t.intv = intv;
+  t.ident = true;
+  for (uint32_t q = 0; q < k && t.ident; ++q)
+    for (int i = 0; i < n; ++i)
+      if (tours[static_cast<size_t>(q) * n + i] != i + 1) {
+        t.ident = false;
+        break;
+      }
   if (intv) {
     for (uint32_t q = 0; q < k; ++q) {
       const double* dist = t.dist.data() + q * n1;
@@ -536,12 +545,16 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     const size_t smem = static_cast<size_t>(a.npad) * (4 + (intv ? 2 : 4) * vt) +
                         static_cast<size_t>(kRing) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
+    auto go = [&](auto kernel) {
+      set_smem(kernel, smem);
+      kernel<<<grid, T, smem, ctx->stream>>>(a);
+    };
     if (intv) {
-      set_smem(split_linear_kernel<FULL, SRC, true>, smem);
-      split_linear_kernel<FULL, SRC, true><<<grid, T, smem, ctx->stream>>>(a);
+      if (a.ident) go(split_linear_kernel<FULL, SRC, true, true>);
+      else go(split_linear_kernel<FULL, SRC, true, false>);
     } else {
-      set_smem(split_linear_kernel<FULL, SRC, false>, smem);
-      split_linear_kernel<FULL, SRC, false><<<grid, T, smem, ctx->stream>>>(a);
+      if (a.ident) go(split_linear_kernel<FULL, SRC, false, true>);
+      else go(split_linear_kernel<FULL, SRC, false, false>);
     }
   } else {
     const int T = quad_threads(n);
@@ -695,6 +708,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.c0 = d_c0;
       a.col = d_col;
       a.npad = tt.npad;
+      a.ident = tt.ident ? 1 : 0;
       a.ccol = reinterpret_cast<const uint32_t*>(dtab + o_ccol);
       a.itab = tt.intv ? reinterpret_cast<const int32_t*>(dtab + o_itab) : nullptr;
       a.dtab = reinterpret_cast<const double*>(dtab + o_dtab);

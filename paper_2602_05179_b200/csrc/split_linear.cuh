@@ -30,12 +30,20 @@
 constexpr int32_t kIntInf = 1 << 30;      // value of an emptied window
 constexpr int32_t kIntFinite = 1 << 29;   // v < kIntFinite  <=>  finite
 constexpr int kK1Threads = 128;           // CTA size (ring stride)
-constexpr int kRingSpan = kRing * kK1Threads;  // slot counters are scaled by T
+constexpr int kRingSpan = kRing * kK1Threads;  // ring elements per array
+constexpr int kStep = kK1Threads * 4;           // counters: byte offsets of 4-byte slots
+constexpr int kMask = kRing * kStep - 1;
+
+// Ring slot at counter c (bytes for 4-byte elements, scaled for wider ones).
+template <typename E>
+__device__ __forceinline__ E& ring_at(E* base, int c) {
+  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + (sizeof(E) / 4) * (c & kMask));
+}
 
 template <typename VT>
 struct K1State {
   uint32_t load;
-  int head, tail;  // slot * kK1Threads, unbounded (masked on access)
+  int head, tail;  // slot * kStep (byte offsets), unbounded, masked on access
   VT front_f, back_f, v;
   uint32_t front_l;
   int32_t front_i, front_rc, rc;
@@ -67,33 +75,37 @@ __device__ __forceinline__ VT k1_neg_inf() {
 }
 
 // One DP position.  PUSH = (i < n).  Ring slot s of this thread lives at
-// rf[s & (kRingSpan-1)] (rf/rl/ri/rr are per-thread base pointers).
+// ring_at(rf, s) (rf/rl/ri/rr are per-thread base pointers).
 template <typename VT, bool FULL, bool PUSH>
 __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
                                         VT t1, VT t2, VT t3, VT* __restrict__ rf,
                                         uint32_t* __restrict__ rl, int32_t* __restrict__ ri,
                                         int32_t* __restrict__ rr, double* Vout, int32_t* Cout) {
   s.load += d;
-  // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96)
+  // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96); the
+  // evicted slot becomes the -inf sentinel below the new head
   while (s.load - s.front_l > Qc) {
-    s.head += kK1Threads;
+    ring_at(rf, s.head) = k1_neg_inf<VT>();
+    s.head += kStep;
     if (s.head == s.tail) {
-      // d_i > Q: the window is empty, V(i) = +inf.  The placeholder front
-      // (inf-class f, load of position i) stands in for entry i until it is
-      // pushed; the back is parked at -inf so nothing is popped.
+      // only when d_i > Q: every route into i overflows, V(i) = +inf.  The
+      // placeholder front (inf-class f, load of position i) stands in for
+      // entry i until it is pushed; the parked back value stops the pops.
+      s.back_f = k1_neg_inf<VT>();
       s.front_f = k1_inf<VT>();
       s.front_l = s.load;
-      s.front_i = -1;
-      s.front_rc = -1;
-      s.back_f = k1_neg_inf<VT>();
+      if (FULL) {
+        s.front_i = -1;
+        s.front_rc = -1;
+      }
       break;
     }
-    const int hs = s.head & (kRingSpan - 1);
-    s.front_f = rf[hs];
-    s.front_l = rl[hs];
+    const int hs = s.head;
+    s.front_f = ring_at(rf, hs);
+    s.front_l = ring_at(rl, hs);
     if (FULL) {
-      s.front_i = ri[hs];
-      s.front_rc = rr[hs];
+      s.front_i = ring_at(ri, hs);
+      s.front_rc = ring_at(rr, hs);
     }
   }
   if constexpr (std::is_same<VT, int32_t>::value) s.v = s.front_f + t0;
@@ -108,33 +120,59 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
     VT fi;
     if constexpr (std::is_same<VT, int32_t>::value) fi = s.v + t1;
     else fi = __dsub_rn(__dadd_rn(s.v, t2), t3);
-    // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113)
+    // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113);
+    // the -inf sentinel in the slot below the head ends the loop when the
+    // deque runs empty
     while (s.back_f > fi) {
-      s.tail -= kK1Threads;
-      if (s.tail == s.head) {
-        // popped empty: entry i becomes the front
-        s.back_f = k1_neg_inf<VT>();
-        s.front_f = fi;
-        s.front_l = s.load;
+      s.tail -= kStep;
+      s.back_f = ring_at(rf, s.tail - kStep);
+    }
+    if (s.tail == s.head) {  // popped empty: entry i becomes the front
+      s.front_f = fi;
+      s.front_l = s.load;
+      if (FULL) {
         s.front_i = i;
         s.front_rc = s.rc;
-        break;
       }
-      s.back_f = rf[(s.tail - kK1Threads) & (kRingSpan - 1)];
     }
-    const int ts = s.tail & (kRingSpan - 1);
-    rf[ts] = fi;
-    rl[ts] = s.load;
+    const int ts = s.tail;
+    ring_at(rf, ts) = fi;
+    ring_at(rl, ts) = s.load;
     if (FULL) {
-      ri[ts] = i;
-      rr[ts] = s.rc;
+      ring_at(ri, ts) = i;
+      ring_at(rr, ts) = s.rc;
     }
-    s.tail += kK1Threads;
+    s.tail += kStep;
     s.back_f = fi;
   }
 }
 
-template <bool FULL, int SRC, bool INTV>
+// Demands of tour slots s0..s0+3.  IDENT (identity giant tour, the
+// reference's default tour, scendp_main.cpp:222-225): slot s reads customer
+// row s, so the four rows are consecutive 128-byte lines (immediate offsets).
+template <int SRC, bool IDENT>
+__device__ __forceinline__ void k1_demand4(const SplitArgs& a, uint64_t stream,
+                                           const uint32_t* tile_base, const uint32_t* s_col,
+                                           int s0, uint32_t& d0, uint32_t& d1, uint32_t& d2,
+                                           uint32_t& d3) {
+  if constexpr (IDENT && SRC == kSrcTiled) {
+    const uint32_t* p = tile_base + static_cast<uint64_t>(s0) * kTile;
+    d0 = __ldg(p);
+    d1 = __ldg(p + kTile);
+    d2 = __ldg(p + 2 * kTile);
+    d3 = __ldg(p + 3 * kTile);
+  } else {
+    uint4 c;
+    if constexpr (IDENT) c = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
+    else c = *reinterpret_cast<const uint4*>(s_col + s0);
+    d0 = demand_at(a, SRC, stream, tile_base, c.x);
+    d1 = demand_at(a, SRC, stream, tile_base, c.y);
+    d2 = demand_at(a, SRC, stream, tile_base, c.z);
+    d3 = demand_at(a, SRC, stream, tile_base, c.w);
+  }
+}
+
+template <bool FULL, int SRC, bool INTV, bool IDENT>
 __global__ void __launch_bounds__(kK1Threads)
 split_linear_kernel(SplitArgs a) {
   using VT = typename std::conditional<INTV, int32_t, double>::type;
@@ -197,43 +235,35 @@ split_linear_kernel(SplitArgs a) {
     s.rc = 0;
     s.v = VT(0);
     s.load = 0u;
-    s.head = 0;
-    s.tail = T;
-    rf[0] = s.front_f;
-    rl[0] = 0u;
+    // slot 0: -inf sentinel (always the slot below the head); slot 1: p = 0
+    s.head = kStep;
+    s.tail = 2 * kStep;
+    rf[0] = k1_neg_inf<VT>();
+    ring_at(rf, kStep) = s.front_f;
+    ring_at(rl, kStep) = 0u;
     if (FULL) {
-      ri[0] = 0;
-      rr[0] = 0;
+      ring_at(ri, kStep) = 0;
+      ring_at(rr, kStep) = 0;
     }
 
     // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
     const int npush = n - 1;
     const int nfull = npush >> 2;
     uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dc3 = 0;
-    if (nfull > 0) {
-      const uint4 c = *reinterpret_cast<const uint4*>(s_col);
-      dc0 = demand_at(a, SRC, stream, tile_base, c.x);
-      dc1 = demand_at(a, SRC, stream, tile_base, c.y);
-      dc2 = demand_at(a, SRC, stream, tile_base, c.z);
-      dc3 = demand_at(a, SRC, stream, tile_base, c.w);
-    }
+    if (nfull > 0) k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, 0, dc0, dc1, dc2, dc3);
     int cidx = 0;
     for (; cidx < nfull; ++cidx) {
-      // a chunk pushes 4 entries: with <= kRing-5 live entries it cannot
-      // overflow the ring; otherwise the scenario takes the generic path
-      if (s.tail - s.head > (kRing - 5) * T) {
+      // the ring holds the sentinel + at most kRing-1 entries, so a push needs
+      // <= kRing-2 live entries; a chunk pushes 4, hence <= kRing-5 at its
+      // start -- otherwise the scenario takes the generic path
+      if (s.tail - s.head > (kRing - 5) * kStep) {
         ok = false;
         break;
       }
       const int s0 = cidx * 4;
       uint32_t dn0 = 0, dn1 = 0, dn2 = 0, dn3 = 0;
-      if (cidx + 1 < nfull) {
-        const uint4 c = *reinterpret_cast<const uint4*>(s_col + s0 + 4);
-        dn0 = demand_at(a, SRC, stream, tile_base, c.x);
-        dn1 = demand_at(a, SRC, stream, tile_base, c.y);
-        dn2 = demand_at(a, SRC, stream, tile_base, c.z);
-        dn3 = demand_at(a, SRC, stream, tile_base, c.w);
-      }
+      if (cidx + 1 < nfull)
+        k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, s0 + 4, dn0, dn1, dn2, dn3);
       VT t0[4], t1[4], t2[4], t3[4];
       if constexpr (INTV) {
         const int4 x0 = *reinterpret_cast<const int4*>(s_tab + s0);
@@ -266,12 +296,12 @@ split_linear_kernel(SplitArgs a) {
     }
     // remaining pushing positions (< 4), then position n (no push)
     for (int i = nfull * 4 + 1; ok && i <= n; ++i) {
-      if (s.tail - s.head >= (kRing - 1) * T) {
+      if (s.tail - s.head > (kRing - 2) * kStep) {
         ok = false;
         break;
       }
       const int sl = i - 1;
-      const uint32_t d = demand_at(a, SRC, stream, tile_base, s_col[sl]);
+      const uint32_t d = demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]);
       const VT x0 = s_tab[sl], x1 = s_tab[npad + sl];
       const VT x2 = INTV ? VT(0) : s_tab[(ntab > 2 ? 2 : 0) * npad + sl];
       const VT x3 = INTV ? VT(0) : s_tab[(ntab > 3 ? 3 : 0) * npad + sl];
