@@ -208,7 +208,10 @@ split_linear_kernel(SplitArgs a) {
   const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;  // wave-local
   const bool active = wl < a.m_wave;
   const uint64_t w = a.w_base + wl;                                  // call-level
-  const uint32_t Qc = static_cast<uint32_t>(a.Q);  // host guarantees Q < 2^31
+  uint32_t Qc = static_cast<uint32_t>(a.Q);  // host guarantees Q < 2^31
+  // keep Q in a register (opaque to the compiler): otherwise it is re-read
+  // from the constant bank at every comparison, one issue slot each
+  Qc += static_cast<uint32_t>(a.m_total >> 62);  // + 0, but not provably so
 
   K1State<VT> s;
   bool ok = true;
@@ -249,21 +252,11 @@ split_linear_kernel(SplitArgs a) {
     // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
     const int npush = n - 1;
     const int nfull = npush >> 2;
-    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dc3 = 0;
-    if (nfull > 0) k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, 0, dc0, dc1, dc2, dc3);
-    int cidx = 0;
-    for (; cidx < nfull; ++cidx) {
-      // the ring holds the sentinel + at most kRing-1 entries, so a push needs
-      // <= kRing-2 live entries; a chunk pushes 4, hence <= kRing-5 at its
-      // start -- otherwise the scenario takes the generic path
-      if (s.tail - s.head > (kRing - 5) * kStep) {
-        ok = false;
-        break;
-      }
-      const int s0 = cidx * 4;
-      uint32_t dn0 = 0, dn1 = 0, dn2 = 0, dn3 = 0;
-      if (cidx + 1 < nfull)
-        k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, s0 + 4, dn0, dn1, dn2, dn3);
+    // the ring holds the sentinel + at most kRing-1 entries, so a push needs
+    // <= kRing-2 live entries; a chunk pushes 4, hence <= kRing-5 at its start
+    // -- otherwise the scenario takes the generic path
+    constexpr int kChunkRoom = (kRing - 5) * kStep;
+    auto chunk = [&](int s0, uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {
       VT t0[4], t1[4], t2[4], t3[4];
       if constexpr (INTV) {
         const int4 x0 = *reinterpret_cast<const int4*>(s_tab + s0);
@@ -285,14 +278,35 @@ split_linear_kernel(SplitArgs a) {
           t3[2 * h] = y3.x; t3[2 * h + 1] = y3.y;
         }
       }
-      k1_step<VT, FULL, true>(s, s0 + 1, dc0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 2, dc1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 3, dc2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 4, dc3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
-      dc0 = dn0;
-      dc1 = dn1;
-      dc2 = dn2;
-      dc3 = dn3;
+      k1_step<VT, FULL, true>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+      k1_step<VT, FULL, true>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+    };
+    // pairs of chunks with ping-pong demand registers (no copies); demands
+    // are loaded one chunk ahead
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    if (nfull > 0) k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, 0, a0, a1, a2, a3);
+    int cidx = 0;
+    for (; cidx + 1 < nfull; cidx += 2) {
+      const int s0 = cidx * 4;
+      if (s.tail - s.head > kChunkRoom) {
+        ok = false;
+        break;
+      }
+      k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, s0 + 4, b0, b1, b2, b3);
+      chunk(s0, a0, a1, a2, a3);
+      if (s.tail - s.head > kChunkRoom) {
+        ok = false;
+        break;
+      }
+      if (cidx + 2 < nfull)
+        k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, s0 + 8, a0, a1, a2, a3);
+      chunk(s0 + 4, b0, b1, b2, b3);
+    }
+    if (ok && cidx < nfull) {
+      if (s.tail - s.head > kChunkRoom) ok = false;
+      else chunk(cidx * 4, a0, a1, a2, a3);
     }
     // remaining pushing positions (< 4), then position n (no push)
     for (int i = nfull * 4 + 1; ok && i <= n; ++i) {
