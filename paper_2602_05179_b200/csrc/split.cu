@@ -542,7 +542,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     const int T = kK1Threads;
     const bool intv = a.itab != nullptr;
     const size_t vt = intv ? 4 : 8;
-    const size_t smem = static_cast<size_t>(a.npad) * (4 + (intv ? 2 : 4) * vt) +
+    const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + (intv ? 2 : 4) * vt) +
                         static_cast<size_t>(kRing) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {

@@ -184,11 +184,11 @@ split_linear_kernel(SplitArgs a) {
   const int npad = a.npad;  // multiple of 4, >= n + 4
   // chunked tour tables, slot s = position s+1: col | t0..t3
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem);
-  VT* s_tab = reinterpret_cast<VT*>(s_col + npad);
+  VT* s_tab = reinterpret_cast<VT*>(s_col + (IDENT ? 0 : npad));  // IDENT: no column table
   constexpr int ntab = INTV ? 2 : 4;
   {
     const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
-    for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
+    if (!IDENT) for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
     if (INTV) {
       const int32_t* g = a.itab + static_cast<uint64_t>(k) * 2 * npad;
       for (int x = threadIdx.x; x < 2 * npad; x += T) reinterpret_cast<int32_t*>(s_tab)[x] = g[x];
