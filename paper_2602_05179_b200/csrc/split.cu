@@ -68,6 +68,7 @@ struct SplitArgs {
   // K1 chunked tables, [k][npad] per row; slot s = position s+1
   int32_t npad;
   int32_t ident;         // every tour is the identity 1..n
+  uint32_t pen_lmax;     // K2-int: loads above this leave the exact int32 range
   const uint32_t* ccol;  // customer row of position s+1
   const int32_t* itab;   // [k][2][npad]: A = dist+ret, B = c0 - dist_next (int path)
   const double* dtab;    // [k][4][npad]: dist, ret, c0, dist_next
@@ -130,6 +131,7 @@ __device__ __forceinline__ void push_overflow(const SplitArgs& a, uint32_t k, ui
 }
 
 #include "split_linear.cuh"
+#include "split_penal.cuh"
 
 // ---------------------------------------------------------------------------
 // K2: O(n^2) Bellman min (split.cpp:45-75), penalized (or forced) mode.
@@ -386,6 +388,7 @@ struct TourTables {
   int npad = 0;
   bool intv = false;  // every tour admits the exact integer path
   bool ident = false; // every tour is the identity (contiguous demand rows)
+  double costbound = 0.0;  // max over tours of dist_n + sum(c0 + ret) + max c0
   std::vector<uint32_t> ccol;
   std::vector<int32_t> itab, f0i;
   std::vector<double> dtab, f0d;
@@ -466,6 +469,7 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, 
     }
     bound += cmax;
     intv &= integral && bound < static_cast<double>(1 << 29);
+    t.costbound = std::max(t.costbound, bound);
     t.f0d[q] = (0.0 + c0[0]) - dist[1];
     for (int i = 1; i <= n; ++i) {
       const size_t sidx = static_cast<size_t>(i - 1);
@@ -529,7 +533,19 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   const bool small_tables = tour_smem_bytes(n) <= 48 * 1024 &&
                             static_cast<size_t>(a.npad) * 36 <= 96 * 1024;
   const int tok = ctx->timing_begin(0);
-  if (use_generic_range || !small_tables) {
+  // penalized with integral data: exact O(n) form (pen_lmax > 0 marks it)
+  if (!linear && !a.hard && a.pen_lmax > 0 && small_tables) {
+    const int T = kPenThreads;
+    const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + 2 * 4) +
+                        static_cast<size_t>(T) * (kRing * 8 + kPosRing * (8 + (FULL ? 4 : 0)));
+    dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
+    auto go = [&](auto kernel) {
+      set_smem(kernel, smem);
+      kernel<<<grid, T, smem, ctx->stream>>>(a);
+    };
+    if (a.ident) go(split_penal_kernel<FULL, SRC, true>);
+    else go(split_penal_kernel<FULL, SRC, false>);
+  } else if (use_generic_range || !small_tables) {
     const uint64_t items = static_cast<uint64_t>(a.k) * a.m_wave;
     split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
         a, 0, items, generic_scratch, generic_stride);
@@ -537,8 +553,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     ctx->count_launch();
     ctx->timing_end(tok);
     return;
-  }
-  if (linear) {
+  } else if (linear) {
     const int T = kK1Threads;
     const bool intv = a.itab != nullptr;
     const size_t vt = intv ? 4 : 8;
@@ -709,6 +724,18 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.col = d_col;
       a.npad = tt.npad;
       a.ident = tt.ident ? 1 : 0;
+      // K2-int eligibility: integral tour costs (tt.intv) and an integral
+      // beta; loads up to pen_lmax keep every sum exact and inside int32
+      // (|values| <= 2 (costbound + beta * L) < 2^30); larger loads are
+      // detected per scenario and re-run on the generic fp64 path
+      a.pen_lmax = 0;
+      if (!inst->hard && tt.intv && !(flags & SCENDP_QUADRATIC) &&
+          inst->penalty_beta == std::floor(inst->penalty_beta) && inst->penalty_beta >= 0.0 &&
+          inst->penalty_beta <= 1048576.0) {
+        const double room = static_cast<double>(1 << 29) - tt.costbound;
+        const double lm = inst->penalty_beta > 0.0 ? room / inst->penalty_beta : 2147483647.0;
+        a.pen_lmax = static_cast<uint32_t>(std::min(lm, 2147483647.0 - static_cast<double>(inst->capacity)));
+      }
       a.ccol = reinterpret_cast<const uint32_t*>(dtab + o_ccol);
       a.itab = tt.intv ? reinterpret_cast<const int32_t*>(dtab + o_itab) : nullptr;
       a.dtab = reinterpret_cast<const double*>(dtab + o_dtab);

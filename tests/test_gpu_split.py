@@ -176,3 +176,35 @@ def test_waves_do_not_change_results(oracle):
         rb = b.split_eval(inst, tour, dem)
     np.testing.assert_array_equal(ra["totals"], rb["totals"])
     assert ra["agg"] == rb["agg"]
+
+
+def test_penalized_exact_path_edges(ctx, oracle, reference):
+    """K2-int (O(n) penalized form) fall-backs: windows longer than the
+    position ring (zero demands), loads beyond the exact int32 range, beta=0,
+    and ties between the window and the penalized prefix."""
+    n = 60
+    rng = np.random.default_rng(12)
+    tour = rand_tour(n, 2)
+    dem = rng.integers(0, 12, size=(700, n)).astype(np.uint32)
+    dem[::5] = 0                       # every route fits: window = whole prefix
+    dem[1::9, 7] = 3_000_000_000       # beta * load leaves the int32 range
+    dem[2::9] = 1                      # long windows
+    for beta in (0.0, 1.0, 10.0, 37.0):
+        inst = RoutingInstance(n, 20, False, beta, oracle.make_random_instance(n, 3))
+        got = ctx.split_eval(inst, tour, dem, full=True)
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+            n, 20, 0, beta, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
+        check_mean(got["agg"][0], mean)
+    # ties: all-equal costs make many candidates coincide
+    c = np.ones((n + 2, n + 2)) * 4.0
+    np.fill_diagonal(c, 0.0)
+    inst = RoutingInstance(n, 15, False, 2.0, c)
+    d2 = rng.integers(1, 6, size=(300, n)).astype(np.uint32)
+    got = ctx.split_eval(inst, tour, d2, full=True)
+    tot, V, cuts, rc, feas, agg = reference.expected_split(n, 15, 0, 2.0, c, tour, d2)
+    np.testing.assert_array_equal(got["cuts"], cuts)
+    np.testing.assert_array_equal(got["totals"][0], tot)
