@@ -1,0 +1,200 @@
+// facade_main.cpp -- drives the C++ drop-in facade (include/scendp/*.hpp)
+// exactly as a user of the reference would, and prints the results as plain
+// text for tests/test_gpu_facade.py, which compares them with the real
+// reference library (oracle/_ref) on identical inputs.
+//
+//   facade_main split <n> <Q> <hard> <beta> <inst_seed> <scen_seed> <m> <tour_seed>
+//   facade_main dsirp <U> <I0> <H> <R> <seed> <m>
+//   facade_main saa <n> <Q> <beta> <inst_seed> <scen_seed> <m> <max_evals> <kbatch>
+//   facade_main gen <kind> <lo> <hi> <mean> <std> <seed> <entities> <steps> <count>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "scendp/oudp.hpp"
+#include "scendp/saa.hpp"
+#include "scendp/scenario.hpp"
+#include "scendp/split.hpp"
+
+using namespace scendp;
+
+namespace {
+
+void print_vec(const char* tag, const std::vector<double>& v) {
+  std::printf("%s %zu", tag, v.size());
+  for (double x : v) std::printf(" %.17g", x);
+  std::printf("\n");
+}
+
+template <typename I>
+void print_ivec(const char* tag, const std::vector<I>& v) {
+  std::printf("%s %zu", tag, v.size());
+  for (I x : v) std::printf(" %lld", static_cast<long long>(x));
+  std::printf("\n");
+}
+
+GiantTour tour_of(int n, unsigned long long seed) {
+  GiantTour t;
+  t.order.resize(n);
+  std::iota(t.order.begin(), t.order.end(), 1);
+  if (seed == 0) return t;
+  SplitMix64 rng(seed);
+  for (int i = n - 1; i > 0; --i) {  // Fisher-Yates as oracle.cpp:23-32
+    const int j = static_cast<int>(rng.next_below(i + 1));
+    std::swap(t.order[i], t.order[j]);
+  }
+  return t;
+}
+
+int run_split(char** a) {
+  const int n = std::atoi(a[0]);
+  const long long Q = std::atoll(a[1]);
+  const bool hard = std::atoi(a[2]) != 0;
+  const double beta = std::atof(a[3]);
+  const unsigned long long iseed = std::strtoull(a[4], nullptr, 10);
+  const unsigned long long sseed = std::strtoull(a[5], nullptr, 10);
+  const std::size_t m = std::strtoull(a[6], nullptr, 10);
+  const unsigned long long tseed = std::strtoull(a[7], nullptr, 10);
+  RoutingInstance inst = make_random_instance(n, iseed, Q, hard, beta);
+  GiantTour tour = tour_of(n, tseed);
+  DistributionSpec dist = DistributionSpec::parse("uniform:1:10", sseed);
+  ScenarioBatch batch = generate_scenarios(dist, n, 1, m);
+  std::printf("demand_sum %llu\n",
+              static_cast<unsigned long long>(std::accumulate(batch.data.begin(), batch.data.end(), 0ull)));
+  auto costs = batched_split_costs(inst, tour, batch, BackendConfig::multi_thread(8));
+  std::vector<double> tot(m);
+  for (std::size_t w = 0; w < m; ++w) tot[w] = costs.per_scenario[w].value;
+  print_vec("totals", tot);
+  std::printf("mean %.17g finite %zu infeasible %zu\n", costs.mean_cost ? *costs.mean_cost : -1.0,
+              costs.finite_count, costs.infeasible_count);
+  auto full = batched_expected_split(inst, tour, batch, BackendConfig::single_thread());
+  std::vector<double> v0;
+  std::vector<int> c0, rcs;
+  for (std::size_t w = 0; w < m && w < 4; ++w) {
+    for (auto& x : full.per_scenario[w].values.values) v0.push_back(x.value);
+    for (int c : full.per_scenario[w].cuts) c0.push_back(c);
+  }
+  for (std::size_t w = 0; w < m; ++w) rcs.push_back(full.per_scenario[w].route_count);
+  print_vec("V4", v0);
+  print_ivec("cuts4", c0);
+  print_ivec("route_count", rcs);
+  std::printf("full_mean %.17g\n", full.mean_cost ? *full.mean_cost : -1.0);
+  auto gen = batched_split_costs_generated(inst, tour, dist, m, BackendConfig::gpu());
+  std::vector<double> gt(m);
+  for (std::size_t w = 0; w < m; ++w) gt[w] = gen.per_scenario[w].value;
+  print_vec("gen_totals", gt);
+  // routes of scenario 0
+  for (auto [p, i] : recover_routes(full.per_scenario[0])) std::printf("route %d %d\n", p, i);
+  return 0;
+}
+
+int run_dsirp(char** a) {
+  CustomerSpec spec;
+  spec.capacity = std::atoi(a[0]);
+  spec.initial_inventory = std::atoi(a[1]);
+  spec.horizon = std::atoi(a[2]);
+  const int R = std::atoi(a[3]);
+  const unsigned long long seed = std::strtoull(a[4], nullptr, 10);
+  const std::size_t m = std::strtoull(a[5], nullptr, 10);
+  spec.holding = 1.25;
+  spec.stockout_multiplier = 2.5;
+  DeliveryCostModel del = DeliveryCostModel::linear(spec.horizon, R, 40.0, 0.5);
+  for (int t = 0; t < spec.horizon; ++t)
+    for (int r = 0; r < R; ++r) {
+      del.fixed[t * R + r] = 40.0 + 5.0 * r + 0.125 * t;
+      del.unit[t * R + r] = 0.5 + 0.25 * r;
+    }
+  HoldingPenaltyModel hold;
+  DistributionSpec dist = DistributionSpec::parse("uniform:0:33", seed);
+  ScenarioBatch batch = generate_scenarios(dist, 1, spec.horizon, m);
+  auto res = batched_expected_cost(spec, del, hold, batch, BackendConfig::gpu());
+  std::vector<double> tot;
+  std::vector<int> dl, q, ei, ro;
+  for (std::size_t w = 0; w < m; ++w) {
+    const ScheduleResult& s = res.per_scenario[w];
+    tot.push_back(s.total.value);
+    for (int t = 0; t < spec.horizon; ++t) {
+      dl.push_back(s.deliver[t]);
+      q.push_back(s.quantity[t]);
+      ei.push_back(s.end_inventory[t]);
+      ro.push_back(s.route_option[t]);
+    }
+  }
+  print_vec("totals", tot);
+  print_ivec("deliver", dl);
+  print_ivec("quantity", q);
+  print_ivec("end_inventory", ei);
+  print_ivec("route_option", ro);
+  std::printf("mean %.17g errors %zu\n", res.mean_cost ? *res.mean_cost : -1.0, res.error_count());
+  // single-scenario API and the replay helper
+  ScheduleResult one = solve_customer_scenario(spec, del, hold, batch.column(0));
+  ExtendedCost replay = simulate_schedule(spec, del, hold, batch.column(0), one.deliver, one.route_option);
+  std::printf("one %.17g replay %.17g\n", one.total.value, replay.value);
+  return 0;
+}
+
+int run_saa(char** a) {
+  const int n = std::atoi(a[0]);
+  const long long Q = std::atoll(a[1]);
+  const double beta = std::atof(a[2]);
+  const unsigned long long iseed = std::strtoull(a[3], nullptr, 10);
+  const unsigned long long sseed = std::strtoull(a[4], nullptr, 10);
+  const std::size_t m = std::strtoull(a[5], nullptr, 10);
+  const unsigned long long max_evals = std::strtoull(a[6], nullptr, 10);
+  set_candidate_batch(std::strtoull(a[7], nullptr, 10));
+  RoutingInstance inst = make_random_instance(n, iseed, Q, false, beta);
+  ScenarioBatch train = generate_scenarios(DistributionSpec::parse("uniform:1:10", sseed), n, 1, m);
+  SearchBudget budget;
+  budget.max_evaluations = max_evals;
+  SearchResult r = improve_first_stage(inst, train, BackendConfig::gpu(), budget);
+  print_ivec("tour", r.tour.order);
+  std::printf("value %.17g evaluations %llu best_found_at %llu\n", r.value,
+              static_cast<unsigned long long>(r.evaluations),
+              static_cast<unsigned long long>(r.best_found_at));
+  std::vector<double> traj;
+  for (auto& p : r.trajectory) traj.push_back(p.best_value);
+  print_vec("trajectory", traj);
+  std::printf("oos %.17g\n", out_of_sample_eval(inst, r.tour, train, BackendConfig::gpu()));
+  return 0;
+}
+
+int run_gen(char** a) {
+  DistributionSpec d;
+  const int kind = std::atoi(a[0]);
+  d.kind = kind == 0 ? DistributionSpec::Kind::kUniformInt
+                     : (kind == 1 ? DistributionSpec::Kind::kTruncatedNormal
+                                  : DistributionSpec::Kind::kPoisson);
+  d.lo = std::atoll(a[1]);
+  d.hi = std::atoll(a[2]);
+  d.mean = std::atof(a[3]);
+  d.stddev = std::atof(a[4]);
+  d.seed = std::strtoull(a[5], nullptr, 10);
+  ScenarioBatch b = generate_scenarios(d, std::strtoull(a[6], nullptr, 10),
+                                       std::strtoull(a[7], nullptr, 10),
+                                       std::strtoull(a[8], nullptr, 10));
+  print_ivec("data", b.data);
+  std::vector<std::uint32_t> col(b.rows);
+  generate_scenario_column(d, 3, col);
+  print_ivec("col3", col);
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) return 2;
+  const std::string mode = argv[1];
+  try {
+    if (mode == "split" && argc == 10) return run_split(argv + 2);
+    if (mode == "dsirp" && argc == 8) return run_dsirp(argv + 2);
+    if (mode == "saa" && argc == 10) return run_saa(argv + 2);
+    if (mode == "gen" && argc == 11) return run_gen(argv + 2);
+  } catch (const std::exception& e) {
+    std::printf("exception %s\n", e.what());
+    return 1;
+  }
+  return 2;
+}
