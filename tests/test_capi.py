@@ -1,11 +1,10 @@
 """C-ABI checks that need no GPU: the library loads, exports every symbol
 include/scendp_cuda.h declares, fails loudly without a device (no CPU
 fallback), and finalizes exact aggregates correctly."""
-import ctypes as C
 import math
 import os
 import re
-import struct
+import sys
 from fractions import Fraction
 
 import numpy as np
@@ -15,6 +14,7 @@ from paper_2602_05179_b200 import _capi as A
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "scendp_cuda.h")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def header_functions():
@@ -58,39 +58,7 @@ def test_no_cpu_fallback_without_device():
 
 
 # ---- exact aggregate -------------------------------------------------------
-def pieces(v):
-    """Python restatement of agg_pieces (csrc/common.cuh)."""
-    bits = struct.unpack("<Q", struct.pack("<d", v))[0]
-    be = (bits >> 52) & 0x7FF
-    M = bits & ((1 << 52) - 1)
-    if be == 0:
-        E = -1074
-    else:
-        M |= 1 << 52
-        E = be - 1075
-    pos = E + 192
-    if pos + 53 > 384:
-        return None
-    if pos < 0:
-        M = 0 if -pos >= 64 else M >> (-pos)
-        pos = 0
-    x = M << (pos & 31)
-    li = pos >> 5
-    return li, [x & 0xFFFFFFFF, (x >> 32) & 0xFFFFFFFF, (x >> 64) & 0xFFFFFFFF]
-
-
-def raw_of(values):
-    r = A.AggRaw()
-    for v in values:
-        if not math.isfinite(v):
-            r.infeasible_count += 1
-            continue
-        li, ps = pieces(v)
-        for j, p in enumerate(ps):
-            if p:
-                r.digits[li + j] += p
-        r.finite_count += 1
-    return r
+from aggref import raw_of  # noqa: E402
 
 
 def finalize(raws, k=1):
