@@ -242,6 +242,7 @@ typedef struct {
 
 #define SCENDP_DSIRP_COST_ONLY 0u
 #define SCENDP_DSIRP_FULL 1u   /* + schedules (ScheduleResult, oudp.hpp:69-75) */
+#define SCENDP_DSIRP_FP64 0x400u /* force the fp64 kernel (no exact-integer path) */
 
 typedef struct {
   uint32_t mem_kind;       /* HOST / DEVICE (reference-like layout below) or

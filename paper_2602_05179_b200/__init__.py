@@ -315,13 +315,13 @@ class Context:
     def dsirp_eval(self, customers: Sequence[Customer], scenarios, count: Optional[int] = None,
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    out_kind: str = "host", device_out: Optional[dict] = None,
-                   sync: bool = True) -> dict:
+                   sync: bool = True, fp64: bool = False) -> dict:
         nc = len(customers)
         H = customers[0].H
         carr = (A.Customer * nc)(*[c.as_c() for c in customers])
         sc, keep = self._scenarios(scenarios, nc * H, count, first_index)
         m = sc.count
-        flags = (A.DSIRP_FULL if full else 0) | (0 if sync else A.ASYNC)
+        flags = (A.DSIRP_FULL if full else 0) | (0 if sync else A.ASYNC) | (A.DSIRP_FP64 if fp64 else 0)
         agg = (A.Agg * nc)()
         res = {}
         if out_kind == "host":

@@ -27,6 +27,7 @@ MEM_HOST, MEM_DEVICE, MEM_DEVICE_TILED, MEM_GENERATED = 0, 1, 2, 3
 CTX_KERNEL_TIMING = 0x1
 SPLIT_COST_ONLY, SPLIT_FULL = 0, 1
 DSIRP_COST_ONLY, DSIRP_FULL = 0, 1
+DSIRP_FP64 = 0x400
 ASYNC = 0x100
 QUADRATIC = 0x200
 AGG_DIGITS = 12

@@ -40,241 +40,16 @@ template <typename T>
 void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst);
 }
 
+#include "dsirp_kernels.cuh"
+
+using namespace scendp_dsirp;
+
+namespace scendp_dsirp {
+void launch_h4(scendp_ctx* c, const DsirpArgs& a, size_t s, bool i, bool f) { launch_h<4>(c, a, s, i, f); }
+void launch_h8(scendp_ctx* c, const DsirpArgs& a, size_t s, bool i, bool f) { launch_h<8>(c, a, s, i, f); }
+}  // namespace scendp_dsirp
+
 namespace {
-
-constexpr double kInfD = __builtin_huge_val();
-constexpr int kDsirpThreads = 128;
-
-struct CustDev {
-  int32_t U, I0, H, R;
-  double h, rh;            // rh = rho * h, same rounding as the reference
-  int32_t del_tab, hold_tab;
-  uint64_t off_fixed, off_unit, off_dtable, off_htable;  // into the pool
-};
-
-struct DsirpArgs {
-  const CustDev* cust;   // [nc]
-  const double* pool;
-  uint32_t nc;
-  int32_t H;
-  uint64_t rows;         // nc * H
-  uint64_t m_wave, w_base, m_total;
-  const uint32_t* tiled; // wave-local tiled demands
-  GenParams gen;
-  double* totals;        // [nc][m_total] or null
-  uint8_t* evaluated;    // [nc][m_total] or null
-  uint8_t* deliver;      // FULL tiled [nc][m/32][H][32]
-  int32_t* quantity;
-  int32_t* end_inventory;
-  int32_t* route_option;
-  unsigned long long* agg;  // [nc][16]
-};
-
-template <int K>
-__device__ __forceinline__ double sel_d(const double (&a)[K], int idx) {
-  double r = a[0];
-#pragma unroll
-  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
-  return r;
-}
-template <int K>
-__device__ __forceinline__ uint32_t sel_u(const uint32_t (&a)[K], int idx) {
-  uint32_t r = a[0];
-#pragma unroll
-  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
-  return r;
-}
-
-template <int HMAX, bool FULL, int SRC>
-__global__ void __launch_bounds__(kDsirpThreads)
-dsirp_kernel(DsirpArgs a) {
-  constexpr int K = HMAX + 1;
-  extern __shared__ __align__(16) double s_fu[];  // fixed [H][R], unit [H][R]
-  __shared__ unsigned long long s_agg[kAggSlots];
-  const uint32_t c = blockIdx.y;
-  const CustDev cd = a.cust[c];
-  const int U = cd.U, H = cd.H, R = cd.R;
-  const int HR = H * R;
-  double* s_fixed = s_fu;
-  double* s_unit = s_fu + HR;
-  if (!cd.del_tab) {
-    for (int x = threadIdx.x; x < HR; x += blockDim.x) {
-      s_fixed[x] = a.pool[cd.off_fixed + x];
-      s_unit[x] = a.pool[cd.off_unit + x];
-    }
-  }
-  agg_cta_init(s_agg);
-  __syncthreads();
-
-  const double h = cd.h, rh = cd.rh;
-  const double* dtable = a.pool + cd.off_dtable;  // [H][U+1]
-  const double* htable = a.pool + cd.off_htable;  // [U+1]
-  const bool dtab = cd.del_tab != 0, htab = cd.hold_tab != 0;
-
-  const int tid = threadIdx.x;
-  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + tid;
-  const bool active = wl < a.m_wave;
-  const uint64_t w = a.w_base + wl;
-
-  // HoldingPenaltyModel::cost (oudp.hpp:58-62): h*J + (rho*h)*s, or table[J]
-  auto hold = [&](int j, int s) -> double {
-    if (htab) return __ldg(htable + j);
-    return __dadd_rn(__dmul_rn(h, static_cast<double>(j)), __dmul_rn(rh, static_cast<double>(s)));
-  };
-
-  double total = kInfD;
-  bool ok = false;
-  if (active) {
-    // demands of this (customer, scenario)
-    int dem[HMAX];
-    const uint64_t row0 = static_cast<uint64_t>(c) * H;
-    if (SRC == 0) {
-      const uint32_t* base = a.tiled + ((wl >> 5) * a.rows + row0) * kTile + (wl & 31);
-#pragma unroll
-      for (int t = 0; t < HMAX; ++t) dem[t] = t < H ? static_cast<int>(__ldg(base + t * kTile)) : 0;
-    } else {
-      const uint64_t stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
-#pragma unroll
-      for (int t = 0; t < HMAX; ++t)
-        dem[t] = t < H ? static_cast<int>(draw_counter(a.gen, stream, row0 + t)) : 0;
-    }
-
-    int st[K];
-    double vl[K];
-    uint32_t dm[K];      // FULL: delivery-day bitmask per slot
-    int opt[HMAX];       // FULL: route option of the day's delivery target
-#pragma unroll
-    for (int e = 0; e < K; ++e) {
-      st[e] = 0;
-      vl[e] = kInfD;
-      dm[e] = 0u;
-    }
-#pragma unroll
-    for (int t = 0; t < HMAX; ++t) opt[t] = 0;
-    st[0] = cd.I0;
-    vl[0] = 0.0;
-    uint64_t live = 1ull;
-
-#pragma unroll
-    for (int t = 0; t < HMAX; ++t) {
-      if (t < H) {
-        const int d = dem[t];
-        const int j1 = max(0, U - d), s1 = max(0, d - U);
-        const double hold1 = hold(j1, s1);
-        // (1) delivery: first minimum over (r, state) of a[i] + (F + hold1)
-        double bv = kInfD;
-        int br = 0, be = -1;
-        for (int r = 0; r < R; ++r) {
-          const double fx = dtab ? 0.0 : s_fixed[t * R + r];
-          const double un = dtab ? 0.0 : s_unit[t * R + r];
-#pragma unroll
-          for (int e = 0; e <= t; ++e) {
-            if (((live >> e) & 1ull) && st[e] < U) {
-              const int q = U - st[e];
-              const double F = dtab ? __ldg(dtable + t * (U + 1) + q)
-                                    : __dadd_rn(fx, __dmul_rn(un, static_cast<double>(q)));
-              const double cand = __dadd_rn(vl[e], __dadd_rn(F, hold1));
-              if (cand < bv) {
-                bv = cand;
-                br = r;
-                be = e;
-              }
-            }
-          }
-        }
-        // (2) no delivery, in place; states <= d collapse onto 0 keeping the
-        // first strict minimum
-        double b0 = kInfD;
-        int k0 = -1, tgt = -1;
-#pragma unroll
-        for (int e = 0; e <= t; ++e) {
-          if ((live >> e) & 1ull) {
-            const int i = st[e];
-            const int j = max(0, i - d), s = max(0, d - i);
-            const double nv = __dadd_rn(vl[e], hold(j, s));
-            if (i == U && j1 > 0) tgt = e;
-            st[e] = j;
-            vl[e] = nv;
-            if (i <= d) {
-              if (nv < b0) {
-                if (k0 >= 0) live &= ~(1ull << k0);
-                b0 = nv;
-                k0 = e;
-              } else {
-                live &= ~(1ull << e);
-              }
-            } else if (!(nv < kInfD)) {
-              live &= ~(1ull << e);
-            }
-          }
-        }
-        if (j1 == 0) tgt = k0;
-        // (3) merge the delivery candidate into state j1 (strict <)
-        if (be >= 0) {
-          const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
-          if (tgt >= 0) {
-            const double tv = ((live >> tgt) & 1ull) ? sel_d<K>(vl, tgt) : kInfD;
-            if (bv < tv) {
-#pragma unroll
-              for (int e = 0; e <= t; ++e) {
-                if (e == tgt) {
-                  vl[e] = bv;
-                  if (FULL) dm[e] = nm;
-                }
-              }
-              live |= 1ull << tgt;
-              if (FULL) opt[t] = br;
-            }
-          } else {
-            st[t + 1] = j1;
-            vl[t + 1] = bv;
-            live |= 1ull << (t + 1);
-            if (FULL) {
-              dm[t + 1] = nm;
-              opt[t] = br;
-            }
-          }
-        }
-      }
-    }
-    // pick_terminal: smallest state with the minimal value
-    int ts = -1;
-#pragma unroll
-    for (int e = 0; e < K; ++e) {
-      if (((live >> e) & 1ull) && vl[e] < total) {
-        total = vl[e];
-        ts = e;
-      }
-    }
-    ok = ts >= 0;
-    if (!ok) total = kInfD;  // logic_error slot: evaluated = 0
-    if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-    if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
-    if (FULL) {
-      const uint32_t mask = ok ? sel_u<K>(dm, ts) : 0u;
-      const uint64_t tiles = (a.m_total + 31) / 32;
-      const uint64_t ob = ((static_cast<uint64_t>(c) * tiles + (w >> 5)) * H) * kTile + (w & 31);
-      int inv = cd.I0;
-#pragma unroll
-      for (int t = 0; t < HMAX; ++t) {
-        if (t < H) {
-          const bool z = ok && ((mask >> t) & 1u);
-          const int q = z ? U - inv : 0;
-          const int j = max(0, inv + q - dem[t]);
-          a.deliver[ob + t * kTile] = z ? 1 : 0;
-          a.quantity[ob + t * kTile] = ok ? q : 0;
-          a.end_inventory[ob + t * kTile] = ok ? j : 0;
-          a.route_option[ob + t * kTile] = z ? opt[t] : 0;
-          inv = j;
-        }
-      }
-    }
-  }
-  __syncwarp();
-  agg_warp_add(s_agg, agg_pieces(total, ok), active);
-  __syncthreads();
-  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
-}
 
 // ---- host ----------------------------------------------------------------
 void validate_customer(const scendp_customer& s, int H) {
@@ -317,25 +92,73 @@ void validate_customer(const scendp_customer& s, int H) {
   }
 }
 
-template <int HMAX, bool FULL, int SRC>
-void launch_dsirp(scendp_ctx* ctx, const DsirpArgs& a, size_t smem) {
-  CUDA_CHECK(cudaFuncSetAttribute(dsirp_kernel<HMAX, FULL, SRC>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max<size_t>(smem, 16))));
-  dim3 grid(static_cast<unsigned>((a.m_wave + kDsirpThreads - 1) / kDsirpThreads), a.nc);
-  const int tok = ctx->timing_begin(0);
-  dsirp_kernel<HMAX, FULL, SRC><<<grid, kDsirpThreads, smem, ctx->stream>>>(a);
-  CUDA_CHECK(cudaGetLastError());
-  ctx->timing_end(tok);
-  ctx->count_launch();
-}
-
-template <bool FULL, int SRC>
-void dispatch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem) {
-  if (a.H <= 4) launch_dsirp<4, FULL, SRC>(ctx, a, smem);
-  else if (a.H <= 8) launch_dsirp<8, FULL, SRC>(ctx, a, smem);
-  else if (a.H <= 16) launch_dsirp<16, FULL, SRC>(ctx, a, smem);
-  else launch_dsirp<32, FULL, SRC>(ctx, a, smem);
+// Exact scaled-integer eligibility of one customer (dsirp_int_kernel): every
+// parameter the reference multiplies or adds is a multiple of 2^-shift and
+// every path cost stays below 2^22 after scaling, for demands <= dlim.
+bool prepare_int(const scendp_customer& s, int H, CustDev& d, std::vector<int32_t>& ipool) {
+  constexpr double kBound = 4194304.0;  // 2^22
+  const int U = s.capacity, R = s.options;
+  const double rh = s.stockout_multiplier * s.holding;  // the reference's rounding
+  std::vector<double> vals = {s.holding, rh};
+  if (s.delivery_tabular) vals.insert(vals.end(), s.delivery_table, s.delivery_table + static_cast<size_t>(H) * (U + 1));
+  else {
+    vals.insert(vals.end(), s.fixed, s.fixed + static_cast<size_t>(H) * R);
+    vals.insert(vals.end(), s.unit, s.unit + static_cast<size_t>(H) * R);
+  }
+  if (s.holding_tabular) vals.insert(vals.end(), s.holding_table, s.holding_table + U + 1);
+  int shift = -1;
+  for (int k = 0; k <= 12 && shift < 0; ++k) {
+    const double sc = std::ldexp(1.0, k);
+    bool ok = true;
+    for (double v : vals) {
+      const double x = v * sc;
+      if (!(x < kBound) || x != std::floor(x)) { ok = false; break; }
+    }
+    if (ok) shift = k;
+  }
+  if (shift < 0) return false;
+  const double sc = std::ldexp(1.0, shift);
+  // per (day, quantity): minimal scaled F and the first option attaining it
+  const size_t base = ipool.size();
+  ipool.resize(base + static_cast<size_t>(H) * (U + 1), INT32_MAX);
+  double maxF = 0.0;
+  for (int t = 0; t < H; ++t)
+    for (int q = 1; q <= U; ++q) {
+      double best = 0.0;
+      int br = -1;
+      for (int r = 0; r < (s.delivery_tabular ? 1 : R); ++r) {
+        const double F = s.delivery_tabular ? s.delivery_table[static_cast<size_t>(t) * (U + 1) + q] * sc
+                                            : s.fixed[t * R + r] * sc + s.unit[t * R + r] * sc * q;
+        if (br < 0 || F < best) { best = F; br = r; }
+      }
+      if (!(best < kBound)) return false;
+      maxF = std::max(maxF, best);
+      ipool[base + static_cast<size_t>(t) * (U + 1) + q] =
+          (static_cast<int32_t>(best) << 8) | br;
+    }
+  double maxHoldJ = 0.0;
+  size_t htab_off = 0;
+  if (s.holding_tabular) {
+    htab_off = ipool.size();
+    for (int j = 0; j <= U; ++j) {
+      ipool.push_back(static_cast<int32_t>(s.holding_table[j] * sc));
+      maxHoldJ = std::max(maxHoldJ, s.holding_table[j] * sc);
+    }
+  } else {
+    maxHoldJ = s.holding * sc * U;
+  }
+  const double perday = kBound / H - maxF - maxHoldJ;
+  if (!(perday > 0.0)) return false;
+  double dlim = 1073741824.0;
+  if (!s.holding_tabular && rh * sc > 0.0) dlim = std::min(dlim, std::floor(perday / (rh * sc)));
+  d.int_ok = 1;
+  d.shift = shift;
+  d.h_i = static_cast<int32_t>(s.holding * sc);
+  d.rh_i = static_cast<int32_t>(rh * sc);
+  d.dlim = static_cast<int32_t>(dlim);
+  d.off_gkey = base;
+  d.off_htab_i = htab_off;
+  return true;
 }
 
 }  // namespace
@@ -361,7 +184,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     CUDA_CHECK(cudaSetDevice(ctx->device));
 
     // customer records + parameter pool
-    std::vector<CustDev> cds(nc);
+    std::vector<CustDev> cds(nc, CustDev{});
     std::vector<double> pool;
     int maxR = 1;
     for (uint32_t c = 0; c < nc; ++c) {
@@ -388,11 +211,20 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       if (s.holding_tabular) pool.insert(pool.end(), s.holding_table, s.holding_table + s.capacity + 1);
     }
     if (pool.empty()) pool.push_back(0.0);
-    char* dcust = static_cast<char*>(ctx->scratch_get(kScrCustomers, nc * sizeof(CustDev) + 16 + pool.size() * 8));
+    // exact scaled-integer path when every customer admits it
+    std::vector<int32_t> ipool;
+    bool int_path = !(flags & SCENDP_DSIRP_FP64);
+    for (uint32_t c = 0; c < nc && int_path; ++c) int_path = prepare_int(customers[c], H, cds[c], ipool);
+    if (ipool.empty()) ipool.push_back(0);
+    const size_t o_pool = (nc * sizeof(CustDev) + 15) & ~size_t(15);
+    const size_t o_ipool = (o_pool + pool.size() * 8 + 15) & ~size_t(15);
+    char* dcust = static_cast<char*>(ctx->scratch_get(kScrCustomers, o_ipool + ipool.size() * 4));
     CustDev* d_cust = reinterpret_cast<CustDev*>(dcust);
-    double* d_pool = reinterpret_cast<double*>(dcust + ((nc * sizeof(CustDev) + 15) & ~size_t(15)));
+    double* d_pool = reinterpret_cast<double*>(dcust + o_pool);
+    int32_t* d_ipool = reinterpret_cast<int32_t*>(dcust + o_ipool);
     ctx->copy(d_cust, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice);
     ctx->copy(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice);
+    ctx->copy(d_ipool, ipool.data(), ipool.size() * 4, cudaMemcpyHostToDevice);
     const size_t smem = static_cast<size_t>(H) * maxR * 2 * sizeof(double);
 
     auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, nc * sizeof(scendp_agg_raw)));
@@ -441,13 +273,14 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       DsirpArgs a{};
       a.cust = d_cust;
       a.pool = d_pool;
+      a.ipool = d_ipool;
       a.nc = nc;
       a.H = H;
       a.rows = sc->rows;
       a.m_wave = mw;
       a.w_base = w0;
       a.m_total = m;
-      a.tiled = tiled;
+      a.tiled = fused ? nullptr : tiled;
       a.gen = gp;
       a.totals = d_totals;
       a.evaluated = d_eval;
@@ -456,13 +289,10 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       a.end_inventory = d_ei;
       a.route_option = d_ro;
       a.agg = d_agg;
-      if (full) {
-        if (fused) dispatch_h<true, 1>(ctx, a, smem);
-        else dispatch_h<true, 0>(ctx, a, smem);
-      } else {
-        if (fused) dispatch_h<false, 1>(ctx, a, smem);
-        else dispatch_h<false, 0>(ctx, a, smem);
-      }
+      if (H <= 4) launch_h4(ctx, a, smem, int_path, full);
+      else if (H <= 8) launch_h8(ctx, a, smem, int_path, full);
+      else if (H <= 16) launch_h16(ctx, a, smem, int_path, full);
+      else launch_h32(ctx, a, smem, int_path, full);
     }
 
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(nc) * kAggWords);

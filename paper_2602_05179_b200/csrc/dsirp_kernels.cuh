@@ -1,0 +1,470 @@
+// dsirp_kernels.cuh -- K3 device code (included by dsirp.cu inside its
+// anonymous namespace).  See dsirp.cu for the formulation.
+//
+//  * dsirp_unit_fp64: one (customer, scenario) unit with the reference's fp64
+//    arithmetic (forward_pass, oudp.cpp:40-87) on the register-resident sparse
+//    frontier; shared by the fp64 kernel and, as the exact fallback, by the
+//    integer kernel.
+//  * dsirp_kernel: fp64 path, CTA = one customer x 128 scenarios.
+//  * dsirp_int_kernel: exact scaled-integer path for dyadic cost models.
+#pragma once
+
+namespace scendp_dsirp {
+
+using namespace scendp_dev;
+
+constexpr double kInfD = __builtin_huge_val();
+constexpr int kDsirpThreads = 128;
+
+struct CustDev {
+  int32_t U, I0, H, R;
+  double h, rh;            // rh = rho * h, same rounding as the reference
+  int32_t del_tab, hold_tab;
+  uint64_t off_fixed, off_unit, off_dtable, off_htable;  // into the pool
+  // exact integer path (int_ok): every cost scaled by 2^shift is an integer
+  int32_t int_ok, shift;
+  int32_t h_i, rh_i;       // scaled h and rho*h
+  int32_t dlim;            // demands above this leave the exact int32 range
+  uint64_t off_gkey;       // int pool: [H][U+1] packed keys (minF << 8 | r)
+  uint64_t off_htab_i;     // int pool: [U+1] scaled holding table
+};
+
+struct DsirpArgs {
+  const CustDev* cust;   // [nc]
+  const double* pool;
+  const int32_t* ipool;  // integer tables (gkeys, scaled holding tables)
+  uint32_t nc;
+  int32_t H;
+  uint64_t rows;         // nc * H
+  uint64_t m_wave, w_base, m_total;
+  const uint32_t* tiled; // wave-local tiled demands
+  GenParams gen;
+  double* totals;        // [nc][m_total] or null
+  uint8_t* evaluated;    // [nc][m_total] or null
+  uint8_t* deliver;      // FULL tiled [nc][m/32][H][32]
+  int32_t* quantity;
+  int32_t* end_inventory;
+  int32_t* route_option;
+  unsigned long long* agg;  // [nc][16]
+};
+
+template <int K>
+__device__ __forceinline__ double sel_d(const double (&a)[K], int idx) {
+  double r = a[0];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
+  return r;
+}
+template <int K>
+__device__ __forceinline__ uint32_t sel_u(const uint32_t (&a)[K], int idx) {
+  uint32_t r = a[0];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r = (e == idx) ? a[e] : r;
+  return r;
+}
+
+template <int HMAX>
+__device__ __forceinline__ void dsirp_load_demands(const DsirpArgs& a, uint32_t c, uint64_t wl,
+                                                   int H, int (&dem)[HMAX]) {
+  const uint64_t row0 = static_cast<uint64_t>(c) * H;
+  if (a.tiled) {
+    const uint32_t* base = a.tiled + ((wl >> 5) * a.rows + row0) * kTile + (wl & 31);
+#pragma unroll
+    for (int t = 0; t < HMAX; ++t) dem[t] = t < H ? static_cast<int>(__ldg(base + t * kTile)) : 0;
+  } else {
+    const uint64_t stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+#pragma unroll
+    for (int t = 0; t < HMAX; ++t)
+      dem[t] = t < H ? static_cast<int>(draw_counter(a.gen, stream, row0 + t)) : 0;
+  }
+}
+
+// Schedule replay from the delivery mask (assemble_schedule, oudp.cpp:108-132).
+template <int HMAX>
+__device__ __forceinline__ void dsirp_write_schedule(const DsirpArgs& a, uint32_t c, uint64_t w,
+                                                     int U, int I0, int H, bool ok,
+                                                     uint32_t mask, const int (&opt)[HMAX],
+                                                     const int (&dem)[HMAX]) {
+  const uint64_t tiles = (a.m_total + 31) / 32;
+  const uint64_t ob = ((static_cast<uint64_t>(c) * tiles + (w >> 5)) * H) * kTile + (w & 31);
+  int inv = I0;
+#pragma unroll
+  for (int t = 0; t < HMAX; ++t) {
+    if (t < H) {
+      const bool z = ok && ((mask >> t) & 1u);
+      const int q = z ? U - inv : 0;
+      const int j = max(0, inv + q - dem[t]);
+      a.deliver[ob + t * kTile] = z ? 1 : 0;
+      a.quantity[ob + t * kTile] = ok ? q : 0;
+      a.end_inventory[ob + t * kTile] = ok ? j : 0;
+      a.route_option[ob + t * kTile] = z ? opt[t] : 0;
+      inv = j;
+    }
+  }
+}
+
+// One unit, fp64, reference arithmetic.  fixed/unit point to [H][R] arrays
+// (shared or global memory).  Writes totals/evaluated/schedule; returns the
+// total (+inf and ok = false for the all-infinite logic_error slot).
+template <int HMAX, bool FULL>
+__device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const CustDev& cd,
+                                                  const double* fixed, const double* unit,
+                                                  uint32_t c, uint64_t w, const int (&dem)[HMAX],
+                                                  bool& ok) {
+  constexpr int K = HMAX + 1;
+  constexpr int kUnr = HMAX <= 16 ? HMAX + 1 : 1;  // long horizons: rolled loops
+  const int U = cd.U, H = cd.H, R = cd.R;
+  const double h = cd.h, rh = cd.rh;
+  const double* dtable = a.pool + cd.off_dtable;  // [H][U+1]
+  const double* htable = a.pool + cd.off_htable;  // [U+1]
+  const bool dtab = cd.del_tab != 0, htab = cd.hold_tab != 0;
+  // HoldingPenaltyModel::cost (oudp.hpp:58-62): h*J + (rho*h)*s, or table[J]
+  auto hold = [&](int j, int s) -> double {
+    if (htab) return __ldg(htable + j);
+    return __dadd_rn(__dmul_rn(h, static_cast<double>(j)), __dmul_rn(rh, static_cast<double>(s)));
+  };
+  int st[K];
+  double vl[K];
+  uint32_t dm[K];  // FULL: delivery-day bitmask per slot
+  int opt[HMAX];   // FULL: route option of the day's delivery target
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    st[e] = 0;
+    vl[e] = kInfD;
+    dm[e] = 0u;
+  }
+#pragma unroll
+  for (int t = 0; t < HMAX; ++t) opt[t] = 0;
+  st[0] = cd.I0;
+  vl[0] = 0.0;
+  uint64_t live = 1ull;
+
+#pragma unroll kUnr
+  for (int t = 0; t < HMAX; ++t) {
+    if (t < H) {
+      const int d = dem[t];
+      const int j1 = max(0, U - d), s1 = max(0, d - U);
+      const double hold1 = hold(j1, s1);
+      // (1) delivery: first minimum over (r, state) of a[i] + (F + hold1)
+      double bv = kInfD;
+      int br = 0, be = -1;
+      for (int r = 0; r < R; ++r) {
+        const double fx = dtab ? 0.0 : fixed[t * R + r];
+        const double un = dtab ? 0.0 : unit[t * R + r];
+#pragma unroll kUnr
+        for (int e = 0; e <= t; ++e) {
+          if (((live >> e) & 1ull) && st[e] < U) {
+            const int q = U - st[e];
+            const double F = dtab ? __ldg(dtable + t * (U + 1) + q)
+                                  : __dadd_rn(fx, __dmul_rn(un, static_cast<double>(q)));
+            const double cand = __dadd_rn(vl[e], __dadd_rn(F, hold1));
+            if (cand < bv) {
+              bv = cand;
+              br = r;
+              be = e;
+            }
+          }
+        }
+      }
+      // (2) no delivery, in place; states <= d collapse onto 0 keeping the
+      // first strict minimum
+      double b0 = kInfD;
+      int k0 = -1, tgt = -1;
+#pragma unroll kUnr
+      for (int e = 0; e <= t; ++e) {
+        if ((live >> e) & 1ull) {
+          const int i = st[e];
+          const int j = max(0, i - d), s = max(0, d - i);
+          const double nv = __dadd_rn(vl[e], hold(j, s));
+          if (i == U && j1 > 0) tgt = e;
+          st[e] = j;
+          vl[e] = nv;
+          if (i <= d) {
+            if (nv < b0) {
+              if (k0 >= 0) live &= ~(1ull << k0);
+              b0 = nv;
+              k0 = e;
+            } else {
+              live &= ~(1ull << e);
+            }
+          } else if (!(nv < kInfD)) {
+            live &= ~(1ull << e);
+          }
+        }
+      }
+      if (j1 == 0) tgt = k0;
+      // (3) merge the delivery candidate into state j1 (strict <)
+      if (be >= 0) {
+        const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
+        if (tgt >= 0) {
+          const double tv = ((live >> tgt) & 1ull) ? sel_d<K>(vl, tgt) : kInfD;
+          if (bv < tv) {
+#pragma unroll kUnr
+            for (int e = 0; e <= t; ++e) {
+              if (e == tgt) {
+                vl[e] = bv;
+                if (FULL) dm[e] = nm;
+              }
+            }
+            live |= 1ull << tgt;
+            if (FULL) opt[t] = br;
+          }
+        } else {
+          st[t + 1] = j1;
+          vl[t + 1] = bv;
+          live |= 1ull << (t + 1);
+          if (FULL) {
+            dm[t + 1] = nm;
+            opt[t] = br;
+          }
+        }
+      }
+    }
+  }
+  // pick_terminal: smallest state with the minimal value
+  double total = kInfD;
+  int ts = -1;
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    if (((live >> e) & 1ull) && vl[e] < total) {
+      total = vl[e];
+      ts = e;
+    }
+  }
+  ok = ts >= 0;
+  if (!ok) total = kInfD;  // logic_error slot: evaluated = 0
+  if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
+  if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+  if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
+  return total;
+}
+
+template <int HMAX, bool FULL>
+__global__ void __launch_bounds__(kDsirpThreads)
+dsirp_kernel(DsirpArgs a) {
+  extern __shared__ __align__(16) double s_fu[];  // fixed [H][R], unit [H][R]
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t c = blockIdx.y;
+  const CustDev cd = a.cust[c];
+  const int HR = cd.H * cd.R;
+  double* s_fixed = s_fu;
+  double* s_unit = s_fu + HR;
+  if (!cd.del_tab) {
+    for (int x = threadIdx.x; x < HR; x += blockDim.x) {
+      s_fixed[x] = a.pool[cd.off_fixed + x];
+      s_unit[x] = a.pool[cd.off_unit + x];
+    }
+  }
+  agg_cta_init(s_agg);
+  __syncthreads();
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const bool active = wl < a.m_wave;
+  double total = kInfD;
+  bool ok = false;
+  if (active) {
+    int dem[HMAX];
+    dsirp_load_demands<HMAX>(a, c, wl, cd.H, dem);
+    total = dsirp_unit_fp64<HMAX, FULL>(a, cd, s_fixed, s_unit, c, a.w_base + wl, dem, ok);
+  }
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(total, ok), active);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
+}
+
+// ---------------------------------------------------------------------------
+// Exact scaled-integer path.  When every cost parameter of a customer is a
+// multiple of 2^-shift (dyadic, e.g. the 1/4 steps of the BASELINE pins) and
+// every path cost stays below 2^22 after scaling, each fp64 operation of the
+// reference (fixed + unit*q, h*J + (rho h)*s, the sums) is exact, so scaled
+// int32 arithmetic reproduces its doubles bit for bit.  Exactness also makes
+// the route-option scan separable: for a fixed state the reference's first
+// minimum over r is the smallest r with minimal F(t, r, q), independent of
+// the frontier value, so the host precomputes per (day, quantity) the key
+// (min_r F << 8) | argmin_r, and the per-slot delivery candidate becomes one
+// table lookup + add: key = gkey[t][U-i] + ((a[i] + hold1) << 8).  Comparing
+// packed keys with strict < over states in ascending order yields the
+// reference's (value, option, state) order.  A demand above `dlim` (bounds)
+// sends the unit through dsirp_unit_fp64 instead (global parameters).
+template <int HMAX, bool FULL>
+__global__ void __launch_bounds__(kDsirpThreads)
+dsirp_int_kernel(DsirpArgs a) {
+  constexpr int K = HMAX + 1;
+  constexpr int kUnr = HMAX <= 16 ? HMAX + 1 : 1;  // long horizons: rolled loops
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t c = blockIdx.y;
+  const CustDev cd = a.cust[c];
+  agg_cta_init(s_agg);
+  __syncthreads();
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;
+  const int U = cd.U, H = cd.H;
+  const int32_t* gkey = a.ipool + cd.off_gkey;     // [H][U+1]
+  const int32_t* htab = a.ipool + cd.off_htab_i;   // [U+1]
+  const bool htabular = cd.hold_tab != 0;
+  const int32_t hI = cd.h_i, rhI = cd.rh_i;
+  const double inv_scale = __longlong_as_double(static_cast<long long>(1023 - cd.shift) << 52);
+
+  double total = kInfD;
+  bool ok = false;
+  if (active) {
+    int dem[HMAX];
+    dsirp_load_demands<HMAX>(a, c, wl, H, dem);
+    bool in_range = true;
+#pragma unroll
+    for (int t = 0; t < HMAX; ++t)
+      if (t < H) in_range &= static_cast<unsigned>(dem[t]) <= static_cast<unsigned>(cd.dlim);
+    if (!in_range) {
+      total = dsirp_unit_fp64<HMAX, FULL>(a, cd, a.pool + cd.off_fixed, a.pool + cd.off_unit, c,
+                                          w, dem, ok);
+    } else {
+      auto hold = [&](int j, int s) -> int32_t {
+        if (htabular) return __ldg(htab + j);
+        return hI * j + rhI * s;
+      };
+      int st[K];
+      int32_t vl[K];
+      uint32_t dm[K];
+      int opt[HMAX];
+#pragma unroll
+      for (int e = 0; e < K; ++e) {
+        st[e] = 0;
+        vl[e] = 0;
+        dm[e] = 0u;
+      }
+#pragma unroll
+      for (int t = 0; t < HMAX; ++t) opt[t] = 0;
+      st[0] = cd.I0;
+      uint32_t live = 1u;
+#pragma unroll kUnr
+      for (int t = 0; t < HMAX; ++t) {
+        if (t < H) {
+          const int d = dem[t];
+          const int j1 = max(0, U - d), s1 = max(0, d - U);
+          const int32_t hold1 = hold(j1, s1);
+          const int32_t* grow = gkey + t * (U + 1) + U;  // grow[-i] = key for q = U - i
+          // (1) delivery candidate: packed (cand << 8 | r), first minimum
+          int32_t bk = INT32_MAX;
+          int be = -1;
+#pragma unroll kUnr
+          for (int e = 0; e <= t; ++e) {
+            if (((live >> e) & 1u) && st[e] < U) {
+              const int32_t key = __ldg(grow - st[e]) + ((vl[e] + hold1) << 8);
+              if (key < bk) {
+                bk = key;
+                be = e;
+              }
+            }
+          }
+          // (2) no delivery
+          int32_t b0 = INT32_MAX;
+          int k0 = -1, tgt = -1;
+#pragma unroll kUnr
+          for (int e = 0; e <= t; ++e) {
+            if ((live >> e) & 1u) {
+              const int i = st[e];
+              const int j = max(0, i - d), s = max(0, d - i);
+              const int32_t nv = vl[e] + hold(j, s);
+              if (i == U && j1 > 0) tgt = e;
+              st[e] = j;
+              vl[e] = nv;
+              if (i <= d) {
+                if (nv < b0) {
+                  if (k0 >= 0) live &= ~(1u << k0);
+                  b0 = nv;
+                  k0 = e;
+                } else {
+                  live &= ~(1u << e);
+                }
+              }
+            }
+          }
+          if (j1 == 0) tgt = k0;
+          // (3) merge (strict <)
+          if (be >= 0) {
+            const int32_t bv = bk >> 8;
+            const int br = bk & 0xff;
+            const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
+            if (tgt >= 0) {
+              int32_t tv = INT32_MAX;
+#pragma unroll kUnr
+              for (int e = 0; e <= t; ++e)
+                if (e == tgt && ((live >> e) & 1u)) tv = vl[e];
+              if (bv < tv) {
+#pragma unroll kUnr
+                for (int e = 0; e <= t; ++e) {
+                  if (e == tgt) {
+                    vl[e] = bv;
+                    if (FULL) dm[e] = nm;
+                  }
+                }
+                live |= 1u << tgt;
+                if (FULL) opt[t] = br;
+              }
+            } else {
+              st[t + 1] = j1;
+              vl[t + 1] = bv;
+              live |= 1u << (t + 1);
+              if (FULL) {
+                dm[t + 1] = nm;
+                opt[t] = br;
+              }
+            }
+          }
+        }
+      }
+      int32_t tv = INT32_MAX;
+      int ts = -1;
+#pragma unroll
+      for (int e = 0; e < K; ++e) {
+        if (((live >> e) & 1u) && vl[e] < tv) {
+          tv = vl[e];
+          ts = e;
+        }
+      }
+      ok = ts >= 0;  // always: the no-delivery chain keeps a state alive
+      total = ok ? static_cast<double>(tv) * inv_scale : kInfD;
+      if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
+      if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+      if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
+    }
+  }
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(total, ok), active);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
+}
+
+// Launch one HMAX instantiation (fp64 or exact-integer kernel).
+template <typename Kern>
+void launch_kernel(scendp_ctx* ctx, Kern kernel, const DsirpArgs& a, size_t smem) {
+  scendp_host::cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem < 16 ? 16 : smem)),
+                          "cudaFuncSetAttribute");
+  dim3 grid(static_cast<unsigned>((a.m_wave + kDsirpThreads - 1) / kDsirpThreads), a.nc);
+  const int tok = ctx->timing_begin(0);
+  kernel<<<grid, kDsirpThreads, smem, ctx->stream>>>(a);
+  scendp_host::cuda_check(cudaGetLastError(), "dsirp kernel launch");
+  ctx->timing_end(tok);
+  ctx->count_launch();
+}
+
+template <int HMAX>
+void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
+  if (int_path) {
+    if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0);
+    else launch_kernel(ctx, dsirp_int_kernel<HMAX, false>, a, 0);
+  } else {
+    if (full) launch_kernel(ctx, dsirp_kernel<HMAX, true>, a, smem);
+    else launch_kernel(ctx, dsirp_kernel<HMAX, false>, a, smem);
+  }
+}
+
+// One translation unit per horizon bound (parallel builds).
+void launch_h4(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);   // dsirp.cu
+void launch_h8(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);   // dsirp.cu
+void launch_h16(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h16.cu
+void launch_h32(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h32.cu
+
+}  // namespace scendp_dsirp
