@@ -336,7 +336,7 @@ dsirp_int_kernel(DsirpArgs a) {
 #pragma unroll
       for (int t = 0; t < HMAX; ++t) opt[t] = 0;
       st[0] = cd.I0;
-      uint32_t live = 1u;
+      uint64_t live = 1ull;  // K = HMAX+1 slots can exceed 32
 #pragma unroll kUnr
       for (int t = 0; t < HMAX; ++t) {
         if (t < H) {
@@ -349,7 +349,7 @@ dsirp_int_kernel(DsirpArgs a) {
           int be = -1;
 #pragma unroll kUnr
           for (int e = 0; e <= t; ++e) {
-            if (((live >> e) & 1u) && st[e] < U) {
+            if (((live >> e) & 1ull) && st[e] < U) {
               const int32_t key = __ldg(grow - st[e]) + ((vl[e] + hold1) << 8);
               if (key < bk) {
                 bk = key;
@@ -362,7 +362,7 @@ dsirp_int_kernel(DsirpArgs a) {
           int k0 = -1, tgt = -1;
 #pragma unroll kUnr
           for (int e = 0; e <= t; ++e) {
-            if ((live >> e) & 1u) {
+            if ((live >> e) & 1ull) {
               const int i = st[e];
               const int j = max(0, i - d), s = max(0, d - i);
               const int32_t nv = vl[e] + hold(j, s);
@@ -371,11 +371,11 @@ dsirp_int_kernel(DsirpArgs a) {
               vl[e] = nv;
               if (i <= d) {
                 if (nv < b0) {
-                  if (k0 >= 0) live &= ~(1u << k0);
+                  if (k0 >= 0) live &= ~(1ull << k0);
                   b0 = nv;
                   k0 = e;
                 } else {
-                  live &= ~(1u << e);
+                  live &= ~(1ull << e);
                 }
               }
             }
@@ -390,7 +390,7 @@ dsirp_int_kernel(DsirpArgs a) {
               int32_t tv = INT32_MAX;
 #pragma unroll kUnr
               for (int e = 0; e <= t; ++e)
-                if (e == tgt && ((live >> e) & 1u)) tv = vl[e];
+                if (e == tgt && ((live >> e) & 1ull)) tv = vl[e];
               if (bv < tv) {
 #pragma unroll kUnr
                 for (int e = 0; e <= t; ++e) {
@@ -399,13 +399,13 @@ dsirp_int_kernel(DsirpArgs a) {
                     if (FULL) dm[e] = nm;
                   }
                 }
-                live |= 1u << tgt;
+                live |= 1ull << tgt;
                 if (FULL) opt[t] = br;
               }
             } else {
               st[t + 1] = j1;
               vl[t + 1] = bv;
-              live |= 1u << (t + 1);
+              live |= 1ull << (t + 1);
               if (FULL) {
                 dm[t + 1] = nm;
                 opt[t] = br;
@@ -418,7 +418,7 @@ dsirp_int_kernel(DsirpArgs a) {
       int ts = -1;
 #pragma unroll
       for (int e = 0; e < K; ++e) {
-        if (((live >> e) & 1u) && vl[e] < tv) {
+        if (((live >> e) & 1ull) && vl[e] < tv) {
           tv = vl[e];
           ts = e;
         }
