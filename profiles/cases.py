@@ -1,0 +1,93 @@
+"""Short, fixed workloads for ncu captures (run under gpurun; never a bench).
+
+    python profiles/cases.py <case> [--reps R]
+
+Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
+  c2        split hard n=200, 10^6 scenarios, tiled HBM input, cost-only (K1 int32)
+  c2float   the same with non-integral costs (K1 fp64)
+  c2full    C2 with full solutions (V, cuts)
+  c2gen     C2 with in-kernel generation (the e2e call, batched_split_costs_generated)
+  c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
+  c5        1000 tours x 10^5 scenarios, n=50, penalized beta=10
+
+Every case runs one warm-up launch and then R timed launches; capture with
+e.g. `ncu --set full -k regex:split_linear -s 1 -c 1 python profiles/cases.py c2`.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("case")
+    p.add_argument("--reps", type=int, default=2)
+    args = p.parse_args()
+    from paper_2602_05179_b200 import (Context, Customer, Distribution, RoutingInstance,
+                                       derive_stream, make_random_instance, pinned_empty)
+    from paper_2602_05179_b200 import _capi as A
+
+    ctx = Context(0, timing=True)
+    c = args.case
+    if c.startswith("c2"):
+        n, m = 200, 1_000_000
+        tour = np.arange(1, n + 1, dtype=np.int32)
+        dist = Distribution("uniform", 1, 10, seed=derive_stream(1, 0x5343454E, 0))
+        if c == "c2float":
+            rng = np.random.default_rng(1)
+            cc = np.triu(rng.random((n + 2, n + 2)) * 20.0, 1)
+            inst = RoutingInstance(n, 100, True, 0.0, cc + cc.T)
+        else:
+            inst = make_random_instance(n, 1, 100, True)
+        tot = ctx.alloc(m * 8)
+        if c == "c2gen":
+            host_tot = pinned_empty(m, np.float64)
+            fn = lambda: ctx.split_eval(inst, tour, dist, count=m, host_totals=host_tot)
+        else:
+            scen = ctx.gen_scenarios(dist, n, m)
+            outs = {"totals": tot}
+            full = c == "c2full"
+            if full:
+                outs.update(values=ctx.alloc(ctx.tiled_bytes(n + 1, m) * 2),
+                            cuts=ctx.alloc(ctx.tiled_bytes(n + 1, m)),
+                            route_count=ctx.alloc(m * 4), feasible=ctx.alloc(m))
+            fn = lambda: ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m,
+                                        full=full, out_kind="device_tiled", device_out=outs,
+                                        sync=False)
+    elif c == "c3":
+        nc, m, H = 50, 100_000, 6
+        custs = [Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
+                          fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                          unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
+        sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m)
+        t3 = ctx.alloc(nc * m * 8)
+        fn = lambda: ctx.dsirp_eval(custs, (sc, A.MEM_DEVICE_TILED), count=m,
+                                    out_kind="device_tiled", device_out={"totals": t3},
+                                    sync=False)
+    elif c == "c5":
+        n5, m5, K5 = 50, 100_000, 1000
+        inst5 = make_random_instance(n5, 5, 100, False, 10.0)
+        rng = np.random.default_rng(5)
+        tours5 = np.stack([rng.permutation(n5) + 1 for _ in range(K5)]).astype(np.int32)
+        scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, m5)
+        fn = lambda: ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=m5,
+                                    totals=False)
+    else:
+        raise SystemExit(f"unknown case {c}")
+    fn()
+    ctx.sync()
+    ctx.kernel_stats(reset=True)
+    for _ in range(args.reps):
+        fn()
+    ctx.sync()
+    st = ctx.kernel_stats(reset=True)
+    print(f"{c}: {st}")
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
