@@ -152,6 +152,33 @@ scendp_status scendp_scenarios_to_tiled(scendp_ctx* ctx, const uint32_t* src,
                                         uint64_t rows, uint64_t count,
                                         uint32_t* dst_tiled);
 
+/* ---- SCNB scenario files (io.hpp:44-49, io.cpp:276-344) -----------------
+ * Little-endian "SCNB" | u16 version=1 | u32 rows | u32 cols | u16 dtype=1
+ * (u32), then rows*cols u32 values, scenario-major.  The 16-byte header keeps
+ * the payload 16-byte aligned, and scenarios [a, b) are one contiguous file
+ * range, so a shard is read without touching the rest of the file.  Errors
+ * use the reference's messages (SCENDP_ERR_RUNTIME = its runtime_error). */
+typedef struct {
+  uint64_t rows;   /* ScenarioBatch::rows */
+  uint64_t count;  /* ScenarioBatch::count (the header's "cols") */
+} scendp_scnb_header;
+
+scendp_status scendp_scnb_header_read(const char* path, scendp_scnb_header* hdr);
+
+/* Streams scenarios [first, first+count) of an SCNB file into device memory
+ * `out` in `layout` (SCENDP_MEM_DEVICE: reference layout, count*rows u32;
+ * SCENDP_MEM_DEVICE_TILED: native layout, scendp_tiled_bytes(rows, count),
+ * scenario `first` in tile 0).  Whole-tile chunks are read with pread() into
+ * two page-locked staging buffers, alternating, while the previous chunk's
+ * H2D copy (and tiling) runs on the context stream.  Synchronous. */
+scendp_status scendp_scnb_load(scendp_ctx* ctx, const char* path, uint64_t first,
+                               uint64_t count, uint32_t layout, uint32_t* out);
+
+/* write_scenario_binary (io.cpp:300-307) for a host scenario set in the
+ * reference layout. */
+scendp_status scendp_scnb_write(const char* path, const uint32_t* data,
+                                uint64_t rows, uint64_t count);
+
 /* ---- aggregates ----------------------------------------------------------
  * Per candidate (tour or customer): the finite-cost sum, exact.  Every
  * finite cost is added into a fixed-point integer accumulator (32-bit digits

@@ -315,7 +315,8 @@ class Context:
     def dsirp_eval(self, customers: Sequence[Customer], scenarios, count: Optional[int] = None,
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    out_kind: str = "host", device_out: Optional[dict] = None,
-                   sync: bool = True, fp64: bool = False) -> dict:
+                   sync: bool = True, fp64: bool = False,
+                   host_totals: Optional[np.ndarray] = None) -> dict:
         nc = len(customers)
         H = customers[0].H
         carr = (A.Customer * nc)(*[c.as_c() for c in customers])
@@ -327,7 +328,8 @@ class Context:
         if out_kind == "host":
             o = A.DsirpOut(A.MEM_HOST, None, None, None, None, None, None, agg, None)
             if totals:
-                res["totals"] = np.empty((nc, m), np.float64)
+                res["totals"] = (host_totals.reshape(nc, m) if host_totals is not None
+                                 else np.empty((nc, m), np.float64))
                 res["evaluated"] = np.empty((nc, m), np.uint8)
                 o.totals = res["totals"].ctypes.data
                 o.evaluated = res["evaluated"].ctypes.data

@@ -47,20 +47,32 @@ struct GenParams {
   int32_t kind;        // SCENDP_DIST_*
   int64_t lo;
   uint64_t span;       // uniform: hi - lo + 1
+  uint32_t span32;     // span when it is < 2^32 (the common case), else 0
   const double* cdf;   // poisson: P[0..cdf_len-1], device
   int32_t cdf_len;
   uint64_t seed;
   uint64_t first_index;
 };
 
+// next_below(span) = (x * span) >> 64 (scenario.hpp:33-37).  For span < 2^32
+// the 128-bit product's high word is (x_hi*span + (x_lo*span >> 32)) >> 32:
+// two 32x32->64 multiplies instead of a full 64x64 high multiply (exact: the
+// dropped low 32 bits of x_lo*span cannot carry into bit 64).
+__device__ __forceinline__ uint32_t uniform_draw(const GenParams& g, uint64_t x) {
+  if (g.span32) {
+    const uint64_t lo = static_cast<uint64_t>(static_cast<uint32_t>(x)) * g.span32;
+    const uint64_t hi = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * g.span32 + (lo >> 32);
+    return static_cast<uint32_t>(g.lo) + static_cast<uint32_t>(hi >> 32);
+  }
+  return static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
+}
+
 // One counter-based draw: DistributionSpec::sample for the kinds that use
 // exactly one next() per value (scenario.cpp:23-26; poisson: SURVEY App. A).
 __device__ __forceinline__ uint32_t draw_counter(const GenParams& g,
                                                  uint64_t stream, uint64_t row) {
   const uint64_t x = mix64(stream + row * kGamma);
-  if (g.kind == SCENDP_DIST_UNIFORM) {
-    return static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
-  }
+  if (g.kind == SCENDP_DIST_UNIFORM) return uniform_draw(g, x);
   // next_unit: ((x >> 11) + 1) * 2^-53, exact in fp64
   const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
   int32_t k = 0;

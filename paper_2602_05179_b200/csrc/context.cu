@@ -120,6 +120,17 @@ void finalize_agg(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
   }
 }
 
+void* mapped_host_alias(void* host) {
+  if (!host) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    (void)cudaGetLastError();  // unregistered pageable pointer
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return at.devicePointer;
+}
+
 }  // namespace scendp_host
 
 // ---- scendp_ctx members ------------------------------------------------------
@@ -145,6 +156,19 @@ void* scendp_ctx::pinned_agg(uint64_t bytes) {
   CUDA_CHECK(cudaMallocHost(&agg_pinned, bytes));
   agg_pinned_bytes = bytes;
   return agg_pinned;
+}
+
+void* scendp_ctx::pinned_stage(int idx, uint64_t bytes) {
+  if (stage_pinned_bytes[idx] >= bytes) return stage_pinned[idx];
+  if (stage_pinned[idx]) {
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    CUDA_CHECK(cudaFreeHost(stage_pinned[idx]));
+  }
+  stage_pinned[idx] = nullptr;
+  stage_pinned_bytes[idx] = 0;
+  CUDA_CHECK(cudaMallocHost(&stage_pinned[idx], bytes));
+  stage_pinned_bytes[idx] = bytes;
+  return stage_pinned[idx];
 }
 
 int scendp_ctx::timing_begin(int kind) {
@@ -243,6 +267,8 @@ void scendp_ctx_destroy(scendp_ctx* ctx) {
   for (int s = 0; s < kScrCount; ++s)
     if (ctx->scratch[s]) cudaFree(ctx->scratch[s]);
   if (ctx->agg_pinned) cudaFreeHost(ctx->agg_pinned);
+  for (void* p : ctx->stage_pinned)
+    if (p) cudaFreeHost(p);
   for (auto& p : ctx->event_pool) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);

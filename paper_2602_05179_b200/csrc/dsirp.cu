@@ -236,8 +236,11 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     const bool dev_out = out_dev_tiled || out_dev_ref;
     double* d_totals = nullptr;
     uint8_t* d_eval = nullptr;
+    double* zc_totals = host_out ? static_cast<double*>(mapped_host_alias(out->totals)) : nullptr;
     if (out->totals)
-      d_totals = dev_out ? out->totals : static_cast<double*>(ctx->scratch_get(kScrTotals, nc * m * 8));
+      d_totals = dev_out    ? out->totals
+                 : zc_totals ? zc_totals
+                             : static_cast<double*>(ctx->scratch_get(kScrTotals, nc * m * 8));
     if (out->evaluated)
       d_eval = dev_out ? out->evaluated : static_cast<uint8_t*>(ctx->scratch_get(kScrOut5, nc * m));
     const uint64_t tiles = (m + 31) / 32;
@@ -298,8 +301,10 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(nc) * kAggWords);
 
     if (host_out) {
-      if (out->totals)
-        ctx->copy(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost);
+      if (out->totals) {
+        if (zc_totals) ctx->stats.d2h_bytes += nc * m * 8;  // stored by the kernels
+        else ctx->copy(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost);
+      }
       if (out->evaluated)
         ctx->copy(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost);
     }

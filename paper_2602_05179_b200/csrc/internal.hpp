@@ -88,6 +88,10 @@ struct scendp_ctx {
   void sync();
   void allreduce_agg(void* dev_raw, uint64_t words);  // NCCL, if attached
   void* pinned_agg(uint64_t bytes);
+  // page-locked staging buffers (SCNB ingestion double buffering)
+  void* stage_pinned[2] = {nullptr, nullptr};
+  uint64_t stage_pinned_bytes[2] = {0, 0};
+  void* pinned_stage(int idx, uint64_t bytes);
 };
 
 namespace scendp_host {
@@ -95,6 +99,12 @@ namespace scendp_host {
 // Finalize raw aggregates (host): combine n shard records per candidate.
 void finalize_agg(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
                   scendp_agg* out);
+
+// Device alias of a page-locked, UVA-mapped host buffer (cudaMallocHost /
+// cudaHostAlloc / cudaHostRegister), or nullptr for pageable memory.  Per-
+// scenario totals bound for such a buffer are stored by the DP kernels
+// straight over PCIe while they run, instead of a D2H copy after them.
+void* mapped_host_alias(void* host);
 
 // C-ABI wrapper: run `f`, translate exceptions to a status.
 template <typename F>

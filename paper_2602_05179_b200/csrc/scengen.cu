@@ -39,7 +39,7 @@ gen_counter_kernel(GenParams g, uint64_t rows, uint64_t count, uint32_t* out) {
     for (uint64_t r = 0; r < rows; ++r) {
       const uint64_t x = mix64(st);
       st += kGamma;
-      dst[r * kTile] = static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
+      dst[r * kTile] = uniform_draw(g, x);
     }
   } else {
     uint64_t st = stream;
@@ -172,6 +172,7 @@ GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_
   g.kind = d->kind;
   g.lo = d->lo;
   g.span = static_cast<uint64_t>(d->hi - d->lo) + 1;
+  g.span32 = g.span < (uint64_t{1} << 32) ? static_cast<uint32_t>(g.span) : 0u;
   g.seed = d->seed;
   g.first_index = first_index;
   if (d->kind == SCENDP_DIST_POISSON) {
@@ -225,6 +226,7 @@ void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t co
   ctx->count_launch();
 }
 
+template void launch_to_tiled<uint32_t>(scendp_ctx*, const uint32_t*, uint64_t, uint64_t, uint32_t*);
 template void launch_from_tiled<double>(scendp_ctx*, const double*, uint64_t, uint64_t, double*);
 template void launch_from_tiled<int32_t>(scendp_ctx*, const int32_t*, uint64_t, uint64_t, int32_t*);
 template void launch_from_tiled<uint8_t>(scendp_ctx*, const uint8_t*, uint64_t, uint64_t, uint8_t*);

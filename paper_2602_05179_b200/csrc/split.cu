@@ -327,6 +327,46 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
             f[i] = fi;
           }
         }
+      } else if (!a.hard && a.pen_lmax > 0 && ld[n] <= static_cast<int64_t>(a.pen_lmax)) {
+        // penalized, exact integral data: the O(n) decomposition of
+        // split_penal.cuh without its ring limits -- window A = {L_i - L_p
+        // <= Q} (deque of f, earliest minimum) and prefix B before it (running
+        // minimum of g(p) = f(p) - beta L_p); B wins ties (earlier indices).
+        // Every value is an integer below 2^31, so each fp64 op is exact and
+        // equals the reference's ((f + dist_i) + ret_i) + beta * excess.
+        int head = 0, tail = 0, lo = 0, bidx = -1;
+        double bmin = kInfD;
+        dq[tail++] = 0;
+        const double beta = a.beta;
+        for (int i = 1; i <= n; ++i) {
+          while (lo < i && ld[i] - ld[lo] > a.Q) {
+            const double g = f[lo] - beta * static_cast<double>(ld[lo]);
+            if (g < bmin) {
+              bmin = g;
+              bidx = lo;
+            }
+            ++lo;
+          }
+          while (head < tail && dq[head] < lo) ++head;
+          const double candA = head < tail ? (f[dq[head]] + dist[i]) + ret[i] : kInfD;
+          const double candB = bidx >= 0 ? ((bmin + dist[i]) + ret[i]) +
+                                               beta * static_cast<double>(ld[i] - a.Q)
+                                         : kInfD;
+          const bool useB = candB <= candA;
+          v = useB ? candB : candA;
+          const int32_t bestp = useB ? bidx : dq[head];
+          rcs[i] = rcs[bestp] + 1;
+          if (FULL) {
+            Vout[static_cast<uint64_t>(i) * kTile] = v;
+            Cout[static_cast<uint64_t>(i) * kTile] = bestp;
+          }
+          if (i < n) {
+            const double fi = (v + c0[i]) - dist[i + 1];
+            while (tail > head && f[dq[tail - 1]] > fi) --tail;
+            dq[tail++] = i;
+            f[i] = fi;
+          }
+        }
       } else {
         for (int i = 1; i <= n; ++i) {
           double best = kInfD;
@@ -657,8 +697,13 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
     const bool out_dev_ref = out->mem_kind == SCENDP_MEM_DEVICE;
     double* d_totals = nullptr;
+    // host totals in pinned memory: the kernels write them over PCIe directly
+    double* zc_totals = nullptr;
+    if (out->totals && out->mem_kind == SCENDP_MEM_HOST)
+      zc_totals = static_cast<double*>(mapped_host_alias(out->totals));
     if (out->totals) {
       d_totals = (out_dev_tiled || out_dev_ref) ? out->totals
+                 : zc_totals                    ? zc_totals
                                                 : static_cast<double*>(ctx->scratch_get(kScrTotals, k * m * 8));
     }
     double* d_V = nullptr;
@@ -767,8 +812,10 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
 
     // copies back
     const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
-    if (out->totals && host_out)
-      ctx->copy(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost);
+    if (out->totals && host_out) {
+      if (zc_totals) ctx->stats.d2h_bytes += k * m * 8;  // stored by the kernels
+      else ctx->copy(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost);
+    }
     if (full && !out_dev_tiled) {
       // tiled -> reference layout [m][n+1]
       double* V_ref = out_dev_ref ? out->values : static_cast<double*>(ctx->scratch_get(kScrOut5, m * n1 * 8));

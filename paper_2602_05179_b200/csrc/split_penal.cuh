@@ -22,8 +22,9 @@
 // Per-thread shared state: the deque ring (K1's, f and position index) and a
 // position ring of the last kPosRing positions (f, L) that feeds the prefix
 // minimum as positions leave the window.  A window longer than the position
-// ring, a deque overflow or a load that would leave the exact int32 range
-// sends the scenario to the generic fp64 path.
+// ring or a deque overflow sends the scenario to the generic kernel's O(n)
+// form of the same decomposition; a load that would leave the exact int32
+// range sends it to the generic fp64 quadratic form.
 #pragma once
 
 constexpr int kPenThreads = 128;
@@ -94,15 +95,16 @@ split_penal_kernel(SplitArgs a) {
     dq_f[T] = f0;
     dq_i[T] = 0;
     int head = 1, tail = 2;  // slot counters (masked by kRing-1)
-    int32_t front_f = f0, front_i = 0, front_rc = 0, back_f = f0;
+    int32_t front_f = f0, front_i = 0, back_f = f0;
     int lo = 0;               // first position inside the window
     int32_t bmin = kPenInf;   // prefix minimum of g over [0, lo)
     int32_t bidx = -1, brc = 0;
     uint32_t load = 0;
 
-    for (int i = 1; i <= n; ++i) {
+    // one DP position; returns false when the scenario must take the generic
+    // path (window longer than the position ring, deque overflow)
+    auto step = [&](int i, uint32_t d) -> bool {
       const int sl = i - 1;
-      const uint32_t d = demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]);
       const int32_t Ai = s_tab[sl], Bi = s_tab[npad + sl];
       load += d;
       // positions leaving the window join the prefix B (in index order)
@@ -145,10 +147,7 @@ split_penal_kernel(SplitArgs a) {
       if (i < n) {
         const int32_t fi = v + Bi;
         // the position ring must hold [lo, i]
-        if (i - lo >= kPosRing - 1) {
-          ok = false;
-          break;
-        }
+        if (i - lo >= kPosRing - 1) return false;
         const int ps = (i & (kPosRing - 1)) * T;
         ps_f[ps] = fi;
         ps_l[ps] = load;
@@ -162,16 +161,36 @@ split_penal_kernel(SplitArgs a) {
           front_f = fi;
           front_i = i;
         }
-        if (tail - head >= kRing - 1) {
-          ok = false;
-          break;
-        }
+        if (tail - head >= kRing - 1) return false;
         const int ts = (tail & (kRing - 1)) * T;
         dq_f[ts] = fi;
         dq_i[ts] = i;
         ++tail;
         back_f = fi;
       }
+      return true;
+    };
+    // demands of slots s0..s0+3 (slot s = position s+1), loaded one chunk
+    // ahead of their use: the gathers hit L2 (C5 reuses each scenario tile
+    // for every tour), and without the prefetch every position waits on one
+    auto load4 = [&](int s0, uint32_t (&dd)[4]) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int sl = s0 + j;
+        dd[j] = sl < n ? demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]) : 0u;
+      }
+    };
+    uint32_t dc[4], dn[4] = {0u, 0u, 0u, 0u};
+    load4(0, dc);
+    for (int s0 = 0; s0 < n && ok; s0 += 4) {
+      if (s0 + 4 < n) load4(s0 + 4, dn);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = s0 + j + 1;
+        if (i <= n && ok) ok = step(i, dc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dc[j] = dn[j];
     }
     if (ok && load > lmax) ok = false;  // values may have left the exact range
     if (!ok) {

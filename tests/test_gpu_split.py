@@ -208,3 +208,53 @@ def test_penalized_exact_path_edges(ctx, oracle, reference):
     tot, V, cuts, rc, feas, agg = reference.expected_split(n, 15, 0, 2.0, c, tour, d2)
     np.testing.assert_array_equal(got["cuts"], cuts)
     np.testing.assert_array_equal(got["totals"][0], tot)
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_penalized_long_windows_cost_only_and_c2_shape(ctx, oracle, reference, full):
+    """Windows longer than K2-int's position ring take the generic kernel's
+    O(n) penalized form (not the quadratic one); C2-shaped penalized batch."""
+    n = 200
+    inst = RoutingInstance(n, 100, False, 10.0, oracle.make_random_instance(n, 1))
+    seed = oracle.derive_stream(1, TAG_SCENARIO, 0)
+    dem = oracle.generate(UNIFORM, 1, 10, seed, n, 3000)
+    dem[::7] = oracle.generate(UNIFORM, 0, 2, seed + 1, n, dem[::7].shape[0])  # windows ~100
+    tour = rand_tour(n, 9)
+    got = ctx.split_eval(inst, tour, dem, full=full)
+    if full:
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+            n, 100, 0, 10.0, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
+    else:
+        tot, (mean, fc, ic) = reference.split_costs(n, 100, 0, 10.0, inst.costs, tour, dem)
+    np.testing.assert_array_equal(got["totals"][0], tot)
+    assert got["agg"][0]["mean"] == mean
+
+
+def test_pinned_host_totals_are_written_in_place(ctx, oracle):
+    """Host totals in page-locked memory are stored by the kernels directly
+    (no D2H copy); results equal the pageable-buffer path."""
+    from paper_2602_05179_b200 import Customer, pinned_empty
+    n, m, k = 50, 5000, 3
+    inst = RoutingInstance(n, 100, True, 0.0, oracle.make_random_instance(n, 1))
+    tours = np.stack([rand_tour(n, s) for s in range(k)])
+    dem = oracle.generate(UNIFORM, 1, 10, 5, n, m)
+    want = ctx.split_eval(inst, tours, dem)
+    pin = pinned_empty(k * m, np.float64)
+    pin[:] = -1.0
+    ctx.kernel_stats(reset=True)
+    got = ctx.split_eval(inst, tours, dem, host_totals=pin)
+    st = ctx.kernel_stats(reset=True)
+    np.testing.assert_array_equal(pin.reshape(k, m), want["totals"])
+    assert got["agg"] == want["agg"]
+    assert st["d2h_bytes"] >= k * m * 8
+    H = 6
+    custs = [Customer(U=60, I0=30, H=H, fixed=np.full((H, 2), 20.0), unit=np.full((H, 2), 0.5))
+             for _ in range(2)]
+    dd = oracle.generate(UNIFORM, 0, 25, 3, 2 * H, 999)
+    want = ctx.dsirp_eval(custs, dd)
+    pin2 = pinned_empty(2 * 999, np.float64)
+    ctx.dsirp_eval(custs, dd, host_totals=pin2)
+    np.testing.assert_array_equal(pin2.reshape(2, 999), want["totals"])
