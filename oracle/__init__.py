@@ -310,9 +310,57 @@ class Reference:
                                               C.POINTER(C.c_double), C.POINTER(C.c_ulonglong),
                                               C.POINTER(C.c_ulonglong), _f64p, C.c_size_t]
 
+        L.ref_write_scenario_file.argtypes = [C.c_char_p, _u32p, C.c_size_t, C.c_size_t]
+        L.ref_read_scenario_file.argtypes = [C.c_char_p, C.POINTER(C.c_size_t),
+                                             C.POINTER(C.c_size_t), C.c_void_p, C.c_size_t]
+        L.ref_parse_instance_file.argtypes = [C.c_char_p, C.c_char_p]
+        L.ref_write_routing_instance.argtypes = [C.c_int, C.c_longlong, C.c_int, C.c_double,
+                                                 _f64p, C.c_char_p]
+        L.ref_experiment.argtypes = [C.c_int, C.c_int, C.c_longlong, C.c_double, _f64p,
+                                     C.c_int, C.c_longlong, C.c_longlong, C.c_double,
+                                     C.c_double, C.POINTER(C.c_size_t), C.c_size_t, C.c_int,
+                                     C.c_size_t, C.c_size_t, C.c_ulonglong, C.c_ulonglong,
+                                     C.c_uint, C.c_char_p]
+
     def _check(self, rc):
         if rc != 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
+
+    # ---- io.hpp --------------------------------------------------------------
+    def write_scenario_file(self, path, data):
+        data = np.ascontiguousarray(data, np.uint32)
+        self._check(self.lib.ref_write_scenario_file(str(path).encode(), data.ravel(),
+                                                     data.shape[1], data.shape[0]))
+
+    def read_scenario_file(self, path):
+        """(rows, count, data[count][rows]) or raises RuntimeError(message)."""
+        rows, count = C.c_size_t(), C.c_size_t()
+        self._check(self.lib.ref_read_scenario_file(str(path).encode(), C.byref(rows),
+                                                    C.byref(count), None, 0))
+        out = np.zeros(rows.value * count.value, np.uint32)
+        self._check(self.lib.ref_read_scenario_file(str(path).encode(), C.byref(rows),
+                                                    C.byref(count), out.ctypes.data, out.size))
+        return rows.value, count.value, out.reshape(count.value, rows.value)
+
+    def parse_instance_file(self, path, out_path):
+        self.lib.ref_parse_instance_file(str(path).encode(), str(out_path).encode())
+        return open(out_path).read()
+
+    def write_routing_instance(self, n, Q, hard, beta, costs, out_path):
+        self.lib.ref_write_routing_instance(n, Q, hard, beta,
+                                            np.ascontiguousarray(costs, np.float64).ravel(),
+                                            str(out_path).encode())
+        return open(out_path).read()
+
+    def experiment(self, which, n, Q, beta, costs, dist, m_list, reps, eval_size, ref_size,
+                   seed, evals, out_path, threads=1):
+        kind, lo, hi, mean, sd = dist
+        ms = (C.c_size_t * len(m_list))(*m_list)
+        self._check(self.lib.ref_experiment(
+            which, n, Q, beta, np.ascontiguousarray(costs, np.float64).ravel(), kind, lo, hi,
+            mean, sd, ms, len(m_list), reps, eval_size, ref_size, seed, evals, threads,
+            str(out_path).encode()))
+        return open(out_path).read()
 
     @staticmethod
     def _agg():

@@ -7,18 +7,22 @@
 // tests/ to pin the oracle restatement and as bench.py's CPU baseline
 // (`cpu_baseline.kind = "reference"`, `--impl reference`).
 #include <cstring>
+#include <fstream>
 #include <exception>
 #include <numeric>
 #include <string>
 #include <vector>
 
 #include "scendp/engine.hpp"
+#include "scendp/io.hpp"
 #include "scendp/minplus.hpp"
 #include "scendp/oracle.hpp"
 #include "scendp/oudp.hpp"
 #include "scendp/saa.hpp"
 #include "scendp/scenario.hpp"
 #include "scendp/split.hpp"
+
+#include "io_dump.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -396,6 +400,102 @@ REF_API int ref_improve_first_stage(int n, long long Q, double beta,
     *best_found_at = r.best_found_at;
     for (size_t k = 0; k < r.trajectory.size() && k < traj_cap; ++k)
       traj_best[k] = r.trajectory[k].best_value;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// ---- io.hpp (io.cpp): scenario files, instance grammar, reports ----------
+REF_API int ref_write_scenario_file(const char* path, const unsigned* data, size_t rows,
+                                    size_t count) {
+  try {
+    ScenarioBatch b;
+    b.rows = rows;
+    b.count = count;
+    b.data.assign(data, data + rows * count);
+    write_scenario_file(b, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+REF_API int ref_read_scenario_file(const char* path, size_t* rows, size_t* count,
+                                   unsigned* out, size_t cap) {
+  try {
+    ScenarioBatch b = read_scenario_file(path);
+    *rows = b.rows;
+    *count = b.count;
+    if (out && b.data.size() <= cap) std::memcpy(out, b.data.data(), b.data.size() * 4);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// parse_instance_file -> canonical dump (io_dump.hpp) or "error <what>"
+REF_API int ref_parse_instance_file(const char* path, const char* out_path) {
+  std::string text;
+  try {
+    text = io_dump::instance<ParsedInstance, RoutingInstance, DsirpInstance>(
+        parse_instance_file(path));
+  } catch (const std::exception& e) {
+    text = std::string("error ") + e.what() + "\n";
+  }
+  std::ofstream(out_path) << text;
+  return 0;
+}
+
+REF_API int ref_write_routing_instance(int n, long long Q, int hard, double beta,
+                                       const double* costs, const char* out_path) {
+  std::ofstream f(out_path);
+  write_routing_instance(make_inst(n, Q, hard, beta, costs), f);
+  return 0;
+}
+
+// SAA experiments (saa.cpp:191-443) -> write_report_csv.  which: 0 bias,
+// 1 convergence, 2 quality, 3 scaling, 4 time budget.
+REF_API int ref_experiment(int which, int n, long long Q, double beta, const double* costs,
+                           int kind, long long lo, long long hi, double mean, double sd,
+                           const size_t* m_list, size_t nm, int reps, size_t eval_size,
+                           size_t ref_size, unsigned long long seed,
+                           unsigned long long evals, unsigned threads,
+                           const char* out_path) {
+  try {
+    RoutingInstance inst = make_inst(n, Q, 0, beta, costs);
+    DistributionSpec d = make_dist(kind, lo, hi, mean, sd, 0);
+    ExperimentConfig cfg;
+    cfg.instance_label = "inst";
+    cfg.seed = seed;
+    cfg.backend = make_cfg(threads);
+    cfg.search_evaluations = evals;
+    std::vector<size_t> ms(m_list, m_list + nm);
+    ExperimentReport rep;
+    if (which == 0) rep = run_bias_experiment(inst, d, ms, reps, eval_size, ref_size, cfg);
+    else if (which == 1) rep = run_convergence_experiment(inst, d, ms, reps, cfg);
+    else if (which == 2) rep = run_quality_experiment(inst, d, ms, reps, eval_size, cfg);
+    else if (which == 3) {
+      ScalingOptions so;
+      so.sizes = ms;
+      so.modes = {cfg.backend};
+      so.target_evaluations = eval_size;
+      rep = run_scaling_benchmark(inst, d, so, cfg);
+    } else {
+      TimeBudgetOptions to;
+      to.budgets_seconds = {0.05, 0.1, 0.2};
+      to.modes = {cfg.backend};
+      to.train_size = eval_size;
+      rep = run_time_budget_experiment(inst, d, to, cfg);
+    }
+    RunMetadata meta;
+    meta.command = "experiment";
+    meta.seed = seed;
+    std::ofstream f(out_path);
+    write_report_csv(f, meta, rep.rows);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

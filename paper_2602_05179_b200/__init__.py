@@ -239,6 +239,34 @@ class Context:
                                               buf.ptr))
         return buf
 
+    # ---- SCNB files (io.cpp:276-344) ------------------------------------------
+    @staticmethod
+    def scnb_header(path: str):
+        """(rows, count) of an SCNB file (reference header checks and messages)."""
+        lib = A.load()
+        h = A.ScnbHeader()
+        A.check(lib.scendp_scnb_header_read(str(path).encode(), C.byref(h)))
+        return h.rows, h.count
+
+    @staticmethod
+    def scnb_write(path: str, data: np.ndarray):
+        """write_scenario_binary of a (count, rows) host array."""
+        lib = A.load()
+        arr = np.ascontiguousarray(data, np.uint32)
+        A.check(lib.scendp_scnb_write(str(path).encode(), arr.ctypes.data, arr.shape[1],
+                                      arr.shape[0]))
+
+    def scnb_load(self, path: str, first: int = 0, count: Optional[int] = None,
+                  tiled: bool = True) -> DeviceBuffer:
+        """Stream scenarios [first, first+count) of an SCNB file into HBM."""
+        rows, total = self.scnb_header(path)
+        count = total - first if count is None else count
+        buf = self.alloc(self.tiled_bytes(rows, count) if tiled else rows * count * 4)
+        A.check(self.lib.scendp_scnb_load(self.handle, str(path).encode(), first, count,
+                                          A.MEM_DEVICE_TILED if tiled else A.MEM_DEVICE,
+                                          buf.ptr))
+        return buf
+
     def to_tiled(self, src: DeviceBuffer, rows: int, count: int) -> DeviceBuffer:
         dst = self.alloc(self.tiled_bytes(rows, count))
         A.check(self.lib.scendp_scenarios_to_tiled(self.handle, src.ptr, rows, count, dst.ptr))

@@ -95,6 +95,10 @@ class KernelStats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
+class ScnbHeader(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("count", C.c_uint64)]
+
+
 # Every symbol include/scendp_cuda.h declares, with its ctypes signature.
 SIGNATURES = {
     "scendp_ctx_create": (C.c_int, [C.POINTER(Opts), C.POINTER(C.c_void_p)]),
@@ -117,6 +121,10 @@ SIGNATURES = {
                                        C.c_uint64, C.c_uint32, C.c_void_p]),
     "scendp_scenarios_to_tiled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                             C.c_void_p]),
+    "scendp_scnb_header_read": (C.c_int, [C.c_char_p, C.POINTER(ScnbHeader)]),
+    "scendp_scnb_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                   C.c_void_p]),
+    "scendp_scnb_write": (C.c_int, [C.c_char_p, C.c_void_p, C.c_uint64, C.c_uint64]),
     "scendp_agg_finalize": (C.c_int, [C.POINTER(AggRaw), C.c_uint32, C.c_uint32,
                                       C.POINTER(Agg)]),
     "scendp_split_eval": (C.c_int, [C.c_void_p, C.POINTER(Routing), C.c_void_p, C.c_uint32,

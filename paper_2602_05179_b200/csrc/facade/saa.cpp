@@ -130,15 +130,53 @@ GiantTour apply_move(const GiantTour& cur, const Scan& s) {
   return cand;
 }
 
-// Training set resident on one device in the tiled layout.
-struct DeviceTrain {
+// Scenario set resident on one device in the tiled layout.
+struct DeviceSet {
   scendp_ctx* ctx = nullptr;
   void* tiled = nullptr;
   std::size_t rows = 0, count = 0;
-  ~DeviceTrain() {
+  DeviceSet() = default;
+  DeviceSet(const DeviceSet&) = delete;
+  DeviceSet& operator=(const DeviceSet&) = delete;
+  ~DeviceSet() {
     if (tiled) scendp_device_free(ctx, tiled);
   }
 };
+using DeviceTrain = DeviceSet;
+
+// A host batch (reference layout) -> tiled device set.
+void upload_set(scendp_ctx* ctx, const ScenarioBatch& b, DeviceSet& ds) {
+  ds.ctx = ctx;
+  ds.rows = b.rows;
+  ds.count = b.count;
+  void* ref = nullptr;
+  const std::uint64_t bytes = static_cast<std::uint64_t>(b.rows) * b.count * 4;
+  detail::check(scendp_device_alloc(ctx, bytes, &ref));
+  scendp_status s = scendp_memcpy(ctx, ref, b.data.data(), bytes, 0, 0);
+  if (s == SCENDP_OK) s = scendp_device_alloc(ctx, scendp_tiled_bytes(b.rows, b.count), &ds.tiled);
+  if (s == SCENDP_OK)
+    s = scendp_scenarios_to_tiled(ctx, static_cast<const std::uint32_t*>(ref), b.rows, b.count,
+                                  static_cast<std::uint32_t*>(ds.tiled));
+  scendp_device_free(ctx, ref);
+  detail::check(s);
+}
+
+// generate_scenarios(dist, rows, 1, count) produced directly in HBM (K4,
+// bit-identical to the host generator for uniform and poisson): the SAA
+// experiments never materialize a training or evaluation batch on the host.
+void generate_set(scendp_ctx* ctx, const DistributionSpec& dist, std::size_t rows,
+                  std::size_t count, DeviceSet& ds) {
+  dist.validate();
+  ds.ctx = ctx;
+  ds.rows = rows;
+  ds.count = count;
+  detail::check(scendp_device_alloc(ctx, std::max<std::uint64_t>(256, scendp_tiled_bytes(rows, count)),
+                                    &ds.tiled));
+  const scendp_dist cd = detail::to_c(dist);
+  if (count)
+    detail::check(scendp_gen_scenarios(ctx, &cd, rows, 0, count, SCENDP_MEM_DEVICE_TILED,
+                                       static_cast<std::uint32_t*>(ds.tiled)));
+}
 
 std::vector<scendp_agg> score_batch(const DeviceTrain& dt, const RoutingInstance& inst,
                                     const std::vector<GiantTour>& cands) {
@@ -215,43 +253,15 @@ double out_of_sample_eval(const RoutingInstance& instance, const GiantTour& tour
   return *res.mean_cost;
 }
 
-SearchResult improve_first_stage(const RoutingInstance& instance, const ScenarioBatch& train,
-                                 const BackendConfig& backend, const SearchBudget& budget) {
-  instance.validate();
-  if (instance.hard)
-    throw std::invalid_argument(
-        "first-stage search scores candidates by expected penalized cost; run the instance in "
-        "penalized mode");
-  if (train.count == 0) throw std::invalid_argument("training batch is empty");
-  backend.validate();
-  const int n = instance.n;
-  if (train.rows != static_cast<std::size_t>(n))
-    throw std::invalid_argument("demand column has " + std::to_string(train.rows) +
-                                " entries, instance has " + std::to_string(n) + " customers");
-  const std::uint64_t t0 = detail::now_ns();
+namespace {
 
-  // upload the training set once (tiled layout) on the first device
-  const int dev = detail::devices_of(backend).front();
-  detail::DeviceSlot& slot = detail::device_slot(dev);
-  std::lock_guard<std::mutex> guard(slot.mu);
-  detail::check(scendp_ctx_set_max_batch(slot.ctx, 0));
-  DeviceTrain dt;
-  dt.ctx = slot.ctx;
-  dt.rows = train.rows;
-  dt.count = train.count;
-  {
-    void* ref = nullptr;
-    const std::uint64_t bytes = static_cast<std::uint64_t>(train.rows) * train.count * 4;
-    detail::check(scendp_device_alloc(dt.ctx, bytes, &ref));
-    scendp_status s = scendp_memcpy(dt.ctx, ref, train.data.data(), bytes, 0, 0);
-    if (s == SCENDP_OK) s = scendp_device_alloc(dt.ctx, scendp_tiled_bytes(train.rows, train.count), &dt.tiled);
-    if (s == SCENDP_OK)
-      s = scendp_scenarios_to_tiled(dt.ctx, static_cast<const std::uint32_t*>(ref), train.rows,
-                                    train.count, static_cast<std::uint32_t*>(dt.tiled));
-    scendp_device_free(dt.ctx, ref);
-    detail::check(s);
-  }
-  const double band = (static_cast<double>(train.count) + 2.0) * 0x1.0p-52;
+// The first-improvement search of improve_first_stage (saa.cpp:106-189) on a
+// training set already resident in HBM.  `t0` is the caller's start time (the
+// reference's clock starts after validation, saa.cpp:106-120).
+SearchResult search_on(const RoutingInstance& instance, const DeviceSet& dt,
+                       const SearchBudget& budget, std::uint64_t t0) {
+  const int n = instance.n;
+  const double band = (static_cast<double>(dt.count) + 2.0) * 0x1.0p-52;
 
   SearchResult out;
   auto over_budget = [&] {
@@ -336,6 +346,292 @@ SearchResult improve_first_stage(const RoutingInstance& instance, const Scenario
       scan = Scan{};
       normalize(scan, n);
     }
+  }
+  return out;
+}
+
+void check_search_inputs(const RoutingInstance& instance, std::size_t rows, std::size_t count) {
+  instance.validate();
+  if (instance.hard)
+    throw std::invalid_argument(
+        "first-stage search scores candidates by expected penalized cost; run the instance in "
+        "penalized mode");
+  if (count == 0) throw std::invalid_argument("training batch is empty");
+  if (rows != static_cast<std::size_t>(instance.n))
+    throw std::invalid_argument("demand column has " + std::to_string(rows) +
+                                " entries, instance has " + std::to_string(instance.n) +
+                                " customers");
+}
+
+}  // namespace
+
+SearchResult improve_first_stage(const RoutingInstance& instance, const ScenarioBatch& train,
+                                 const BackendConfig& backend, const SearchBudget& budget) {
+  check_search_inputs(instance, train.rows, train.count);
+  backend.validate();
+  // upload the training set once (tiled layout) on the first device
+  detail::DeviceSlot& slot = detail::device_slot(detail::devices_of(backend).front());
+  std::lock_guard<std::mutex> guard(slot.mu);
+  detail::check(scendp_ctx_set_max_batch(slot.ctx, 0));
+  DeviceSet dt;
+  const std::uint64_t t0 = detail::now_ns();
+  upload_set(slot.ctx, train, dt);
+  return search_on(instance, dt, budget, t0);
+}
+
+// ---------------------------------------------------------------------------
+// SAA experiments (saa.cpp:191-443).  Same seeds, streams, row order and
+// statistics as the reference; every training, evaluation and reference set
+// is generated directly in HBM, every search and out-of-sample evaluation
+// runs on it, and only means cross back to the host.
+namespace {
+
+struct Stats {
+  double mean = 0.0, se = 0.0, stddev = 0.0;
+};
+
+// sample mean, sample standard deviation (n-1) and standard error
+Stats summarize(const std::vector<double>& xs) {
+  Stats st;
+  if (xs.empty()) return st;
+  double sum = 0.0;
+  for (double x : xs) sum += x;
+  st.mean = sum / static_cast<double>(xs.size());
+  if (xs.size() < 2) return st;
+  double ss = 0.0;
+  for (double x : xs) ss += (x - st.mean) * (x - st.mean);
+  st.stddev = std::sqrt(ss / static_cast<double>(xs.size() - 1));
+  st.se = st.stddev / std::sqrt(static_cast<double>(xs.size()));
+  return st;
+}
+
+std::uint64_t rep_index(std::size_t mi, int rep) {
+  return static_cast<std::uint64_t>(mi) * 1000003ULL + static_cast<std::uint64_t>(rep);
+}
+
+DistributionSpec reseeded(DistributionSpec d, std::uint64_t seed) {
+  d.seed = seed;
+  return d;
+}
+
+// One experiment session: the first device of the config, locked for the
+// whole experiment.
+struct Session {
+  detail::DeviceSlot& slot;
+  std::lock_guard<std::mutex> guard;
+  explicit Session(const BackendConfig& b)
+      : slot(detail::device_slot(detail::devices_of(b).front())), guard(slot.mu) {
+    detail::check(scendp_ctx_set_max_batch(slot.ctx, 0));
+  }
+  scendp_ctx* ctx() const { return slot.ctx; }
+};
+
+// Train on a fresh set (stream index rep_index(mi, rep)) with the config's
+// evaluation budget.
+SearchResult train_and_search(Session& ss, const RoutingInstance& inst,
+                              const DistributionSpec& demand, const ExperimentConfig& cfg,
+                              std::size_t mi, int rep, std::size_t m) {
+  DeviceSet train;
+  generate_set(ss.ctx(), reseeded(demand, derive_stream(cfg.seed, kStreamExperiment, rep_index(mi, rep))),
+               static_cast<std::size_t>(inst.n), m, train);
+  check_search_inputs(inst, train.rows, train.count);
+  const std::uint64_t t0 = detail::now_ns();
+  return search_on(inst, train, {cfg.search_evaluations, std::numeric_limits<double>::infinity()},
+                   t0);
+}
+
+ReportRow row(const std::string& exp, const ExperimentConfig& cfg, std::uint64_t m,
+              std::int64_t rep, const std::string& metric, double value, double ms = 0.0) {
+  return ReportRow{exp, cfg.instance_label, m, rep, metric, value, ms, cfg.seed};
+}
+
+}  // namespace
+
+ExperimentReport run_bias_experiment(const RoutingInstance& instance,
+                                     const DistributionSpec& demand,
+                                     const std::vector<std::size_t>& m_list, int reps,
+                                     std::size_t eval_size, std::size_t reference_size,
+                                     const ExperimentConfig& config) {
+  if (reps < 2) throw std::invalid_argument("bias experiment needs reps >= 2");
+  const std::size_t n = static_cast<std::size_t>(instance.n);
+  Session ss(config.backend);
+  DeviceSet eval;
+  generate_set(ss.ctx(), reseeded(demand, derive_stream(config.seed, kStreamEvaluation, 0)), n,
+               eval_size, eval);
+  ExperimentReport rep_out;
+  const std::string exp = "saa_bias";
+  double best_oos = std::numeric_limits<double>::infinity();
+  GiantTour best_tour;
+  for (std::size_t mi = 0; mi < m_list.size(); ++mi) {
+    const std::size_t m = m_list[mi];
+    std::vector<double> zs, oos;
+    for (int rep = 0; rep < reps; ++rep) {
+      const SearchResult sr = train_and_search(ss, instance, demand, config, mi, rep, m);
+      const double o = sequential_mean(eval, instance, sr.tour);
+      zs.push_back(sr.value);
+      oos.push_back(o);
+      if (o < best_oos) {
+        best_oos = o;
+        best_tour = sr.tour;
+      }
+      rep_out.rows.push_back(row(exp, config, m, rep, "in_sample", sr.value));
+      rep_out.rows.push_back(row(exp, config, m, rep, "out_of_sample", o));
+      rep_out.rows.push_back(row(exp, config, m, rep, "candidates", static_cast<double>(sr.evaluations)));
+      rep_out.rows.push_back(row(exp, config, m, rep, "best_found_at", static_cast<double>(sr.best_found_at)));
+    }
+    const Stats z = summarize(zs), o = summarize(oos);
+    rep_out.rows.push_back(row(exp, config, m, -1, "in_sample_mean", z.mean));
+    rep_out.rows.push_back(row(exp, config, m, -1, "in_sample_se", z.se));
+    rep_out.rows.push_back(row(exp, config, m, -1, "out_of_sample_mean", o.mean));
+    rep_out.rows.push_back(row(exp, config, m, -1, "out_of_sample_se", o.se));
+  }
+  if (reference_size > 0 && !best_tour.order.empty()) {
+    DeviceSet ref;
+    generate_set(ss.ctx(), reseeded(demand, derive_stream(config.seed, kStreamEvaluation, 1)), n,
+                 reference_size, ref);
+    rep_out.rows.push_back(row(exp, config, 0, -1, "reference_value",
+                               sequential_mean(ref, instance, best_tour)));
+  }
+  return rep_out;
+}
+
+ExperimentReport run_convergence_experiment(const RoutingInstance& instance,
+                                            const DistributionSpec& demand,
+                                            const std::vector<std::size_t>& m_list, int reps,
+                                            const ExperimentConfig& config) {
+  if (m_list.size() < 2 || m_list.back() < 100 * m_list.front())
+    throw std::invalid_argument(
+        "convergence experiment needs m values spanning at least two decades");
+  Session ss(config.backend);
+  ExperimentReport out;
+  const std::string exp = "saa_convergence";
+  std::vector<double> lx, ly;
+  for (std::size_t mi = 0; mi < m_list.size(); ++mi) {
+    const std::size_t m = m_list[mi];
+    std::vector<double> zs;
+    for (int rep = 0; rep < reps; ++rep) {
+      const SearchResult sr = train_and_search(ss, instance, demand, config, mi, rep, m);
+      zs.push_back(sr.value);
+      out.rows.push_back(row(exp, config, m, rep, "in_sample", sr.value));
+      out.rows.push_back(row(exp, config, m, rep, "candidates", static_cast<double>(sr.evaluations)));
+    }
+    const Stats z = summarize(zs);
+    out.rows.push_back(row(exp, config, m, -1, "in_sample_mean", z.mean));
+    out.rows.push_back(row(exp, config, m, -1, "in_sample_std", z.stddev));
+    if (z.stddev > 0.0) {
+      lx.push_back(std::log(static_cast<double>(m)));
+      ly.push_back(std::log(z.stddev));
+    }
+  }
+  out.rows.push_back(row(exp, config, 0, -1, "log_std_slope",
+                         lx.size() >= 2 ? least_squares_slope(lx, ly) : 0.0));
+  return out;
+}
+
+ExperimentReport run_quality_experiment(const RoutingInstance& instance,
+                                        const DistributionSpec& demand,
+                                        const std::vector<std::size_t>& m_list, int reps,
+                                        std::size_t eval_size, const ExperimentConfig& config) {
+  Session ss(config.backend);
+  DeviceSet eval;
+  generate_set(ss.ctx(), reseeded(demand, derive_stream(config.seed, kStreamEvaluation, 0)),
+               static_cast<std::size_t>(instance.n), eval_size, eval);
+  ExperimentReport out;
+  const std::string exp = "quality_vs_scenarios";
+  for (std::size_t mi = 0; mi < m_list.size(); ++mi) {
+    const std::size_t m = m_list[mi];
+    std::vector<double> oos;
+    for (int rep = 0; rep < reps; ++rep) {
+      const SearchResult sr = train_and_search(ss, instance, demand, config, mi, rep, m);
+      const double o = sequential_mean(eval, instance, sr.tour);
+      oos.push_back(o);
+      out.rows.push_back(row(exp, config, m, rep, "out_of_sample", o));
+    }
+    const Stats o = summarize(oos);
+    out.rows.push_back(row(exp, config, m, -1, "out_of_sample_mean", o.mean));
+    out.rows.push_back(row(exp, config, m, -1, "out_of_sample_se", o.se));
+  }
+  return out;
+}
+
+ExperimentReport run_scaling_benchmark(const RoutingInstance& instance,
+                                       const DistributionSpec& demand,
+                                       const ScalingOptions& options,
+                                       const ExperimentConfig& config) {
+  ExperimentReport out;
+  const std::string exp = "scaling";
+  GiantTour tour;
+  tour.order.resize(instance.n);
+  std::iota(tour.order.begin(), tour.order.end(), 1);
+  const DistributionSpec dist = reseeded(demand, derive_stream(config.seed, kStreamScenario, 1));
+  for (const BackendConfig& mode : options.modes) {
+    const std::string label = mode_label(mode);
+    std::vector<double> lx, ly;
+    // warm-up (context creation, first-launch costs) outside the timings
+    batched_split_costs_generated(instance, tour, dist,
+                                  std::min<std::size_t>(options.sizes.front(), 1000), mode);
+    for (std::size_t size : options.sizes) {
+      const std::size_t reps = std::max<std::size_t>(1, options.target_evaluations / size);
+      const std::uint64_t t0 = detail::now_ns();
+      for (std::size_t r = 0; r < reps; ++r)
+        batched_split_costs_generated(instance, tour, dist, size, mode);
+      const double ms = detail::ms_since(t0) / static_cast<double>(reps);
+      out.rows.push_back(row(exp, config, size, -1, label + "_wall_ms", ms, ms));
+      lx.push_back(std::log(static_cast<double>(size)));
+      ly.push_back(std::log(ms));
+    }
+    out.rows.push_back(row(exp, config, 0, -1, label + "_loglog_slope", least_squares_slope(lx, ly)));
+  }
+  return out;
+}
+
+ExperimentReport run_time_budget_experiment(const RoutingInstance& instance,
+                                            const DistributionSpec& demand,
+                                            const TimeBudgetOptions& options,
+                                            const ExperimentConfig& config) {
+  if (options.budgets_seconds.empty() ||
+      !std::is_sorted(options.budgets_seconds.begin(), options.budgets_seconds.end()))
+    throw std::invalid_argument("budgets must be ascending and nonempty");
+  ExperimentReport out;
+  const std::string exp = "time_budget";
+  const DistributionSpec tdist = reseeded(demand, derive_stream(config.seed, kStreamScenario, 0));
+  for (const BackendConfig& mode : options.modes) {
+    const std::string label = mode_label(mode);
+    SearchResult sr;
+    {
+      Session ss(mode);
+      DeviceSet train;
+      generate_set(ss.ctx(), tdist, static_cast<std::size_t>(instance.n), options.train_size, train);
+      check_search_inputs(instance, train.rows, train.count);
+      const std::uint64_t t0 = detail::now_ns();
+      SearchBudget budget;
+      budget.max_wall_seconds = options.budgets_seconds.back();
+      sr = search_on(instance, train, budget, t0);
+    }
+    for (std::size_t bi = 0; bi < options.budgets_seconds.size(); ++bi) {
+      const double limit = options.budgets_seconds[bi] * 1000.0;
+      // last trajectory point inside the budget (the first stands in when
+      // even the first evaluation overran it)
+      TrajectoryPoint at = sr.trajectory.front();
+      for (const TrajectoryPoint& p : sr.trajectory) {
+        if (p.elapsed_ms > limit) break;
+        at = p;
+      }
+      const auto b = static_cast<std::int64_t>(bi);
+      out.rows.push_back(row(exp, config, options.train_size, b, label + "_budget_seconds",
+                             options.budgets_seconds[bi]));
+      out.rows.push_back(row(exp, config, options.train_size, b, label + "_best_cost",
+                             at.best_value, at.elapsed_ms));
+      out.rows.push_back(row(exp, config, options.train_size, b, label + "_candidates",
+                             static_cast<double>(at.evaluations), at.elapsed_ms));
+    }
+  }
+  if (!options.scaling_sizes.empty()) {
+    ScalingOptions sc;
+    sc.sizes = options.scaling_sizes;
+    sc.modes = options.modes;
+    const ExperimentReport sub = run_scaling_benchmark(instance, demand, sc, config);
+    out.rows.insert(out.rows.end(), sub.rows.begin(), sub.rows.end());
   }
   return out;
 }

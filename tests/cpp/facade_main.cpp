@@ -7,17 +7,27 @@
 //   facade_main dsirp <U> <I0> <H> <R> <seed> <m>
 //   facade_main saa <n> <Q> <beta> <inst_seed> <scen_seed> <m> <max_evals> <kbatch>
 //   facade_main gen <kind> <lo> <hi> <mean> <std> <seed> <entities> <steps> <count>
+//   facade_main io-write <path> <rows> <count> <seed>        (no GPU)
+//   facade_main io-read <path>                               (no GPU)
+//   facade_main io-parse <path> <out>                        (no GPU)
+//   facade_main io-write-inst <n> <Q> <hard> <beta> <inst_seed> <out>   (no GPU)
+//   facade_main exp <which> <n> <Q> <beta> <inst_seed> <kind> <lo> <hi> <mean> <sd>
+//                   <seed> <evals> <reps> <eval_size> <ref_size> <out> <m...>
 #include <cstdio>
+#include <fstream>
 #include <cstdlib>
 #include <exception>
 #include <numeric>
 #include <string>
 #include <vector>
 
+#include "scendp/io.hpp"
 #include "scendp/oudp.hpp"
 #include "scendp/saa.hpp"
 #include "scendp/scenario.hpp"
 #include "scendp/split.hpp"
+
+#include "../../oracle/io_dump.hpp"
 
 using namespace scendp;
 
@@ -182,6 +192,96 @@ int run_gen(char** a) {
   return 0;
 }
 
+int run_io_write(char** a) {
+  ScenarioBatch b;
+  b.rows = std::strtoull(a[1], nullptr, 10);
+  b.count = std::strtoull(a[2], nullptr, 10);
+  SplitMix64 rng(std::strtoull(a[3], nullptr, 10));
+  b.data.resize(b.rows * b.count);
+  for (auto& v : b.data) v = static_cast<std::uint32_t>(rng.next() >> 40);
+  write_scenario_file(b, a[0]);
+  print_ivec("data", b.data);
+  return 0;
+}
+
+int run_io_read(char** a) {
+  ScenarioBatch b = read_scenario_file(a[0]);
+  std::printf("rows %zu count %zu\n", b.rows, b.count);
+  print_ivec("data", b.data);
+  return 0;
+}
+
+int run_io_parse(char** a) {
+  std::string text;
+  try {
+    text = io_dump::instance<ParsedInstance, RoutingInstance, DsirpInstance>(
+        parse_instance_file(a[0]));
+  } catch (const std::exception& e) {
+    text = std::string("error ") + e.what() + "\n";
+  }
+  std::ofstream(a[1]) << text;
+  return 0;
+}
+
+int run_io_write_inst(char** a) {
+  RoutingInstance inst = make_random_instance(std::atoi(a[0]), std::strtoull(a[4], nullptr, 10),
+                                              std::atoll(a[1]), std::atoi(a[2]) != 0,
+                                              std::atof(a[3]));
+  std::ofstream f(a[5]);
+  write_routing_instance(inst, f);
+  return 0;
+}
+
+// SAA experiment -> write_report_csv (same arguments as ref_experiment)
+int run_exp(char** a, int nm) {
+  const int which = std::atoi(a[0]);
+  const int n = std::atoi(a[1]);
+  RoutingInstance inst = make_random_instance(n, std::strtoull(a[4], nullptr, 10),
+                                              std::atoll(a[2]), false, std::atof(a[3]));
+  DistributionSpec d;
+  const int kind = std::atoi(a[5]);
+  d.kind = kind == 0 ? DistributionSpec::Kind::kUniformInt
+                     : (kind == 1 ? DistributionSpec::Kind::kTruncatedNormal
+                                  : DistributionSpec::Kind::kPoisson);
+  d.lo = std::atoll(a[6]);
+  d.hi = std::atoll(a[7]);
+  d.mean = std::atof(a[8]);
+  d.stddev = std::atof(a[9]);
+  ExperimentConfig cfg;
+  cfg.instance_label = "inst";
+  cfg.seed = std::strtoull(a[10], nullptr, 10);
+  cfg.backend = BackendConfig::gpu();
+  cfg.search_evaluations = std::strtoull(a[11], nullptr, 10);
+  const int reps = std::atoi(a[12]);
+  const std::size_t eval_size = std::strtoull(a[13], nullptr, 10);
+  const std::size_t ref_size = std::strtoull(a[14], nullptr, 10);
+  std::vector<std::size_t> ms;
+  for (int k = 0; k < nm; ++k) ms.push_back(std::strtoull(a[16 + k], nullptr, 10));
+  ExperimentReport rep;
+  if (which == 0) rep = run_bias_experiment(inst, d, ms, reps, eval_size, ref_size, cfg);
+  else if (which == 1) rep = run_convergence_experiment(inst, d, ms, reps, cfg);
+  else if (which == 2) rep = run_quality_experiment(inst, d, ms, reps, eval_size, cfg);
+  else if (which == 3) {
+    ScalingOptions so;
+    so.sizes = ms;
+    so.modes = {cfg.backend};
+    so.target_evaluations = eval_size;
+    rep = run_scaling_benchmark(inst, d, so, cfg);
+  } else {
+    TimeBudgetOptions to;
+    to.budgets_seconds = {0.05, 0.1, 0.2};
+    to.modes = {cfg.backend};
+    to.train_size = eval_size;
+    rep = run_time_budget_experiment(inst, d, to, cfg);
+  }
+  RunMetadata meta;
+  meta.command = "experiment";
+  meta.seed = cfg.seed;
+  std::ofstream f(a[15]);
+  write_report_csv(f, meta, rep.rows);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -192,6 +292,11 @@ int main(int argc, char** argv) {
     if (mode == "dsirp" && argc == 8) return run_dsirp(argv + 2);
     if (mode == "saa" && argc == 10) return run_saa(argv + 2);
     if (mode == "gen" && argc == 11) return run_gen(argv + 2);
+    if (mode == "io-write" && argc == 6) return run_io_write(argv + 2);
+    if (mode == "io-read" && argc == 3) return run_io_read(argv + 2);
+    if (mode == "io-parse" && argc == 4) return run_io_parse(argv + 2);
+    if (mode == "io-write-inst" && argc == 8) return run_io_write_inst(argv + 2);
+    if (mode == "exp" && argc >= 19) return run_exp(argv + 2, argc - 18);
   } catch (const std::exception& e) {
     std::printf("exception %s\n", e.what());
     return 1;

@@ -118,3 +118,55 @@ def test_facade_generator(reference, oracle):
     got = run("gen", 2, 0, 47, 5.0, 1, 79, 6, 1, 30)
     np.testing.assert_array_equal(got["data"], oracle.generate(POISSON, 0, 47, 79, 6, 30,
                                                                mean=5.0).ravel())
+
+
+# ---- SAA experiment suite (saa.cpp:191-443) ---------------------------------
+EXP_N, EXP_Q, EXP_BETA, EXP_SEED = 12, 30, 5.0, 1
+
+
+def _exp(reference, tmp_path, which, m_list, reps, eval_size, ref_size, evals, seed=7,
+         dist=(UNIFORM, 1, 10, 0.0, 1.0)):
+    costs = reference.make_random_instance(EXP_N, EXP_SEED)
+    want = reference.experiment(which, EXP_N, EXP_Q, EXP_BETA, costs, dist, m_list, reps,
+                                eval_size, ref_size, seed, evals, tmp_path / "ref.csv")
+    kind, lo, hi, mean, sd = dist
+    run("exp", which, EXP_N, EXP_Q, EXP_BETA, EXP_SEED, kind, lo, hi, mean, sd, seed, evals,
+        reps, eval_size, ref_size, tmp_path / "ours.csv", *m_list)
+    return (tmp_path / "ours.csv").read_text(), want
+
+
+@pytest.mark.parametrize("which,m_list,reps,eval_size,ref_size", [
+    (0, [20, 300], 2, 700, 1500),      # bias, with the reference-value row
+    (1, [10, 100, 1000], 3, 0, 0),     # convergence (two decades) + log-log slope
+    (2, [50, 400], 2, 900, 0),         # quality vs scenarios
+])
+def test_saa_experiment_reports_match_reference(reference, tmp_path, which, m_list, reps,
+                                                eval_size, ref_size):
+    """Report CSVs (write_report_csv) of the GPU experiment suite equal the
+    reference's byte for byte: same training/evaluation streams, searches,
+    out-of-sample means and statistics."""
+    got, want = _exp(reference, tmp_path, which, m_list, reps, eval_size, ref_size, evals=40)
+    assert got == want
+
+
+def test_saa_experiment_poisson_free_tnormal(reference, tmp_path):
+    """tnormal training sets are generated on the GPU (CUDA libm); the
+    quality report must still match when no draw straddles a rounding edge."""
+    got, want = _exp(reference, tmp_path, 2, [60], 2, 300, 0, evals=25,
+                     dist=(TNORMAL, 0, 12, 5.0, 2.0))
+    assert got == want
+
+
+def test_time_budget_and_scaling_reports(reference, tmp_path):
+    """Wall-clock experiments: same row schema and labels as the reference's
+    (the values are timings of different hardware)."""
+    def rows(text):
+        return [ln.split(",") for ln in text.splitlines() if ln and not ln.startswith("#")][1:]
+    for which, ms, size in ((3, [100, 1000, 10000], 20000), (4, [], 300)):
+        got, want = _exp(reference, tmp_path, which, ms or [1], 1, size, 0, evals=0)
+        g, w = rows(got), rows(want)
+        assert len(g) == len(w)
+        for a, b in zip(g, w):
+            assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3]
+            assert a[4].split("_", 1)[1] == b[4].split("_", 1)[1]   # gpu1_* vs single_*
+            assert float(a[5]) >= 0.0
