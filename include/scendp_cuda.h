@@ -291,6 +291,34 @@ scendp_status scendp_dsirp_eval(scendp_ctx* ctx,
                                 const scendp_scenarios* sc, uint32_t flags,
                                 const scendp_dsirp_out* out);
 
+/* ---- K5: generic dense (min,+) stage sweep (minplus.hpp / minplus.cpp) ---
+ * forward_sweep (minplus.cpp:94-102) of `batch` initial frontiers through one
+ * shared chain of stage matrices: J_{s+1}[j] = min over options r, then
+ * predecessors i, of A_s(i,j;r) + J_s[i] (the reference's scan order and
+ * +inf semantics; minplus_apply_options, minplus.cpp:76-92).  Stage s is
+ * [depth][rows][cols] row-major (MaskedTransition's slice-major entries);
+ * rows of stage 0 == init_size and rows of stage s+1 == cols of stage s. */
+typedef struct {
+  uint64_t rows, cols, depth;
+  const double* entries;  /* host or device, per mem_kind */
+} scendp_minplus_stage;
+
+#define SCENDP_MINPLUS_ALL_STAGES 0x1u /* out = every frontier: [B][init_size +
+                                          sum cols], else the last: [B][cols] */
+#define SCENDP_MINPLUS_EXACT_TIES 0x2u /* force the compare-select min (sign of
+                                          zero ties as the reference); chosen
+                                          automatically when a host input
+                                          holds -0.0 */
+
+/* init: [batch][init_size]; mem_kind SCENDP_MEM_HOST or SCENDP_MEM_DEVICE
+ * applies to the stage entries, init and out alike.  Synchronous. */
+scendp_status scendp_minplus_sweep(scendp_ctx* ctx,
+                                   const scendp_minplus_stage* stages,
+                                   uint32_t n_stages, const double* init,
+                                   uint64_t init_size, uint64_t batch,
+                                   uint32_t mem_kind, uint32_t flags,
+                                   double* out);
+
 /* ---- multi-GPU: one tiny NCCL all-reduce of the aggregates --------------
  * Scenario shards never exchange data; only the per-candidate raw
  * aggregates (16 x u64 each) are summed across ranks.  NCCL is loaded at

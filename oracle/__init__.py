@@ -322,6 +322,23 @@ class Reference:
                                      C.c_size_t, C.c_size_t, C.c_ulonglong, C.c_ulonglong,
                                      C.c_uint, C.c_char_p]
 
+        L.ref_forward_sweep.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+
+    def forward_sweep(self, stages, init):
+        """stages: list of [depth][rows][cols] arrays; returns every frontier."""
+        init = np.ascontiguousarray(init, np.float64)
+        rows = np.array([a.shape[1] for a in stages], np.uint64)
+        cols = np.array([a.shape[2] for a in stages], np.uint64)
+        depth = np.array([a.shape[0] for a in stages], np.uint64)
+        ent = np.concatenate([np.ascontiguousarray(a, np.float64).ravel() for a in stages]) \
+            if stages else np.zeros(1)
+        out = np.zeros(init.size + int(cols.sum()), np.float64)
+        self._check(self.lib.ref_forward_sweep(len(stages), rows.ctypes.data, cols.ctypes.data,
+                                               depth.ctypes.data, ent.ctypes.data,
+                                               init.ctypes.data, init.size, out.ctypes.data))
+        return out
+
     def _check(self, rc):
         if rc != 0:
             raise RuntimeError(self.lib.ref_last_error().decode())

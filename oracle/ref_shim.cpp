@@ -502,3 +502,31 @@ REF_API int ref_experiment(int which, int n, long long Q, double beta, const dou
     return 1;
   }
 }
+
+// forward_sweep (minplus.cpp:94-102) over option-sliced stages; writes every
+// frontier (initial included) back to back.
+REF_API int ref_forward_sweep(size_t n_stages, const size_t* rows, const size_t* cols,
+                              const size_t* depth, const double* entries,
+                              const double* init, size_t width, double* out) {
+  try {
+    std::vector<MaskedTransition> st;
+    size_t off = 0;
+    for (size_t s = 0; s < n_stages; ++s) {
+      MaskedTransition a(rows[s], cols[s], depth[s]);
+      for (size_t r = 0; r < depth[s]; ++r)
+        for (size_t i = 0; i < rows[s]; ++i)
+          for (size_t j = 0; j < cols[s]; ++j) a.at(i, j, r) = ExtendedCost{entries[off++]};
+      st.push_back(std::move(a));
+    }
+    ValueFrontier f;
+    f.values.resize(width);
+    for (size_t k = 0; k < width; ++k) f.values[k] = ExtendedCost{init[k]};
+    size_t o = 0;
+    for (const ValueFrontier& fr : forward_sweep(st, f))
+      for (const ExtendedCost& v : fr.values) out[o++] = v.value;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}

@@ -267,6 +267,27 @@ class Context:
                                           buf.ptr))
         return buf
 
+    # ---- K5: dense (min,+) sweep (minplus.cpp) -------------------------------
+    def minplus_sweep(self, stages, init: np.ndarray, all_stages: bool = False,
+                      exact_ties: bool = False) -> np.ndarray:
+        """forward_sweep of a batch of frontiers (init [B][n]) through `stages`
+        ([depth][rows][cols] arrays).  Returns [B][n + sum cols] (all_stages)
+        or the last frontiers [B][cols]."""
+        init = np.ascontiguousarray(np.atleast_2d(init), np.float64)
+        keep = [np.ascontiguousarray(a, np.float64) for a in stages]
+        cs = (A.MinplusStage * max(1, len(keep)))()
+        for s, a in enumerate(keep):
+            cs[s] = A.MinplusStage(a.shape[1], a.shape[2], a.shape[0], a.ctypes.data)
+        width = init.shape[1] + (sum(a.shape[2] for a in keep) if all_stages else 0)
+        if not all_stages:
+            width = keep[-1].shape[2] if keep else init.shape[1]
+        out = np.empty((init.shape[0], width), np.float64)
+        flags = (A.MINPLUS_ALL_STAGES if all_stages else 0) | (A.MINPLUS_EXACT_TIES if exact_ties else 0)
+        A.check(self.lib.scendp_minplus_sweep(self.handle, cs, len(keep), init.ctypes.data,
+                                              init.shape[1], init.shape[0], A.MEM_HOST, flags,
+                                              out.ctypes.data))
+        return out
+
     def to_tiled(self, src: DeviceBuffer, rows: int, count: int) -> DeviceBuffer:
         dst = self.alloc(self.tiled_bytes(rows, count))
         A.check(self.lib.scendp_scenarios_to_tiled(self.handle, src.ptr, rows, count, dst.ptr))

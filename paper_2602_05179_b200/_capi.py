@@ -95,6 +95,15 @@ class KernelStats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
+class MinplusStage(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("depth", C.c_uint64),
+                ("entries", C.c_void_p)]
+
+
+MINPLUS_ALL_STAGES = 0x1
+MINPLUS_EXACT_TIES = 0x2
+
+
 class ScnbHeader(C.Structure):
     _fields_ = [("rows", C.c_uint64), ("count", C.c_uint64)]
 
@@ -132,6 +141,9 @@ SIGNATURES = {
     "scendp_best_candidate": (C.c_int64, [C.POINTER(Agg), C.c_uint32]),
     "scendp_dsirp_eval": (C.c_int, [C.c_void_p, C.POINTER(Customer), C.c_uint32,
                                     C.POINTER(Scenarios), C.c_uint32, C.POINTER(DsirpOut)]),
+    "scendp_minplus_sweep": (C.c_int, [C.c_void_p, C.POINTER(MinplusStage), C.c_uint32,
+                                       C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                       C.c_uint32, C.c_void_p]),
     "scendp_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "scendp_comm_init_rank": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     "scendp_comm_init_all": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32]),

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <stdexcept>
 #include <string>
 
@@ -96,6 +97,77 @@ ExtendedCost simulate_schedule(const CustomerSpec& spec, const DeliveryCostModel
     inv = j;
   }
   return ExtendedCost{total};
+}
+
+MaskedTransition build_transition_matrix(const CustomerSpec& spec,
+                                         const DeliveryCostModel& delivery,
+                                         const HoldingPenaltyModel& holding, int day,
+                                         int demand) {
+  const int states = spec.capacity + 1;
+  MaskedTransition a(states, states, 1);
+  for (int i = 0; i < states; ++i) {
+    // the two order-up-to actions in tie order: no delivery (one cost), then
+    // a delivery of U - I over every route option (absent when I == U)
+    const int full = spec.capacity - i;
+    for (int act = 0; act < (full > 0 ? 2 : 1); ++act) {
+      const int q = act == 0 ? 0 : full;
+      const int j = std::max(0, i + q - demand);
+      const int shortage = std::max(0, demand - i - q);
+      const int opts = q == 0 ? 1 : delivery.options;
+      for (int r = 0; r < opts; ++r)
+        a.at(i, j) = extended_min(
+            a.at(i, j), ExtendedCost{delivery.cost(day, r, q) + holding.cost(spec, j, shortage)});
+    }
+  }
+  return a;
+}
+
+std::vector<ValueFrontier> sweep_customer_scenario(const CustomerSpec& spec,
+                                                   const DeliveryCostModel& delivery,
+                                                   const HoldingPenaltyModel& holding,
+                                                   std::span<const std::uint32_t> demands) {
+  spec.validate();
+  delivery.validate(spec);
+  holding.validate(spec);
+  if (demands.size() != static_cast<std::size_t>(spec.horizon))
+    throw std::invalid_argument("scenario has " + std::to_string(demands.size()) +
+                                " days, spec horizon is " + std::to_string(spec.horizon));
+  std::vector<MaskedTransition> stages;
+  stages.reserve(spec.horizon);
+  for (int t = 1; t <= spec.horizon; ++t)
+    stages.push_back(
+        build_transition_matrix(spec, delivery, holding, t, static_cast<int>(demands[t - 1])));
+  return forward_sweep(stages, ValueFrontier::initial(1, spec.capacity + 1,
+                                                      static_cast<std::size_t>(spec.initial_inventory)));
+}
+
+ExtendedCost brute_force_schedule(const CustomerSpec& spec, const DeliveryCostModel& delivery,
+                                  const HoldingPenaltyModel& holding,
+                                  std::span<const std::uint32_t> demands) {
+  spec.validate();
+  delivery.validate(spec);
+  holding.validate(spec);
+  if (demands.size() != static_cast<std::size_t>(spec.horizon))
+    throw std::invalid_argument("scenario has " + std::to_string(demands.size()) +
+                                " days, spec horizon is " + std::to_string(spec.horizon));
+  if (spec.horizon > 14) throw std::invalid_argument("brute-force schedule is limited to H <= 14");
+  double best = std::numeric_limits<double>::infinity();
+  for (std::uint32_t pattern = 0; pattern < (1u << spec.horizon); ++pattern) {
+    double total = 0.0;
+    int inv = spec.initial_inventory;
+    for (int t = 1; t <= spec.horizon; ++t) {
+      const int d = static_cast<int>(demands[t - 1]);
+      const int q = (pattern >> (t - 1)) & 1u ? spec.capacity - inv : 0;
+      // options add independently per day: the cheapest one is optimal
+      double f = delivery.cost(t, 0, q);
+      for (int r = 1; q > 0 && r < delivery.options; ++r) f = std::min(f, delivery.cost(t, r, q));
+      const int j = std::max(0, inv + q - d);
+      total += f + holding.cost(spec, j, std::max(0, d - inv - q));
+      inv = j;
+    }
+    best = std::min(best, total);
+  }
+  return ExtendedCost{best};
 }
 
 std::uint64_t oudp_per_scenario_bytes(const CustomerSpec& spec) {

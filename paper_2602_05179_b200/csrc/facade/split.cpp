@@ -193,6 +193,38 @@ SplitSolution split_scenario_linear(const RoutingInstance& inst, const GiantTour
   return single_scenario(inst, tour, demand, false);
 }
 
+ExtendedCost brute_force_split(const RoutingInstance& inst, const GiantTour& tour,
+                               std::span<const std::uint32_t> demand) {
+  check_inputs(inst, tour, demand.size());
+  const int n = inst.n;
+  if (n > 20) throw std::invalid_argument("brute-force split is limited to n <= 20");
+  double best = std::numeric_limits<double>::infinity();
+  // bit p-1 of `cuts` set: a route ends after tour position p (p < n)
+  for (std::uint64_t cuts = 0; cuts < (std::uint64_t{1} << (n - 1)); ++cuts) {
+    double total = 0.0;
+    bool feasible = true;
+    for (int first = 1; first <= n && feasible;) {
+      int last = first;
+      while (last < n && !((cuts >> (last - 1)) & 1)) ++last;
+      double c = inst.cost(0, tour.order[first - 1]);
+      std::int64_t load = 0;
+      for (int k = first; k <= last; ++k) {
+        load += demand[tour.order[k - 1] - 1];
+        if (k > first) c += inst.cost(tour.order[k - 2], tour.order[k - 1]);
+      }
+      c += inst.cost(tour.order[last - 1], inst.depot_in());
+      if (load > inst.capacity) {
+        if (inst.hard) feasible = false;
+        else c += inst.penalty_beta * static_cast<double>(load - inst.capacity);
+      }
+      total += c;
+      first = last + 1;
+    }
+    if (feasible && total < best) best = total;
+  }
+  return ExtendedCost{best};
+}
+
 std::uint64_t split_per_scenario_bytes(int n) {
   const std::uint64_t states = static_cast<std::uint64_t>(n) + 1;
   return states * sizeof(ExtendedCost) + states * sizeof(std::int32_t) +

@@ -11,6 +11,8 @@
 //   facade_main io-read <path>                               (no GPU)
 //   facade_main io-parse <path> <out>                        (no GPU)
 //   facade_main io-write-inst <n> <Q> <hard> <beta> <inst_seed> <out>   (no GPU)
+//   facade_main trials <which> <trials> <seed> <max_n>
+//   facade_main dense <U> <I0> <H> <R> <seed> <m>
 //   facade_main exp <which> <n> <Q> <beta> <inst_seed> <kind> <lo> <hi> <mean> <sd>
 //                   <seed> <evals> <reps> <eval_size> <ref_size> <out> <m...>
 #include <cstdio>
@@ -22,6 +24,8 @@
 #include <vector>
 
 #include "scendp/io.hpp"
+#include "scendp/minplus.hpp"
+#include "scendp/oracle.hpp"
 #include "scendp/oudp.hpp"
 #include "scendp/saa.hpp"
 #include "scendp/scenario.hpp"
@@ -282,6 +286,58 @@ int run_exp(char** a, int nm) {
   return 0;
 }
 
+// the reference's randomized self-checks against this library
+int run_trials(char** a) {
+  const int which = std::atoi(a[0]);
+  const std::size_t trials = std::strtoull(a[1], nullptr, 10);
+  const std::uint64_t seed = std::strtoull(a[2], nullptr, 10);
+  const OracleOutcome o = which == 0   ? run_split_oracle_trials(trials, seed)
+                          : which == 1 ? run_split_agreement_trials(trials, seed, std::atoi(a[3]))
+                                       : run_dsirp_oracle_trials(trials, seed);
+  std::printf("trials %zu mismatches %zu\n", o.trials, o.mismatches);
+  if (!o.ok()) std::printf("failure %s\n", o.first_failure.c_str());
+  return 0;
+}
+
+// dense DSIRP path: every frontier of sweep_customer_scenario for m scenarios
+// (the customer of run_dsirp), plus forward_sweep_batch of the scenario-0
+// stage chain from m different start states
+int run_dense(char** a) {
+  CustomerSpec spec;
+  spec.capacity = std::atoi(a[0]);
+  spec.initial_inventory = std::atoi(a[1]);
+  spec.horizon = std::atoi(a[2]);
+  const int R = std::atoi(a[3]);
+  const unsigned long long seed = std::strtoull(a[4], nullptr, 10);
+  const std::size_t m = std::strtoull(a[5], nullptr, 10);
+  spec.holding = 1.25;
+  spec.stockout_multiplier = 2.5;
+  DeliveryCostModel del = DeliveryCostModel::linear(spec.horizon, R, 40.0, 0.5);
+  for (int t = 0; t < spec.horizon; ++t)
+    for (int r = 0; r < R; ++r) {
+      del.fixed[t * R + r] = 40.0 + 5.0 * r + 0.125 * t;
+      del.unit[t * R + r] = 0.5 + 0.25 * r;
+    }
+  HoldingPenaltyModel hold;
+  ScenarioBatch batch = generate_scenarios(DistributionSpec::parse("uniform:0:33", seed), 1,
+                                           spec.horizon, m);
+  std::vector<double> fr;
+  for (std::size_t w = 0; w < m; ++w)
+    for (const ValueFrontier& f : sweep_customer_scenario(spec, del, hold, batch.column(w)))
+      for (const ExtendedCost& v : f.values) fr.push_back(v.value);
+  print_vec("frontiers", fr);
+  std::vector<MaskedTransition> stages;
+  for (int t = 1; t <= spec.horizon; ++t)
+    stages.push_back(build_transition_matrix(spec, del, hold, t, static_cast<int>(batch.column(0)[t - 1])));
+  std::vector<ValueFrontier> starts;
+  for (int s = 0; s <= spec.capacity; ++s) starts.push_back(ValueFrontier::initial(1, spec.capacity + 1, s));
+  std::vector<double> last;
+  for (const ValueFrontier& f : forward_sweep_batch(stages, starts))
+    for (const ExtendedCost& v : f.values) last.push_back(v.value);
+  print_vec("batch_last", last);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -296,6 +352,8 @@ int main(int argc, char** argv) {
     if (mode == "io-read" && argc == 3) return run_io_read(argv + 2);
     if (mode == "io-parse" && argc == 4) return run_io_parse(argv + 2);
     if (mode == "io-write-inst" && argc == 8) return run_io_write_inst(argv + 2);
+    if (mode == "trials" && argc == 6) return run_trials(argv + 2);
+    if (mode == "dense" && argc == 8) return run_dense(argv + 2);
     if (mode == "exp" && argc >= 19) return run_exp(argv + 2, argc - 18);
   } catch (const std::exception& e) {
     std::printf("exception %s\n", e.what());

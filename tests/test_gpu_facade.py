@@ -25,7 +25,9 @@ def run(*args):
     res = {}
     for line in out.stdout.splitlines():
         t = line.split()
-        if t[0] in ("totals", "V4", "gen_totals", "trajectory"):
+        if t[0] == "failure":
+            res["failure"] = line
+        elif t[0] in ("totals", "V4", "gen_totals", "trajectory", "frontiers", "batch_last"):
             res[t[0]] = np.array([float(x) for x in t[2:]])
         elif t[0] in ("cuts4", "route_count", "tour", "deliver", "quantity", "end_inventory",
                       "route_option", "data", "col3"):
