@@ -577,7 +577,8 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   if (!linear && !a.hard && a.pen_lmax > 0 && small_tables) {
     const int T = kPenThreads;
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + 2 * 4) +
-                        static_cast<size_t>(T) * (kRing * 8 + kPosRing * (8 + (FULL ? 4 : 0)));
+                        static_cast<size_t>(T) * (kRing * (8 + (FULL ? 4 : 0)) +
+                                                  kPosRing * (8 + (FULL ? 8 : 0)));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {
       set_smem(kernel, smem);

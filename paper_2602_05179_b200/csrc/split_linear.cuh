@@ -76,7 +76,14 @@ __device__ __forceinline__ VT k1_neg_inf() {
 
 // One DP position.  PUSH = (i < n).  Ring slot s of this thread lives at
 // ring_at(rf, s) (rf/rl/ri/rr are per-thread base pointers).
-template <typename VT, bool FULL, bool PUSH>
+//
+// SAFE = false is the fast form for a position with d_i <= Q (checked per
+// chunk): entry i-1, at the back, then survives the eviction, so the window
+// never empties and the eviction loop needs no emptiness test; and since the
+// deque is non-empty before the pops, it can only become empty by popping,
+// so the "popped empty" front update lives inside the (rarer) pop branch.
+// SAFE = true handles any d_i (window emptied when d_i > Q).
+template <typename VT, bool FULL, bool PUSH, bool SAFE = true>
 __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
                                         VT t1, VT t2, VT t3, VT* __restrict__ rf,
                                         uint32_t* __restrict__ rl, int32_t* __restrict__ ri,
@@ -84,28 +91,44 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
   s.load += d;
   // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96); the
   // evicted slot becomes the -inf sentinel below the new head
-  while (s.load - s.front_l > Qc) {
-    ring_at(rf, s.head) = k1_neg_inf<VT>();
-    s.head += kStep;
-    if (s.head == s.tail) {
-      // only when d_i > Q: every route into i overflows, V(i) = +inf.  The
-      // placeholder front (inf-class f, load of position i) stands in for
-      // entry i until it is pushed; the parked back value stops the pops.
-      s.back_f = k1_neg_inf<VT>();
-      s.front_f = k1_inf<VT>();
-      s.front_l = s.load;
-      if (FULL) {
-        s.front_i = -1;
-        s.front_rc = -1;
+  if constexpr (SAFE) {
+    while (s.load - s.front_l > Qc) {
+      ring_at(rf, s.head) = k1_neg_inf<VT>();
+      s.head += kStep;
+      if (s.head == s.tail) {
+        // only when d_i > Q: every route into i overflows, V(i) = +inf.  The
+        // placeholder front (inf-class f, load of position i) stands in for
+        // entry i until it is pushed; the parked back value stops the pops.
+        s.back_f = k1_neg_inf<VT>();
+        s.front_f = k1_inf<VT>();
+        s.front_l = s.load;
+        if (FULL) {
+          s.front_i = -1;
+          s.front_rc = -1;
+        }
+        break;
       }
-      break;
+      const int hs = s.head;
+      s.front_f = ring_at(rf, hs);
+      s.front_l = ring_at(rl, hs);
+      if (FULL) {
+        s.front_i = ring_at(ri, hs);
+        s.front_rc = ring_at(rr, hs);
+      }
     }
-    const int hs = s.head;
-    s.front_f = ring_at(rf, hs);
-    s.front_l = ring_at(rl, hs);
-    if (FULL) {
-      s.front_i = ring_at(ri, hs);
-      s.front_rc = ring_at(rr, hs);
+  } else {
+    if (s.load - s.front_l > Qc) {
+      do {
+        ring_at(rf, s.head) = k1_neg_inf<VT>();
+        s.head += kStep;
+        s.front_l = ring_at(rl, s.head);
+      } while (s.load - s.front_l > Qc);
+      const int hs = s.head;
+      s.front_f = ring_at(rf, hs);
+      if (FULL) {
+        s.front_i = ring_at(ri, hs);
+        s.front_rc = ring_at(rr, hs);
+      }
     }
   }
   if constexpr (std::is_same<VT, int32_t>::value) s.v = s.front_f + t0;
@@ -123,16 +146,27 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
     // strict pop: earlier candidates stay ahead on f ties (split.cpp:110-113);
     // the -inf sentinel in the slot below the head ends the loop when the
     // deque runs empty
-    while (s.back_f > fi) {
-      s.tail -= kStep;
-      s.back_f = ring_at(rf, s.tail - kStep);
-    }
-    if (s.tail == s.head) {  // popped empty: entry i becomes the front
+    auto become_front = [&] {  // entry i is the only one left
       s.front_f = fi;
       s.front_l = s.load;
       if (FULL) {
         s.front_i = i;
         s.front_rc = s.rc;
+      }
+    };
+    if constexpr (SAFE) {
+      while (s.back_f > fi) {
+        s.tail -= kStep;
+        s.back_f = ring_at(rf, s.tail - kStep);
+      }
+      if (s.tail == s.head) become_front();
+    } else {
+      if (s.back_f > fi) {
+        do {
+          s.tail -= kStep;
+          s.back_f = ring_at(rf, s.tail - kStep);
+        } while (s.back_f > fi);
+        if (s.tail == s.head) become_front();
       }
     }
     const int ts = s.tail;
@@ -278,10 +312,18 @@ split_linear_kernel(SplitArgs a) {
           t3[2 * h] = y3.x; t3[2 * h + 1] = y3.y;
         }
       }
-      k1_step<VT, FULL, true>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
-      k1_step<VT, FULL, true>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+      // fast form unless a demand of this chunk exceeds Q (window may empty)
+      if (max(max(d0, d1), max(d2, d3)) <= Qc) {
+        k1_step<VT, FULL, true, false>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true, false>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true, false>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true, false>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+      } else {
+        k1_step<VT, FULL, true>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+        k1_step<VT, FULL, true>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+      }
     };
     // pairs of chunks with ping-pong demand registers (no copies); demands
     // are loaded one chunk ahead

@@ -11,25 +11,36 @@
 //   p before it     B = {L_i - L_p >  Q}:   cand = g(p) + (dist_i + ret_i)
 //                                                 + beta (L_i - Q),
 //   g(p) = f(p) - beta L_p.
-// A is a suffix of positions and B the complementary prefix, so
+// A is a suffix [lo, i) of positions and B the complementary prefix [0, lo),
+// so
 //   min over A = the monotone-deque front of K1 (earliest minimal f), and
-//   min over B = a running prefix minimum of g (earliest minimal g),
-// both maintained in O(1) amortized per position; on equal candidates B wins
-// because all of its indices precede A's -- exactly the reference's
-// first-strict-minimum over p = 0..i-1.  Penalized mode never produces +inf
-// (every p is admissible), so no masking is needed.
+//   min over B = PM(lo-1), the prefix minimum of g up to lo-1 (earliest
+//                minimal g), recorded for every position when it is pushed;
+// on equal candidates B wins because all of its indices precede A's --
+// exactly the reference's first strict minimum over p = 0..i-1.  Penalized
+// mode never produces +inf (every p is admissible), so no masking is needed.
 //
-// Per-thread shared state: the deque ring (K1's, f and position index) and a
-// position ring of the last kPosRing positions (f, L) that feeds the prefix
-// minimum as positions leave the window.  A window longer than the position
-// ring or a deque overflow sends the scenario to the generic kernel's O(n)
-// form of the same decomposition; a load that would leave the exact int32
-// range sends it to the generic fp64 quadratic form.
+// Per thread: the deque ring (f, position) and a position ring holding
+// (L_p, PM(p)) for p in [lo-1, i]; per position the window start advances
+// with one shared load per step and the B candidate is one more load.  All
+// ring counters are byte offsets (slot * 4T), masked on access.  The kernel
+// assumes d_i <= Q (the window never empties, so the deque is never empty
+// after the front evictions); a larger demand, a window longer than the
+// position ring, a deque overflow or a load beyond the exact int32 range
+// sends the scenario to the generic kernel (its O(n) form of the same
+// decomposition, or the fp64 quadratic form when the range is exceeded).
 #pragma once
 
 constexpr int kPenThreads = 128;
-constexpr int kPosRing = 32;  // positions per thread (window length < 32)
+constexpr int kPosRing = 32;                  // positions per thread
+constexpr int kPosStep = kPenThreads * 4;     // bytes per ring slot (all threads)
+constexpr int kPosMask = kPosRing * kPosStep - 1;
 constexpr int32_t kPenInf = 0x7fffffff;
+
+template <typename E>
+__device__ __forceinline__ E& pos_at(E* base, int c) {
+  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + (c & kPosMask));
+}
 
 template <bool FULL, int SRC, bool IDENT>
 __global__ void __launch_bounds__(kPenThreads)
@@ -50,13 +61,15 @@ split_penal_kernel(SplitArgs a) {
     for (int x = threadIdx.x; x < 2 * npad; x += T) s_tab[x] = g[x];
   }
   const int tid = threadIdx.x;
-  // rings, thread-minor: deque [kRing][T] (f, idx), positions [kPosRing][T]
-  // (f, L[, rc])
+  // thread-minor rings: deque [kRing][T] f | position (| rc);
+  // positions [kPosRing][T] L | PM (| PM index | PM rc)
   int32_t* dq_f = s_tab + 2 * npad + tid;
-  int32_t* dq_i = dq_f + kRing * T;
-  int32_t* ps_f = dq_i + kRing * T;
-  uint32_t* ps_l = reinterpret_cast<uint32_t*>(ps_f + kPosRing * T);
-  int32_t* ps_r = reinterpret_cast<int32_t*>(ps_l + kPosRing * T);  // FULL
+  int32_t* dq_p = dq_f + kRing * T;
+  int32_t* dq_r = dq_p + kRing * T;                                          // FULL
+  uint32_t* ps_l = reinterpret_cast<uint32_t*>(dq_f + (FULL ? 3 : 2) * kRing * T);
+  int32_t* ps_pm = reinterpret_cast<int32_t*>(ps_l + kPosRing * T);
+  int32_t* ps_pi = ps_pm + kPosRing * T;                                     // FULL
+  int32_t* ps_pr = ps_pi + kPosRing * T;                                     // FULL
   agg_cta_init(s_agg);
   __syncthreads();
 
@@ -85,87 +98,104 @@ split_penal_kernel(SplitArgs a) {
       Vout[0] = 0.0;
       Cout[0] = 0;
     }
-    // position 0: f(0) = (0.0 + c(0, s_1)) - dist[1], L_0 = 0
+    // position 0: f(0) = (0.0 + c(0, s_1)) - dist[1], L_0 = 0, g(0) = f(0)
     const int32_t f0 = a.f0i[k];
-    ps_f[0] = f0;
     ps_l[0] = 0u;
-    if (FULL) ps_r[0] = 0;
-    // deque: -inf sentinel in slot 0, entry p=0 in slot 1 (K1 layout)
+    ps_pm[0] = f0;
+    if (FULL) {
+      ps_pi[0] = 0;
+      ps_pr[0] = 0;
+    }
+    // deque: -inf sentinel in slot 0, entry p = 0 in slot 1 (K1 layout)
     dq_f[0] = INT32_MIN;
     dq_f[T] = f0;
-    dq_i[T] = 0;
-    int head = 1, tail = 2;  // slot counters (masked by kRing-1)
-    int32_t front_f = f0, front_i = 0, back_f = f0;
-    int lo = 0;               // first position inside the window
-    int32_t bmin = kPenInf;   // prefix minimum of g over [0, lo)
+    dq_p[T] = 0;
+    if (FULL) dq_r[T] = 0;
+    int head = kStep, tail = 2 * kStep;  // deque slot counters (bytes)
+    int32_t front_f = f0, back_f = f0;
+    int front_c = 0;                    // position counter (bytes) of the front
+    int32_t front_rc = 0;
+    int lo_c = 0;                       // window start lo, as a position counter
+    int32_t bmin = kPenInf;             // PM(lo - 1); kPenInf while lo == 0
     int32_t bidx = -1, brc = 0;
+    int32_t pm = f0, pm_i = 0, pm_rc = 0;  // running prefix minimum of g
     uint32_t load = 0;
 
-    // one DP position; returns false when the scenario must take the generic
-    // path (window longer than the position ring, deque overflow)
-    auto step = [&](int i, uint32_t d) -> bool {
+    // one DP position (i_c = i * kPosStep); false -> generic path
+    auto step = [&](int i, int i_c, uint32_t d) -> bool {
       const int sl = i - 1;
       const int32_t Ai = s_tab[sl], Bi = s_tab[npad + sl];
       load += d;
-      // positions leaving the window join the prefix B (in index order)
-      while (lo < i && load - ps_l[(lo & (kPosRing - 1)) * T] > Qc) {
-        const int ls = (lo & (kPosRing - 1)) * T;
-        const int32_t g = ps_f[ls] - beta * static_cast<int32_t>(ps_l[ls]);
-        if (g < bmin) {
-          bmin = g;
-          bidx = lo;
-          if (FULL) brc = ps_r[ls];
+      // the window start advances past positions whose route (p, i]
+      // overflows; d_i <= Q keeps p = i-1 inside, so no bound test is needed
+      if (load - pos_at(ps_l, lo_c) > Qc) {
+        do {
+          lo_c += kPosStep;
+        } while (load - pos_at(ps_l, lo_c) > Qc);
+        const int pc = lo_c - kPosStep;  // lo - 1
+        bmin = pos_at(ps_pm, pc);
+        if (FULL) {
+          bidx = pos_at(ps_pi, pc);
+          brc = pos_at(ps_pr, pc);
         }
-        ++lo;
-      }
-      // deque front leaves with the window; the vacated slot becomes the -inf
-      // sentinel below the head (ends the pop loop on an empty deque)
-      while (head != tail && front_i < lo) {
-        dq_f[(head & (kRing - 1)) * T] = INT32_MIN;
-        ++head;
-        if (head != tail) {
-          const int hs = (head & (kRing - 1)) * T;
-          front_f = dq_f[hs];
-          front_i = dq_i[hs];
-        } else {
-          back_f = INT32_MIN;
+        // deque entries before lo leave from the front (entry i-1 stays);
+        // the vacated slot becomes the -inf sentinel below the head
+        if (front_c < lo_c) {
+          do {
+            ring_at(dq_f, head) = INT32_MIN;
+            head += kStep;
+            front_c = ring_at(dq_p, head);
+          } while (front_c < lo_c);
+          front_f = ring_at(dq_f, head);
+          if (FULL) front_rc = ring_at(dq_r, head);
         }
       }
       // candidates: window A (deque front) and prefix B (prefix minimum)
-      const bool hasA = head != tail;
-      const int32_t candA = hasA ? front_f + Ai : kPenInf;
-      const int32_t candB = bidx >= 0 ? bmin + Ai + beta * static_cast<int32_t>(load - Qc) : kPenInf;
+      const int32_t candA = front_f + Ai;
+      const int32_t candB = lo_c > 0 ? bmin + Ai + beta * static_cast<int32_t>(load - Qc) : kPenInf;
       const bool useB = candB <= candA;  // B's indices come first: ties go to B
       v = useB ? candB : candA;
-      const int32_t cut = useB ? bidx : front_i;
       if (FULL) {
-        const int32_t frc = useB ? brc : (hasA ? ps_r[(front_i & (kPosRing - 1)) * T] : 0);
-        rc = frc + 1;
+        rc = (useB ? brc : front_rc) + 1;
         Vout[static_cast<uint64_t>(i) * kTile] = static_cast<double>(v);
-        Cout[static_cast<uint64_t>(i) * kTile] = cut;
+        Cout[static_cast<uint64_t>(i) * kTile] = useB ? bidx : front_c / kPosStep;
       }
       if (i < n) {
         const int32_t fi = v + Bi;
-        // the position ring must hold [lo, i]
-        if (i - lo >= kPosRing - 1) return false;
-        const int ps = (i & (kPosRing - 1)) * T;
-        ps_f[ps] = fi;
-        ps_l[ps] = load;
-        if (FULL) ps_r[ps] = rc;
-        // strict pop (sentinel-terminated), then push (K1 deque)
-        while (back_f > fi) {
-          --tail;
-          back_f = dq_f[((tail - 1) & (kRing - 1)) * T];
+        // the position ring must hold [lo-1, i]
+        if (i_c - lo_c >= (kPosRing - 1) * kPosStep) return false;
+        const int32_t g = fi - beta * static_cast<int32_t>(load);
+        if (g < pm) {  // strict: the earliest minimum stays
+          pm = g;
+          if (FULL) {
+            pm_i = i;
+            pm_rc = rc;
+          }
         }
-        if (tail == head) {
-          front_f = fi;
-          front_i = i;
+        pos_at(ps_l, i_c) = load;
+        pos_at(ps_pm, i_c) = pm;
+        if (FULL) {
+          pos_at(ps_pi, i_c) = pm_i;
+          pos_at(ps_pr, i_c) = pm_rc;
         }
-        if (tail - head >= kRing - 1) return false;
-        const int ts = (tail & (kRing - 1)) * T;
-        dq_f[ts] = fi;
-        dq_i[ts] = i;
-        ++tail;
+        // strict pop (sentinel-terminated), then push (K1 deque); the deque
+        // is non-empty here, so it can only empty by popping
+        if (back_f > fi) {
+          do {
+            tail -= kStep;
+            back_f = ring_at(dq_f, tail - kStep);
+          } while (back_f > fi);
+          if (tail == head) {
+            front_f = fi;
+            front_c = i_c;
+            if (FULL) front_rc = rc;
+          }
+        }
+        if (tail - head >= (kRing - 1) * kStep) return false;
+        ring_at(dq_f, tail) = fi;
+        ring_at(dq_p, tail) = i_c;
+        if (FULL) ring_at(dq_r, tail) = rc;
+        tail += kStep;
         back_f = fi;
       }
       return true;
@@ -184,10 +214,15 @@ split_penal_kernel(SplitArgs a) {
     load4(0, dc);
     for (int s0 = 0; s0 < n && ok; s0 += 4) {
       if (s0 + 4 < n) load4(s0 + 4, dn);
+      // a demand above Q would empty the window: generic path
+      if (max(max(dc[0], dc[1]), max(dc[2], dc[3])) > Qc) {
+        ok = false;
+        break;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int i = s0 + j + 1;
-        if (i <= n && ok) ok = step(i, dc[j]);
+        if (i <= n && ok) ok = step(i, i * kPosStep, dc[j]);
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) dc[j] = dn[j];
