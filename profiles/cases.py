@@ -9,6 +9,7 @@ Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
   c2gen     C2 with in-kernel generation (the e2e call, batched_split_costs_generated)
   c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
   c5        1000 tours x 10^5 scenarios, n=50, penalized beta=10
+  k5        dense (min,+) sweep: 6 stages x 3 options x 101x101, 10^5 frontiers
 
 Every case runs one warm-up launch and then R timed launches; capture with
 e.g. `ncu --set full -k regex:split_linear -s 1 -c 1 python profiles/cases.py c2`.
@@ -76,6 +77,16 @@ def main():
         scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, m5)
         fn = lambda: ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=m5,
                                     totals=False)
+    elif c == "k5":
+        rng = np.random.default_rng(11)
+        stages = []
+        for _ in range(6):
+            st = np.floor(rng.random((3, 101, 101)) * 100.0)
+            st[rng.random(st.shape) < 0.5] = np.inf
+            stages.append(st)
+        init = np.full((100_000, 101), np.inf)
+        init[np.arange(100_000), rng.integers(0, 101, 100_000)] = 0.0
+        fn = lambda: ctx.minplus_sweep(stages, init)
     else:
         raise SystemExit(f"unknown case {c}")
     fn()
