@@ -67,11 +67,17 @@ __device__ __forceinline__ uint32_t uniform_draw(const GenParams& g, uint64_t x)
   return static_cast<uint32_t>(g.lo + static_cast<int64_t>(__umul64hi(x, g.span)));
 }
 
+// The value of one next() output x (uniform or poisson).
+__device__ __forceinline__ uint32_t draw_value(const GenParams& g, uint64_t x);
+
 // One counter-based draw: DistributionSpec::sample for the kinds that use
 // exactly one next() per value (scenario.cpp:23-26; poisson: SURVEY App. A).
 __device__ __forceinline__ uint32_t draw_counter(const GenParams& g,
                                                  uint64_t stream, uint64_t row) {
-  const uint64_t x = mix64(stream + row * kGamma);
+  return draw_value(g, mix64(stream + row * kGamma));
+}
+
+__device__ __forceinline__ uint32_t draw_value(const GenParams& g, uint64_t x) {
   if (g.kind == SCENDP_DIST_UNIFORM) return uniform_draw(g, x);
   // next_unit: ((x >> 11) + 1) * 2^-53, exact in fp64
   const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;

@@ -24,6 +24,9 @@
 // penalized cand = ((f + dist[i]) + ret) + beta*(double)excess.  Ties keep
 // the earliest predecessor (strict <), as the reference.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <type_traits>
 #include <cstring>
@@ -441,13 +444,25 @@ void validate_instance(const scendp_routing* inst) {
   if (inst->capacity <= 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "capacity Q must be > 0");
   if (!inst->costs) fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix must be (n+2) x (n+2)");
   const size_t side = static_cast<size_t>(n) + 2;
-  for (size_t x = 0; x < side; ++x)
-    for (size_t y = 0; y < side; ++y) {
-      const double c = inst->costs[x * side + y];
-      if (!std::isfinite(c) || c < 0.0)
-        fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix entries must be finite and >= 0");
-      if (x == y && c != 0.0) fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix diagonal must be 0");
-    }
+  // branch-free (vectorized) scan; the messages follow the reference's
+  // row-major check order (split.cpp:148-156): the first offending entry
+  // decides which one is reported
+  const double* c = inst->costs;
+  const size_t cells = side * side;
+  unsigned good = 1u;
+  for (size_t e = 0; e < cells; ++e)
+    good &= static_cast<unsigned>(c[e] >= 0.0) & static_cast<unsigned>(c[e] <= 1.7976931348623157e308);
+  bool bad = good == 0u;
+  for (size_t x = 0; x < side; ++x) bad |= c[x * side + x] != 0.0;
+  if (bad) {
+    for (size_t x = 0; x < side; ++x)
+      for (size_t y = 0; y < side; ++y) {
+        const double v = c[x * side + y];
+        if (!std::isfinite(v) || v < 0.0)
+          fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix entries must be finite and >= 0");
+        if (x == y && v != 0.0) fail(SCENDP_ERR_INVALID_ARGUMENT, "cost matrix diagonal must be 0");
+      }
+  }
   if (!inst->hard && !(inst->penalty_beta >= 0.0))
     fail(SCENDP_ERR_INVALID_ARGUMENT, "penalty beta must be >= 0");
 }
@@ -632,10 +647,33 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
 
 }  // namespace
 
+// SCENDP_HOST_TRACE=1: per-call host-side phase times (microseconds) on
+// stderr -- validation, tables + upload, launches, completion.
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  char buf[256];
+  int len = 0;
+  HostTrace() : on(std::getenv("SCENDP_HOST_TRACE") != nullptr) {
+    if (on) t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    len += std::snprintf(buf + len, sizeof(buf) - len, " %s=%.1f", what,
+                         std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+  ~HostTrace() {
+    if (on) std::fprintf(stderr, "split_eval host us:%s\n", buf);
+  }
+};
+
 extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing* inst,
                                            const int32_t* tours, uint32_t k_tours,
                                            const scendp_scenarios* sc, uint32_t flags,
                                            const scendp_split_out* out) {
+  HostTrace trace;
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (!sc || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenarios/out is null");
@@ -659,6 +697,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const bool linear = inst->hard && !(flags & SCENDP_QUADRATIC);
     const uint64_t m = sc->count;
     const uint32_t k = k_tours;
+    trace.mark("validate");
     CUDA_CHECK(cudaSetDevice(ctx->device));
 
     // tour tables
@@ -689,6 +728,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const double* d_c0 = reinterpret_cast<const double*>(dtab + o_c0);
     const uint32_t* d_col = reinterpret_cast<const uint32_t*>(dtab + o_col);
 
+    trace.mark("tables");
     // aggregates
     auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw)));
     CUDA_CHECK(cudaMemsetAsync(d_agg, 0, k * sizeof(scendp_agg_raw), ctx->stream));
@@ -808,6 +848,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       }
     }
 
+    trace.mark("launch");
     // the single collective: per-candidate raw aggregates, K x 16 u64
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(k) * kAggWords);
 
@@ -837,6 +878,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       ctx->copy(h_raw, d_agg, k * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost);
     }
     if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
+    trace.mark("sync");
     if (want_agg) {
       if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, k * sizeof(scendp_agg_raw));
       if (out->agg) finalize_agg(h_raw, 1, k, out->agg);
