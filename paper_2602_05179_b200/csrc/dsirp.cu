@@ -45,8 +45,7 @@ void launch_from_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t co
 using namespace scendp_dsirp;
 
 namespace scendp_dsirp {
-void launch_h4(scendp_ctx* c, const DsirpArgs& a, size_t s, bool i, bool f) { launch_h<4>(c, a, s, i, f); }
-void launch_h8(scendp_ctx* c, const DsirpArgs& a, size_t s, bool i, bool f) { launch_h<8>(c, a, s, i, f); }
+
 }  // namespace scendp_dsirp
 
 namespace {
@@ -292,8 +291,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       a.end_inventory = d_ei;
       a.route_option = d_ro;
       a.agg = d_agg;
-      if (H <= 4) launch_h4(ctx, a, smem, int_path, full);
-      else if (H <= 8) launch_h8(ctx, a, smem, int_path, full);
+      if (H <= 8) launch_exact(ctx, a, smem, int_path, full);
       else if (H <= 16) launch_h16(ctx, a, smem, int_path, full);
       else launch_h32(ctx, a, smem, int_path, full);
     }

@@ -112,6 +112,9 @@ __device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const Cust
                                                   uint32_t c, uint64_t w, const int (&dem)[HMAX],
                                                   bool& ok) {
   constexpr int K = HMAX + 1;
+  // slot loops with a constant trip count (guarded by e <= t) unroll fully,
+  // keeping the slot arrays in registers; long horizons keep t+1 trips
+  constexpr bool kSlotsExact = HMAX <= 8;
   constexpr int kUnr = HMAX <= 16 ? HMAX + 1 : 1;  // long horizons: rolled loops
   const int U = cd.U, H = cd.H, R = cd.R;
   const double h = cd.h, rh = cd.rh;
@@ -152,7 +155,7 @@ __device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const Cust
         const double fx = dtab ? 0.0 : fixed[t * R + r];
         const double un = dtab ? 0.0 : unit[t * R + r];
 #pragma unroll kUnr
-        for (int e = 0; e <= t; ++e) {
+        for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
           if (((live >> e) & 1ull) && st[e] < U) {
             const int q = U - st[e];
             const double F = dtab ? __ldg(dtable + t * (U + 1) + q)
@@ -171,7 +174,7 @@ __device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const Cust
       double b0 = kInfD;
       int k0 = -1, tgt = -1;
 #pragma unroll kUnr
-      for (int e = 0; e <= t; ++e) {
+      for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
         if ((live >> e) & 1ull) {
           const int i = st[e];
           const int j = max(0, i - d), s = max(0, d - i);
@@ -200,11 +203,12 @@ __device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const Cust
           const double tv = ((live >> tgt) & 1ull) ? sel_d<K>(vl, tgt) : kInfD;
           if (bv < tv) {
 #pragma unroll kUnr
-            for (int e = 0; e <= t; ++e) {
-              if (e == tgt) {
-                vl[e] = bv;
-                if (FULL) dm[e] = nm;
-              }
+            for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+              // per-slot selects (not `vl[tgt] = bv`): a dynamic index
+              // would move the slot arrays to local memory
+              const bool hit = e == tgt;
+              vl[e] = hit ? bv : vl[e];
+              if (FULL) dm[e] = hit ? nm : dm[e];
             }
             live |= 1ull << tgt;
             if (FULL) opt[t] = br;
@@ -290,7 +294,15 @@ template <int HMAX, bool FULL>
 __global__ void __launch_bounds__(kDsirpThreads)
 dsirp_int_kernel(DsirpArgs a) {
   constexpr int K = HMAX + 1;
+  // slot loops with a constant trip count (guarded by e <= t) unroll fully,
+  // keeping the slot arrays in registers; long horizons keep t+1 trips
+  constexpr bool kSlotsExact = HMAX <= 8;
   constexpr int kUnr = HMAX <= 16 ? HMAX + 1 : 1;  // long horizons: rolled loops
+  // horizons <= 8 are launched with HMAX == H exactly (launch_exact): every
+  // day/slot loop is then fully unrolled with compile-time bounds, so the
+  // frontier arrays stay in registers
+  constexpr bool kExact = HMAX <= 8;
+  using Mask = typename std::conditional<(K <= 32), uint32_t, uint64_t>::type;
   __shared__ unsigned long long s_agg[kAggSlots];
   const uint32_t c = blockIdx.y;
   const CustDev cd = a.cust[c];
@@ -299,7 +311,7 @@ dsirp_int_kernel(DsirpArgs a) {
   const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const bool active = wl < a.m_wave;
   const uint64_t w = a.w_base + wl;
-  const int U = cd.U, H = cd.H;
+  const int U = cd.U, H = kExact ? HMAX : cd.H;
   const int32_t* gkey = a.ipool + cd.off_gkey;     // [H][U+1]
   const int32_t* htab = a.ipool + cd.off_htab_i;   // [U+1]
   const bool htabular = cd.hold_tab != 0;
@@ -336,7 +348,7 @@ dsirp_int_kernel(DsirpArgs a) {
 #pragma unroll
       for (int t = 0; t < HMAX; ++t) opt[t] = 0;
       st[0] = cd.I0;
-      uint64_t live = 1ull;  // K = HMAX+1 slots can exceed 32
+      Mask live = 1u;  // K = HMAX+1 slots can exceed 32
 #pragma unroll kUnr
       for (int t = 0; t < HMAX; ++t) {
         if (t < H) {
@@ -348,8 +360,8 @@ dsirp_int_kernel(DsirpArgs a) {
           int32_t bk = INT32_MAX;
           int be = -1;
 #pragma unroll kUnr
-          for (int e = 0; e <= t; ++e) {
-            if (((live >> e) & 1ull) && st[e] < U) {
+          for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+            if (((live >> e) & 1u) && st[e] < U) {
               const int32_t key = __ldg(grow - st[e]) + ((vl[e] + hold1) << 8);
               if (key < bk) {
                 bk = key;
@@ -361,8 +373,8 @@ dsirp_int_kernel(DsirpArgs a) {
           int32_t b0 = INT32_MAX;
           int k0 = -1, tgt = -1;
 #pragma unroll kUnr
-          for (int e = 0; e <= t; ++e) {
-            if ((live >> e) & 1ull) {
+          for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+            if ((live >> e) & 1u) {
               const int i = st[e];
               const int j = max(0, i - d), s = max(0, d - i);
               const int32_t nv = vl[e] + hold(j, s);
@@ -371,11 +383,11 @@ dsirp_int_kernel(DsirpArgs a) {
               vl[e] = nv;
               if (i <= d) {
                 if (nv < b0) {
-                  if (k0 >= 0) live &= ~(1ull << k0);
+                  if (k0 >= 0) live &= ~(Mask{1} << k0);
                   b0 = nv;
                   k0 = e;
                 } else {
-                  live &= ~(1ull << e);
+                  live &= ~(Mask{1} << e);
                 }
               }
             }
@@ -389,23 +401,22 @@ dsirp_int_kernel(DsirpArgs a) {
             if (tgt >= 0) {
               int32_t tv = INT32_MAX;
 #pragma unroll kUnr
-              for (int e = 0; e <= t; ++e)
-                if (e == tgt && ((live >> e) & 1ull)) tv = vl[e];
+              for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e)
+                if (e == tgt && ((live >> e) & 1u)) tv = vl[e];
               if (bv < tv) {
 #pragma unroll kUnr
-                for (int e = 0; e <= t; ++e) {
-                  if (e == tgt) {
-                    vl[e] = bv;
-                    if (FULL) dm[e] = nm;
-                  }
+                for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+                  const bool hit = e == tgt;  // per-slot selects (see above)
+                  vl[e] = hit ? bv : vl[e];
+                  if (FULL) dm[e] = hit ? nm : dm[e];
                 }
-                live |= 1ull << tgt;
+                live |= Mask{1} << tgt;
                 if (FULL) opt[t] = br;
               }
             } else {
               st[t + 1] = j1;
               vl[t + 1] = bv;
-              live |= 1ull << (t + 1);
+              live |= Mask{1} << (t + 1);
               if (FULL) {
                 dm[t + 1] = nm;
                 opt[t] = br;
@@ -418,7 +429,7 @@ dsirp_int_kernel(DsirpArgs a) {
       int ts = -1;
 #pragma unroll
       for (int e = 0; e < K; ++e) {
-        if (((live >> e) & 1ull) && vl[e] < tv) {
+        if (((live >> e) & 1u) && vl[e] < tv) {
           tv = vl[e];
           ts = e;
         }
@@ -451,6 +462,12 @@ void launch_kernel(scendp_ctx* ctx, Kern kernel, const DsirpArgs& a, size_t smem
 }
 
 template <int HMAX>
+void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full);
+
+// Horizons 1..8: instantiations with HMAX == H (dsirp_exact.cu).
+void launch_exact(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full);
+
+template <int HMAX>
 void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
   if (int_path) {
     if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0);
@@ -462,8 +479,6 @@ void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, b
 }
 
 // One translation unit per horizon bound (parallel builds).
-void launch_h4(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);   // dsirp.cu
-void launch_h8(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);   // dsirp.cu
 void launch_h16(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h16.cu
 void launch_h32(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h32.cu
 
