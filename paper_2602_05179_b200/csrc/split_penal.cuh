@@ -121,8 +121,10 @@ split_penal_kernel(SplitArgs a) {
     int32_t pm = f0, pm_i = 0, pm_rc = 0;  // running prefix minimum of g
     uint32_t load = 0;
 
-    // one DP position (i_c = i * kPosStep); false -> generic path
-    auto step = [&](int i, int i_c, uint32_t d) -> bool {
+    // one DP position (i_c = i * kPosStep); ring capacities are checked per
+    // chunk by the caller (room for the chunk's pushes)
+    auto step = [&](int i, int i_c, uint32_t d, auto push_tag) {
+      constexpr bool PUSH = decltype(push_tag)::value;
       const int sl = i - 1;
       const int32_t Ai = s_tab[sl], Bi = s_tab[npad + sl];
       load += d;
@@ -160,10 +162,8 @@ split_penal_kernel(SplitArgs a) {
         Vout[static_cast<uint64_t>(i) * kTile] = static_cast<double>(v);
         Cout[static_cast<uint64_t>(i) * kTile] = useB ? bidx : front_c / kPosStep;
       }
-      if (i < n) {
+      if constexpr (PUSH) {
         const int32_t fi = v + Bi;
-        // the position ring must hold [lo-1, i]
-        if (i_c - lo_c >= (kPosRing - 1) * kPosStep) return false;
         const int32_t g = fi - beta * static_cast<int32_t>(load);
         if (g < pm) {  // strict: the earliest minimum stays
           pm = g;
@@ -191,14 +191,12 @@ split_penal_kernel(SplitArgs a) {
             if (FULL) front_rc = rc;
           }
         }
-        if (tail - head >= (kRing - 1) * kStep) return false;
         ring_at(dq_f, tail) = fi;
         ring_at(dq_p, tail) = i_c;
         if (FULL) ring_at(dq_r, tail) = rc;
         tail += kStep;
         back_f = fi;
       }
-      return true;
     };
     // demands of slots s0..s0+3 (slot s = position s+1), loaded one chunk
     // ahead of their use: the gathers hit L2 (C5 reuses each scenario tile
@@ -210,22 +208,44 @@ split_penal_kernel(SplitArgs a) {
         dd[j] = sl < n ? demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]) : 0u;
       }
     };
+    using Push = std::true_type;
+    using Last = std::false_type;
+    // room for 4 pushes: the position ring must hold [lo-1, i] for every i
+    // of the chunk, the deque its live entries + 4 + the sentinel slot
+    auto room = [&](int s0) {
+      return (s0 + 4) * kPosStep - lo_c <= (kPosRing - 2) * kPosStep &&
+             (tail - head) + 4 * kStep <= (kRing - 1) * kStep;
+    };
+    // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
+    const int npush = n - 1;
     uint32_t dc[4], dn[4] = {0u, 0u, 0u, 0u};
     load4(0, dc);
-    for (int s0 = 0; s0 < n && ok; s0 += 4) {
+    int s0 = 0;
+    for (; s0 + 4 <= npush; s0 += 4) {
       if (s0 + 4 < n) load4(s0 + 4, dn);
       // a demand above Q would empty the window: generic path
-      if (max(max(dc[0], dc[1]), max(dc[2], dc[3])) > Qc) {
+      if (max(max(dc[0], dc[1]), max(dc[2], dc[3])) > Qc || !room(s0)) {
         ok = false;
         break;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = s0 + j + 1;
-        if (i <= n && ok) ok = step(i, i * kPosStep, dc[j]);
-      }
+      for (int j = 0; j < 4; ++j) step(s0 + j + 1, (s0 + j + 1) * kPosStep, dc[j], Push{});
 #pragma unroll
       for (int j = 0; j < 4; ++j) dc[j] = dn[j];
+    }
+    // the remaining (< 4) pushing positions and position n (no push); dc
+    // holds the demands of slots s0..s0+3
+    if (ok) {
+      if (max(max(dc[0], dc[1]), max(dc[2], dc[3])) > Qc || !room(s0)) {
+        ok = false;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = s0 + j + 1;
+          if (i < n) step(i, i * kPosStep, dc[j], Push{});
+          else if (i == n) step(i, i * kPosStep, dc[j], Last{});
+        }
+      }
     }
     if (ok && load > lmax) ok = false;  // values may have left the exact range
     if (!ok) {
