@@ -1,0 +1,59 @@
+"""The in-library NCCL path (dlopen'ed libnccl, one all-reduce of the raw
+per-candidate aggregates) exercised on the single GPU this pool provides:
+a one-rank communicator (multi-process form, scendp_comm_init_rank, and
+in-process form, scendp_comm_init_all) must leave every result unchanged.
+The N > 1 exchange itself is covered host-side by test_multiprocess.py."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import TAG_SCENARIO, UNIFORM
+from paper_2602_05179_b200 import Context, Customer, RoutingInstance
+from paper_2602_05179_b200 import _capi as A
+
+pytestmark = pytest.mark.gpu
+
+
+def _workload(oracle):
+    n, m = 50, 3000
+    inst = RoutingInstance(n, 100, True, 0.0, oracle.make_random_instance(n, 1))
+    tours = np.stack([np.arange(1, n + 1, dtype=np.int32),
+                      (np.random.default_rng(2).permutation(n) + 1).astype(np.int32)])
+    dem = oracle.generate(UNIFORM, 1, 10, oracle.derive_stream(1, TAG_SCENARIO, 0), n, m)
+    return inst, tours, dem
+
+
+def test_single_rank_communicator_keeps_results(oracle):
+    inst, tours, dem = _workload(oracle)
+    with Context(0) as plain:
+        want = plain.split_eval(inst, tours, dem)
+    with Context(0) as ctx:
+        uid = Context.nccl_unique_id()
+        assert len(uid) == A.NCCL_ID_BYTES
+        ctx.comm_init_rank(uid, 1, 0)
+        got = ctx.split_eval(inst, tours, dem)
+        assert got["agg"] == want["agg"]
+        np.testing.assert_array_equal(got["totals"], want["totals"])
+        H = 6
+        cust = [Customer(U=60, I0=30, H=H, fixed=np.full((H, 2), 20.0), unit=np.full((H, 2), 0.5))]
+        dd = oracle.generate(UNIFORM, 0, 25, 3, H, 777)
+        a = ctx.dsirp_eval(cust, dd)
+        ctx.comm_destroy()
+        b = ctx.dsirp_eval(cust, dd)
+        assert a["agg"] == b["agg"]
+
+
+def test_in_process_communicator(oracle):
+    inst, tours, dem = _workload(oracle)
+    lib = A.load()
+    ctx = Context(0)
+    try:
+        want = ctx.split_eval(inst, tours, dem)
+        arr = (C.c_void_p * 1)(ctx.handle)
+        A.check(lib.scendp_comm_init_all(arr, 1))
+        got = ctx.split_eval(inst, tours, dem)
+        assert got["agg"] == want["agg"]
+        A.check(lib.scendp_comm_destroy(ctx.handle))
+    finally:
+        ctx.close()
