@@ -24,6 +24,8 @@
 // so customer parameters are CTA-uniform (shared memory) and demand rows
 // c*H+t are coalesced 128-byte lines of the tiled layout.
 #include <algorithm>
+#include <string_view>
+#include <unordered_map>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -160,6 +162,28 @@ bool prepare_int(const scendp_customer& s, int H, CustDev& d, std::vector<int32_
   return true;
 }
 
+// Bytes of everything the device tables of one customer depend on (the
+// scenarios, outputs and flags aside): equal bytes => equal tables.
+void append_customer_key(const scendp_customer& s, int H, std::vector<char>& key) {
+  auto put = [&key](const void* p, size_t n) {
+    const char* c = static_cast<const char*>(p);
+    key.insert(key.end(), c, c + n);
+  };
+  const int32_t ints[6] = {s.capacity, s.initial_inventory, H, s.options, s.delivery_tabular,
+                           s.holding_tabular};
+  const double dbl[2] = {s.holding, s.stockout_multiplier};
+  put(ints, sizeof(ints));
+  put(dbl, sizeof(dbl));
+  const size_t HR = static_cast<size_t>(H) * s.options;
+  if (s.delivery_tabular) {
+    put(s.delivery_table, static_cast<size_t>(H) * (s.capacity + 1) * 8);
+  } else {
+    put(s.fixed, HR * 8);
+    put(s.unit, HR * 8);
+  }
+  if (s.holding_tabular) put(s.holding_table, static_cast<size_t>(s.capacity + 1) * 8);
+}
+
 }  // namespace
 
 extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_customer* customers,
@@ -182,48 +206,80 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     const uint32_t nc = n_customers;
     CUDA_CHECK(cudaSetDevice(ctx->device));
 
-    // customer records + parameter pool
-    std::vector<CustDev> cds(nc, CustDev{});
-    std::vector<double> pool;
-    int maxR = 1;
+    // customer records + parameter pools.  Customers with identical
+    // parameters share one table set; a call whose whole customer set equals
+    // the previous call's reuses the device tables as they are.
+    const bool want_int = !(flags & SCENDP_DSIRP_FP64);
+    std::vector<char> key;
+    std::vector<size_t> kofs(nc + 1, 0);
     for (uint32_t c = 0; c < nc; ++c) {
-      const scendp_customer& s = customers[c];
-      CustDev& d = cds[c];
-      d.U = s.capacity;
-      d.I0 = s.initial_inventory;
-      d.H = H;
-      d.R = s.options;
-      d.h = s.holding;
-      d.rh = s.stockout_multiplier * s.holding;
-      d.del_tab = s.delivery_tabular;
-      d.hold_tab = s.holding_tabular;
-      maxR = std::max(maxR, s.options);
-      const size_t HR = static_cast<size_t>(H) * s.options;
-      d.off_fixed = pool.size();
-      if (!s.delivery_tabular) pool.insert(pool.end(), s.fixed, s.fixed + HR);
-      d.off_unit = pool.size();
-      if (!s.delivery_tabular) pool.insert(pool.end(), s.unit, s.unit + HR);
-      d.off_dtable = pool.size();
-      if (s.delivery_tabular)
-        pool.insert(pool.end(), s.delivery_table, s.delivery_table + static_cast<size_t>(H) * (s.capacity + 1));
-      d.off_htable = pool.size();
-      if (s.holding_tabular) pool.insert(pool.end(), s.holding_table, s.holding_table + s.capacity + 1);
+      append_customer_key(customers[c], H, key);
+      kofs[c + 1] = key.size();
     }
-    if (pool.empty()) pool.push_back(0.0);
-    // exact scaled-integer path when every customer admits it
-    std::vector<int32_t> ipool;
-    bool int_path = !(flags & SCENDP_DSIRP_FP64);
-    for (uint32_t c = 0; c < nc && int_path; ++c) int_path = prepare_int(customers[c], H, cds[c], ipool);
-    if (ipool.empty()) ipool.push_back(0);
-    const size_t o_pool = (nc * sizeof(CustDev) + 15) & ~size_t(15);
-    const size_t o_ipool = (o_pool + pool.size() * 8 + 15) & ~size_t(15);
-    char* dcust = static_cast<char*>(ctx->scratch_get(kScrCustomers, o_ipool + ipool.size() * 4));
-    CustDev* d_cust = reinterpret_cast<CustDev*>(dcust);
-    double* d_pool = reinterpret_cast<double*>(dcust + o_pool);
-    int32_t* d_ipool = reinterpret_cast<int32_t*>(dcust + o_ipool);
-    ctx->copy(d_cust, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice);
-    ctx->copy(d_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice);
-    ctx->copy(d_ipool, ipool.data(), ipool.size() * 4, cudaMemcpyHostToDevice);
+    key.push_back(want_int ? 1 : 0);
+    bool int_path;
+    int maxR = 1;
+    if (!ctx->dsirp_key.empty() && ctx->dsirp_key == key) {
+      int_path = ctx->dsirp_int_path;
+      maxR = ctx->dsirp_maxR;
+    } else {
+      std::vector<CustDev> cds(nc, CustDev{});
+      std::vector<double> pool;
+      std::vector<int32_t> ipool;
+      int_path = want_int;
+      std::unordered_map<std::string_view, uint32_t> seen;  // key bytes -> first customer
+      for (uint32_t c = 0; c < nc; ++c) {
+        const scendp_customer& s = customers[c];
+        maxR = std::max(maxR, s.options);
+        const std::string_view kc(key.data() + kofs[c], kofs[c + 1] - kofs[c]);
+        const auto hit = seen.find(kc);
+        if (hit != seen.end()) {
+          cds[c] = cds[hit->second];
+          continue;
+        }
+        seen.emplace(kc, c);
+        CustDev& d = cds[c];
+        d.U = s.capacity;
+        d.I0 = s.initial_inventory;
+        d.H = H;
+        d.R = s.options;
+        d.h = s.holding;
+        d.rh = s.stockout_multiplier * s.holding;
+        d.del_tab = s.delivery_tabular;
+        d.hold_tab = s.holding_tabular;
+        const size_t HR = static_cast<size_t>(H) * s.options;
+        d.off_fixed = pool.size();
+        if (!s.delivery_tabular) pool.insert(pool.end(), s.fixed, s.fixed + HR);
+        d.off_unit = pool.size();
+        if (!s.delivery_tabular) pool.insert(pool.end(), s.unit, s.unit + HR);
+        d.off_dtable = pool.size();
+        if (s.delivery_tabular)
+          pool.insert(pool.end(), s.delivery_table, s.delivery_table + static_cast<size_t>(H) * (s.capacity + 1));
+        d.off_htable = pool.size();
+        if (s.holding_tabular) pool.insert(pool.end(), s.holding_table, s.holding_table + s.capacity + 1);
+        // exact scaled-integer path when every customer admits it
+        if (int_path) int_path = prepare_int(s, H, d, ipool);
+      }
+      if (pool.empty()) pool.push_back(0.0);
+      if (ipool.empty()) ipool.push_back(0);
+      const size_t o_pool = (nc * sizeof(CustDev) + 15) & ~size_t(15);
+      const size_t o_ipool = (o_pool + pool.size() * 8 + 15) & ~size_t(15);
+      ctx->dsirp_key.clear();
+      char* dc = static_cast<char*>(ctx->scratch_get(kScrCustomers, o_ipool + ipool.size() * 4));
+      ctx->copy(dc, cds.data(), nc * sizeof(CustDev), cudaMemcpyHostToDevice);
+      ctx->copy(dc + o_pool, pool.data(), pool.size() * 8, cudaMemcpyHostToDevice);
+      ctx->copy(dc + o_ipool, ipool.data(), ipool.size() * 4, cudaMemcpyHostToDevice);
+      ctx->dsirp_key = std::move(key);
+      ctx->dsirp_int_path = int_path;
+      ctx->dsirp_maxR = maxR;
+      ctx->dsirp_o_pool = o_pool;
+      ctx->dsirp_o_ipool = o_ipool;
+    }
+    // layout of kScrCustomers (rebuilt above or reused): records | pool | ipool
+    char* dcust = static_cast<char*>(ctx->scratch[kScrCustomers]);
+    const CustDev* d_cust = reinterpret_cast<const CustDev*>(dcust);
+    const double* d_pool = reinterpret_cast<const double*>(dcust + ctx->dsirp_o_pool);
+    const int32_t* d_ipool = reinterpret_cast<const int32_t*>(dcust + ctx->dsirp_o_ipool);
     const size_t smem = static_cast<size_t>(H) * maxR * 2 * sizeof(double);
 
     auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, nc * sizeof(scendp_agg_raw)));

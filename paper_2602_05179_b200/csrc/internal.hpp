@@ -88,6 +88,13 @@ struct scendp_ctx {
   void sync();
   void allreduce_agg(void* dev_raw, uint64_t words);  // NCCL, if attached
   void* pinned_agg(uint64_t bytes);
+  // DSIRP customer tables resident in kScrCustomers: the serialized customer
+  // set they were built from (calls with an identical set skip the host
+  // preparation and the upload)
+  std::vector<char> dsirp_key;
+  bool dsirp_int_path = false;
+  int dsirp_maxR = 1;
+  size_t dsirp_o_pool = 0, dsirp_o_ipool = 0;  // offsets inside kScrCustomers
   // page-locked staging buffers (SCNB ingestion double buffering)
   void* stage_pinned[2] = {nullptr, nullptr};
   uint64_t stage_pinned_bytes[2] = {0, 0};

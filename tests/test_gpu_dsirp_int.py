@@ -80,3 +80,40 @@ def test_ties_between_options(ctx, reference):
               OCustomer(20, 10, H, 0.25, 3.0, fixed=fixed, unit=unit))]
     dem = np.random.default_rng(1).integers(0, 12, size=(999, H)).astype(np.uint32)
     check(ctx, reference, custs, dem, H)
+
+
+def test_customer_table_cache_and_dedupe(ctx, reference):
+    """Identical customers share one table set, and a call with the same
+    customer set as the previous call reuses the device tables; alternating
+    sets, the FP64 flag and in-place edits of the caller's arrays must all
+    invalidate correctly."""
+    from oracle import UNIFORM
+    from oracle import Customer as RCustomer
+    from paper_2602_05179_b200 import Customer
+    H = 5
+    fa = np.tile(30.0 + 4.0 * np.arange(2.0), (H, 1))
+    ua = np.tile(0.5 + 0.25 * np.arange(2.0), (H, 1))
+    fb = fa + 1.5
+    set_a = [Customer(U=40, I0=20, H=H, fixed=fa, unit=ua) for _ in range(3)]
+    set_b = [Customer(U=40, I0=20, H=H, fixed=fa, unit=ua),
+             Customer(U=40, I0=20, H=H, fixed=fb, unit=ua),
+             Customer(U=40, I0=20, H=H, fixed=fa, unit=ua)]
+    dd = reference.generate(UNIFORM, 0, 25, 9, 3, H, 500)
+
+    def want(custs):
+        out = []
+        for c, cu in enumerate(custs):
+            rc = RCustomer(40, 20, H, 1.0, 2.0, fixed=cu.fixed, unit=cu.unit)
+            out.append(reference.expected_cost(rc, dd[:, c * H:(c + 1) * H])[0])
+        return np.stack(out)
+
+    wa, wb = want(set_a), want(set_b)
+    for custs, w in ((set_a, wa), (set_a, wa), (set_b, wb), (set_a, wa), (set_b, wb)):
+        np.testing.assert_array_equal(ctx.dsirp_eval(custs, dd)["totals"], w)
+        np.testing.assert_array_equal(ctx.dsirp_eval(custs, dd, fp64=True)["totals"], w)
+    # editing the caller's array in place between calls is seen
+    fixed = fa.copy()
+    c1 = [Customer(U=40, I0=20, H=H, fixed=fixed, unit=ua) for _ in range(3)]
+    np.testing.assert_array_equal(ctx.dsirp_eval(c1, dd)["totals"], wa)
+    fixed += 1.5
+    np.testing.assert_array_equal(ctx.dsirp_eval(c1, dd)["totals"], want(c1))
