@@ -70,6 +70,13 @@ __device__ __forceinline__ uint32_t uniform_draw(const GenParams& g, uint64_t x)
 // The value of one next() output x (uniform or poisson).
 __device__ __forceinline__ uint32_t draw_value(const GenParams& g, uint64_t x);
 
+// uniform_draw for a launch known to have span < 2^32 (no tests).
+__device__ __forceinline__ uint32_t uniform_draw32(const GenParams& g, uint64_t x) {
+  const uint64_t lo = static_cast<uint64_t>(static_cast<uint32_t>(x)) * g.span32;
+  const uint64_t hi = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * g.span32 + (lo >> 32);
+  return static_cast<uint32_t>(g.lo) + static_cast<uint32_t>(hi >> 32);
+}
+
 // One counter-based draw: DistributionSpec::sample for the kinds that use
 // exactly one next() per value (scenario.cpp:23-26; poisson: SURVEY App. A).
 __device__ __forceinline__ uint32_t draw_counter(const GenParams& g,

@@ -51,7 +51,9 @@ namespace {
 constexpr int kRing = 16;  // deque ring entries per thread (power of two)
 constexpr double kInfD = __builtin_huge_val();
 
-enum Src { kSrcTiled = 0, kSrcGen = 1 };
+// kSrcGenU32: generated uniform draws with span < 2^32 (the common case),
+// specialized in K1 so no per-draw distribution test remains
+enum Src { kSrcTiled = 0, kSrcGen = 1, kSrcGenU32 = 2 };
 
 struct SplitArgs {
   int32_t n;
@@ -96,6 +98,7 @@ struct SplitArgs {
 __device__ __forceinline__ uint32_t demand_at(const SplitArgs& a, int src, uint64_t stream,
                                               const uint32_t* tile_base, uint32_t row) {
   if (src == kSrcTiled) return __ldg(tile_base + static_cast<uint64_t>(row) * kTile);
+  if (src == kSrcGenU32) return uniform_draw32(a.gen, mix64(stream + row * kGamma));
   return draw_counter(a.gen, stream, row);
 }
 
@@ -577,9 +580,11 @@ void set_smem(K kernel, size_t bytes) {
                                   static_cast<int>(bytes)));
 }
 
-template <bool FULL, int SRC>
+template <bool FULL, int KSRC>
 void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic_scratch,
                  uint64_t generic_stride, int generic_blocks) {
+  // K1 takes the specialized source; every other kernel the generic one
+  constexpr int SRC = KSRC == kSrcGenU32 ? kSrcGen : KSRC;
   const int n = a.n;
   // deque form needs Q < 2^31 (u32 window arithmetic); the quadratic form
   // needs its per-thread arrays to fit in shared memory
@@ -621,11 +626,11 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
       kernel<<<grid, T, smem, ctx->stream>>>(a);
     };
     if (intv) {
-      if (a.ident) go(split_linear_kernel<FULL, SRC, true, true>);
-      else go(split_linear_kernel<FULL, SRC, true, false>);
+      if (a.ident) go(split_linear_kernel<FULL, KSRC, true, true>);
+      else go(split_linear_kernel<FULL, KSRC, true, false>);
     } else {
-      if (a.ident) go(split_linear_kernel<FULL, SRC, false, true>);
-      else go(split_linear_kernel<FULL, SRC, false, false>);
+      if (a.ident) go(split_linear_kernel<FULL, KSRC, false, true>);
+      else go(split_linear_kernel<FULL, KSRC, false, false>);
     }
   } else {
     const int T = quad_threads(n);
@@ -839,11 +844,14 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ovf_items = d_ovf_items;
       a.ovf_cap = ovf_cap;
       CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
+      const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
       if (full) {
-        if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        if (u32) launch_wave<true, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        else if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
         else launch_wave<true, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
       } else {
-        if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        if (u32) launch_wave<false, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        else if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
         else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
       }
     }

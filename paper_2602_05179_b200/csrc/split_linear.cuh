@@ -195,13 +195,17 @@ __device__ __forceinline__ void k1_demand4(const SplitArgs& a, uint64_t stream,
     d1 = __ldg(p + kTile);
     d2 = __ldg(p + 2 * kTile);
     d3 = __ldg(p + 3 * kTile);
-  } else if constexpr (IDENT && SRC == kSrcGen) {
+  } else if constexpr (IDENT && SRC != kSrcTiled) {
     // rows s0..s0+3: consecutive SplitMix64 counters, one multiply per chunk
     const uint64_t ctr = stream + static_cast<uint64_t>(static_cast<uint32_t>(s0)) * kGamma;
-    d0 = draw_value(a.gen, mix64(ctr));
-    d1 = draw_value(a.gen, mix64(ctr + kGamma));
-    d2 = draw_value(a.gen, mix64(ctr + 2 * kGamma));
-    d3 = draw_value(a.gen, mix64(ctr + 3 * kGamma));
+    auto val = [&](uint64_t x) {
+      if constexpr (SRC == kSrcGenU32) return uniform_draw32(a.gen, x);
+      else return draw_value(a.gen, x);
+    };
+    d0 = val(mix64(ctr));
+    d1 = val(mix64(ctr + kGamma));
+    d2 = val(mix64(ctr + 2 * kGamma));
+    d3 = val(mix64(ctr + 3 * kGamma));
   } else {
     uint4 c;
     if constexpr (IDENT) c = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
