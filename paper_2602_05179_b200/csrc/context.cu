@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -172,6 +173,23 @@ void* scendp_ctx::pinned_stage(int idx, uint64_t bytes) {
   return stage_pinned[idx];
 }
 
+void* scendp_ctx::pinned_tables(uint64_t bytes) {
+  if (tables_done) CUDA_CHECK(cudaEventSynchronize(tables_done));
+  if (tables_pinned_bytes >= bytes) return tables_pinned;
+  if (tables_pinned) CUDA_CHECK(cudaFreeHost(tables_pinned));
+  tables_pinned = nullptr;
+  tables_pinned_bytes = 0;
+  const uint64_t want = std::max<uint64_t>(bytes, 64 << 10);
+  CUDA_CHECK(cudaMallocHost(&tables_pinned, want));
+  tables_pinned_bytes = want;
+  return tables_pinned;
+}
+
+void scendp_ctx::tables_uploaded() {
+  if (!tables_done) CUDA_CHECK(cudaEventCreateWithFlags(&tables_done, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventRecord(tables_done, stream));
+}
+
 int scendp_ctx::timing_begin(int kind) {
   if (!(opts.flags & SCENDP_CTX_KERNEL_TIMING)) return -1;
   const int idx = static_cast<int>(pending.size());
@@ -270,6 +288,8 @@ void scendp_ctx_destroy(scendp_ctx* ctx) {
   if (ctx->agg_pinned) cudaFreeHost(ctx->agg_pinned);
   for (void* p : ctx->stage_pinned)
     if (p) cudaFreeHost(p);
+  if (ctx->tables_pinned) cudaFreeHost(ctx->tables_pinned);
+  if (ctx->tables_done) cudaEventDestroy(ctx->tables_done);
   for (auto& p : ctx->event_pool) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);

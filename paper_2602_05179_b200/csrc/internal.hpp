@@ -99,6 +99,13 @@ struct scendp_ctx {
   void* stage_pinned[2] = {nullptr, nullptr};
   uint64_t stage_pinned_bytes[2] = {0, 0};
   void* pinned_stage(int idx, uint64_t bytes);
+  // pinned staging of per-call tables (split tour tables); the event marks
+  // the last upload from it, so the next call waits only if it is pending
+  void* tables_pinned = nullptr;
+  uint64_t tables_pinned_bytes = 0;
+  cudaEvent_t tables_done = nullptr;
+  void* pinned_tables(uint64_t bytes);
+  void tables_uploaded();
 };
 
 namespace scendp_host {

@@ -24,6 +24,8 @@
 // penalized cand = ((f + dist[i]) + ret) + beta*(double)excess.  Ties keep
 // the earliest predecessor (strict <), as the reference.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -574,10 +576,22 @@ int quad_threads(int n) {
   return std::min(t, 256);
 }
 
+// cudaFuncSetAttribute only when a (device, kernel) needs more dynamic
+// shared memory than already granted (it is a driver call per launch
+// otherwise).
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  const auto key = std::make_pair(dev, reinterpret_cast<const void*>(kernel));
+  std::lock_guard<std::mutex> g(mu);
+  auto it = granted.find(key);
+  if (it != granted.end() && it->second >= bytes) return;
   CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
+  granted[key] = bytes;
 }
 
 template <bool FULL, int KSRC>
@@ -727,7 +741,12 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const size_t o_f0d = put(tt.f0d.data(), tt.f0d.size() * 8);
     const size_t o_f0i = put(tt.f0i.data(), tt.f0i.size() * 4);
     char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, blob.size()));
-    ctx->copy(dtab, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    // through the context's pinned staging (an async DMA, no driver-side
+    // bounce copy); the previous call's upload from it must have finished
+    char* stage = static_cast<char*>(ctx->pinned_tables(blob.size()));
+    std::memcpy(stage, blob.data(), blob.size());
+    ctx->copy(dtab, stage, blob.size(), cudaMemcpyHostToDevice);
+    ctx->tables_uploaded();
     const double* d_dist = reinterpret_cast<const double*>(dtab + o_dist);
     const double* d_ret = reinterpret_cast<const double*>(dtab + o_ret);
     const double* d_c0 = reinterpret_cast<const double*>(dtab + o_c0);
