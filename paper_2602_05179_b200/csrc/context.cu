@@ -139,6 +139,7 @@ void* scendp_ctx::scratch_get(int slot, uint64_t bytes) {
   if (bytes == 0) bytes = 256;
   if (scratch_bytes[slot] >= bytes) return scratch[slot];
   if (slot == scendp_host::kScrCustomers) dsirp_key.clear();  // tables move
+  if (slot == scendp_host::kScrTours) tours_dev = nullptr;
   if (scratch[slot]) {
     CUDA_CHECK(cudaStreamSynchronize(stream));
     CUDA_CHECK(cudaFree(scratch[slot]));

@@ -105,6 +105,8 @@ struct scendp_ctx {
   uint64_t tables_pinned_bytes = 0;
   cudaEvent_t tables_done = nullptr;
   void* pinned_tables(uint64_t bytes);
+  std::vector<char> tours_blob;  // split tour tables resident at tours_dev
+  void* tours_dev = nullptr;
   void tables_uploaded();
 };
 

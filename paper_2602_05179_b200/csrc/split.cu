@@ -741,12 +741,17 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const size_t o_f0d = put(tt.f0d.data(), tt.f0d.size() * 8);
     const size_t o_f0i = put(tt.f0i.data(), tt.f0i.size() * 4);
     char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, blob.size()));
-    // through the context's pinned staging (an async DMA, no driver-side
-    // bounce copy); the previous call's upload from it must have finished
-    char* stage = static_cast<char*>(ctx->pinned_tables(blob.size()));
-    std::memcpy(stage, blob.data(), blob.size());
-    ctx->copy(dtab, stage, blob.size(), cudaMemcpyHostToDevice);
-    ctx->tables_uploaded();
+    // unchanged tables (same instance and tours as the previous call, same
+    // device buffer) are not uploaded again; otherwise through the context's
+    // pinned staging (an async DMA, no driver-side bounce copy)
+    if (dtab != ctx->tours_dev || blob != ctx->tours_blob) {
+      char* stage = static_cast<char*>(ctx->pinned_tables(blob.size()));
+      std::memcpy(stage, blob.data(), blob.size());
+      ctx->copy(dtab, stage, blob.size(), cudaMemcpyHostToDevice);
+      ctx->tables_uploaded();
+      ctx->tours_blob = blob;
+      ctx->tours_dev = dtab;
+    }
     const double* d_dist = reinterpret_cast<const double*>(dtab + o_dist);
     const double* d_ret = reinterpret_cast<const double*>(dtab + o_ret);
     const double* d_c0 = reinterpret_cast<const double*>(dtab + o_c0);
@@ -754,8 +759,12 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
 
     trace.mark("tables");
     // aggregates
-    auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw)));
-    CUDA_CHECK(cudaMemsetAsync(d_agg, 0, k * sizeof(scendp_agg_raw), ctx->stream));
+    // raw aggregates [k] followed by the overflow counter of the first wave:
+    // one memset clears both
+    char* aggbuf = static_cast<char*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw) + 16));
+    auto* d_agg = reinterpret_cast<unsigned long long*>(aggbuf);
+    unsigned int* d_ovf_count = reinterpret_cast<unsigned int*>(aggbuf + k * sizeof(scendp_agg_raw));
+    CUDA_CHECK(cudaMemsetAsync(aggbuf, 0, k * sizeof(scendp_agg_raw) + 16, ctx->stream));
 
     // outputs: device destinations (caller's device buffers when tiled/device
     // layout matches, else scratch)
@@ -796,7 +805,6 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     // overflow list + generic-path scratch
     const uint32_t ovf_cap = 1u << 16;
     char* ovf = static_cast<char*>(ctx->scratch_get(kScrOverflow, 16 + ovf_cap * 8ull));
-    auto* d_ovf_count = reinterpret_cast<unsigned int*>(ovf);
     auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + 16);
     const int generic_blocks = ctx->sm_count * kGenericBlocksPerSm;
     const uint64_t generic_stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
@@ -862,7 +870,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ovf_count = d_ovf_count;
       a.ovf_items = d_ovf_items;
       a.ovf_cap = ovf_cap;
-      CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
+      if (w0 > 0) CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
       const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
       if (full) {
         if (u32) launch_wave<true, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
