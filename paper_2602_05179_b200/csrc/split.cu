@@ -429,17 +429,40 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
 }
 
 // ---- host ----------------------------------------------------------------
-struct TourTables {
-  std::vector<double> dist, ret, c0;
-  std::vector<uint32_t> col;
-  // K1 chunked tables
+// Tour-only tables, written in place into one staging blob (one H2D copy);
+// sections 16-byte aligned.  Per tour q, positions i = 0..n:
+//   dist/ret/c0/col [k][n+1]   (generic / quadratic kernels)
+//   ccol [k][npad]             (K1 / K2-int column table, slot s = position s+1)
+//   itab [k][2][npad] int32    (exact integer path) | dtab [k][4][npad] fp64
+//   f0d [k], f0i [k]           (f(0))
+struct TableLayout {
   int npad = 0;
-  bool intv = false;  // every tour admits the exact integer path
+  size_t o_dist, o_ret, o_c0, o_col, o_ccol, o_f0d, o_f0i, o_tab, bytes;
+  TableLayout(int n, uint32_t k) {
+    const size_t n1 = static_cast<size_t>(n) + 1;
+    npad = ((n + 3) / 4) * 4 + 4;
+    size_t off = 0;
+    auto sec = [&off](size_t bytes) {
+      const size_t o = (off + 15) & ~size_t(15);
+      off = o + bytes;
+      return o;
+    };
+    o_dist = sec(k * n1 * 8);
+    o_ret = sec(k * n1 * 8);
+    o_c0 = sec(k * n1 * 8);
+    o_col = sec(k * n1 * 4);
+    o_ccol = sec(static_cast<size_t>(k) * npad * 4);
+    o_f0d = sec(static_cast<size_t>(k) * 8);
+    o_f0i = sec(static_cast<size_t>(k) * 4);
+    o_tab = sec(static_cast<size_t>(k) * 4 * npad * 8);  // itab or dtab, whichever applies
+    bytes = (off + 15) & ~size_t(15);
+  }
+};
+
+struct TourTables {
+  bool intv = false;  // every tour admits the exact integer path (itab at o_tab)
   bool ident = false; // every tour is the identity (contiguous demand rows)
   double costbound = 0.0;  // max over tours of dist_n + sum(c0 + ret) + max c0
-  std::vector<uint32_t> ccol;
-  std::vector<int32_t> itab, f0i;
-  std::vector<double> dtab, f0d;
 };
 
 void validate_instance(const scendp_routing* inst) {
@@ -483,42 +506,46 @@ void validate_tour(const int32_t* tour, int n) {
 }
 
 // Tour-only prefix constants, in the reference's sequential order
-// (fill_prefixes, split.cpp:24-39).
-void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, TourTables& t) {
-  const int n = inst->n, side = n + 2;
+// (fill_prefixes, split.cpp:24-39), built straight into `blob` (layout L).
+// The integer-path check: all tour costs integral and every partial sum
+// < 2^29, so each fp64 op of the reference is exact and integer adds
+// reproduce it bit for bit.
+void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
+                  const TableLayout& L, char* blob, TourTables& t) {
+  const int n = inst->n, side = n + 2, npad = L.npad;
   const size_t n1 = static_cast<size_t>(n) + 1;
-  t.dist.assign(k * n1, 0.0);
-  t.ret.assign(k * n1, 0.0);
-  t.c0.assign(k * n1, 0.0);
-  t.col.assign(k * n1, 0u);
   const double* c = inst->costs;
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(blob + o); };
+  double* dist_all = D(L.o_dist);
+  double* ret_all = D(L.o_ret);
+  double* c0_all = D(L.o_c0);
+  uint32_t* col_all = reinterpret_cast<uint32_t*>(blob + L.o_col);
+  uint32_t* ccol_all = reinterpret_cast<uint32_t*>(blob + L.o_ccol);
+  double* f0d = D(L.o_f0d);
+  int32_t* f0i = reinterpret_cast<int32_t*>(blob + L.o_f0i);
+  bool intv = true, ident = true;
+  double costbound = 0.0;
   for (uint32_t q = 0; q < k; ++q) {
-    const int32_t* s = tours + static_cast<size_t>(q) * n;
-    double* dist = t.dist.data() + q * n1;
+    const int32_t* sq = tours + static_cast<size_t>(q) * n;
+    double* dist = dist_all + q * n1;
+    double* ret = ret_all + q * n1;
+    double* c0 = c0_all + q * n1;
+    uint32_t* col = col_all + q * n1;
+    uint32_t* ccol = ccol_all + static_cast<size_t>(q) * npad;
     dist[0] = 0.0;
     dist[1] = 0.0;
-    for (int i = 2; i <= n; ++i) dist[i] = dist[i - 1] + c[s[i - 2] * side + s[i - 1]];
+    for (int i = 2; i <= n; ++i) dist[i] = dist[i - 1] + c[sq[i - 2] * side + sq[i - 1]];
+    ret[0] = 0.0;
+    col[0] = 0u;
     for (int i = 1; i <= n; ++i) {
-      t.ret[q * n1 + i] = c[s[i - 1] * side + (n + 1)];
-      t.col[q * n1 + i] = static_cast<uint32_t>(s[i - 1] - 1);
+      ret[i] = c[sq[i - 1] * side + (n + 1)];
+      col[i] = static_cast<uint32_t>(sq[i - 1] - 1);
+      ccol[i - 1] = col[i];
+      ident &= sq[i - 1] == i;
     }
-    for (int i = 0; i < n; ++i) t.c0[q * n1 + i] = c[0 * side + s[i]];
-  }
-  // chunked K1 tables (slot s = position s+1) and the integer-path check:
-  // all tour costs integral and every partial sum < 2^29, so each fp64 op of
-  // the reference is exact and integer adds reproduce it bit for bit.
-  const int npad = ((n + 3) / 4) * 4 + 4;
-  t.npad = npad;
-  t.ccol.assign(static_cast<size_t>(k) * npad, 0u);
-  t.itab.assign(static_cast<size_t>(k) * 2 * npad, 0);
-  t.dtab.assign(static_cast<size_t>(k) * 4 * npad, 0.0);
-  t.f0d.assign(k, 0.0);
-  t.f0i.assign(k, 0);
-  bool intv = true;
-  for (uint32_t q = 0; q < k; ++q) {
-    const double* dist = t.dist.data() + q * n1;
-    const double* ret = t.ret.data() + q * n1;
-    const double* c0 = t.c0.data() + q * n1;
+    for (int i = n; i < npad; ++i) ccol[i] = 0u;
+    for (int i = 0; i < n; ++i) c0[i] = c[0 * side + sq[i]];
+    c0[n] = 0.0;
     double bound = dist[n], cmax = 0.0;
     bool integral = true;
     for (int i = 0; i <= n; ++i) {
@@ -529,39 +556,39 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k, 
     }
     bound += cmax;
     intv &= integral && bound < static_cast<double>(1 << 29);
-    t.costbound = std::max(t.costbound, bound);
-    t.f0d[q] = (0.0 + c0[0]) - dist[1];
-    for (int i = 1; i <= n; ++i) {
-      const size_t sidx = static_cast<size_t>(i - 1);
-      t.ccol[q * npad + sidx] = t.col[q * n1 + i];
-      double* dt = t.dtab.data() + static_cast<size_t>(q) * 4 * npad;
-      dt[0 * npad + sidx] = dist[i];
-      dt[1 * npad + sidx] = ret[i];
-      dt[2 * npad + sidx] = c0[i];
-      dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
-    }
+    costbound = std::max(costbound, bound);
+    f0d[q] = (0.0 + c0[0]) - dist[1];
   }
-  t.intv = intv;
-  t.ident = true;
-  for (uint32_t q = 0; q < k && t.ident; ++q)
-    for (int i = 0; i < n; ++i)
-      if (tours[static_cast<size_t>(q) * n + i] != i + 1) {
-        t.ident = false;
-        break;
-      }
-  if (intv) {
-    for (uint32_t q = 0; q < k; ++q) {
-      const double* dist = t.dist.data() + q * n1;
-      const double* ret = t.ret.data() + q * n1;
-      const double* c0 = t.c0.data() + q * n1;
-      t.f0i[q] = static_cast<int32_t>(t.f0d[q]);
-      int32_t* it = t.itab.data() + static_cast<size_t>(q) * 2 * npad;
+  // per-position K1/K2 tables: integer A/B when every tour admits it, else
+  // the fp64 quadruple
+  for (uint32_t q = 0; q < k; ++q) {
+    const double* dist = dist_all + q * n1;
+    const double* ret = ret_all + q * n1;
+    const double* c0 = c0_all + q * n1;
+    if (intv) {
+      f0i[q] = static_cast<int32_t>(f0d[q]);
+      int32_t* it = reinterpret_cast<int32_t*>(blob + L.o_tab) + static_cast<size_t>(q) * 2 * npad;
       for (int i = 1; i <= n; ++i) {
         it[0 * npad + (i - 1)] = static_cast<int32_t>(dist[i] + ret[i]);
         it[1 * npad + (i - 1)] = i < n ? static_cast<int32_t>(c0[i] - dist[i + 1]) : 0;
       }
+      for (int i = n; i < npad; ++i) it[i] = it[npad + i] = 0;
+    } else {
+      f0i[q] = 0;
+      double* dt = D(L.o_tab) + static_cast<size_t>(q) * 4 * npad;
+      for (int i = 1; i <= n; ++i) {
+        const size_t sidx = static_cast<size_t>(i - 1);
+        dt[0 * npad + sidx] = dist[i];
+        dt[1 * npad + sidx] = ret[i];
+        dt[2 * npad + sidx] = c0[i];
+        dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
+      }
+      for (int i = n; i < npad; ++i) dt[i] = dt[npad + i] = dt[2 * npad + i] = dt[3 * npad + i] = 0.0;
     }
   }
+  t.intv = intv;
+  t.ident = ident;
+  t.costbound = costbound;
 }
 
 constexpr int kMaxQuadSmem = 200 * 1024;
@@ -719,39 +746,35 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     trace.mark("validate");
     CUDA_CHECK(cudaSetDevice(ctx->device));
 
-    // tour tables
+    // tour tables, built in the context's pinned staging buffer (the
+    // previous call's upload from it has finished) and uploaded in one
+    // async copy -- unless they equal the tables already resident on the
+    // device (same instance and tours as the previous call; small K only,
+    // where the comparison is cheap)
     TourTables tt;
-    build_tables(inst, tours, k, tt);
+    const TableLayout L(n, k);
     const size_t n1 = static_cast<size_t>(n) + 1;
-    // one staging blob -> one H2D copy; sections 16-byte aligned
-    std::vector<char> blob;
-    auto put = [&blob](const void* src, size_t bytes) {
-      const size_t off = (blob.size() + 15) & ~size_t(15);
-      blob.resize(off + bytes);
-      if (bytes) std::memcpy(blob.data() + off, src, bytes);
-      return off;
-    };
-    const size_t o_dist = put(tt.dist.data(), tt.dist.size() * 8);
-    const size_t o_ret = put(tt.ret.data(), tt.ret.size() * 8);
-    const size_t o_c0 = put(tt.c0.data(), tt.c0.size() * 8);
-    const size_t o_col = put(tt.col.data(), tt.col.size() * 4);
-    const size_t o_ccol = put(tt.ccol.data(), tt.ccol.size() * 4);
-    const size_t o_itab = put(tt.itab.data(), tt.itab.size() * 4);
-    const size_t o_dtab = put(tt.dtab.data(), tt.dtab.size() * 8);
-    const size_t o_f0d = put(tt.f0d.data(), tt.f0d.size() * 8);
-    const size_t o_f0i = put(tt.f0i.data(), tt.f0i.size() * 4);
-    char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, blob.size()));
-    // unchanged tables (same instance and tours as the previous call, same
-    // device buffer) are not uploaded again; otherwise through the context's
-    // pinned staging (an async DMA, no driver-side bounce copy)
-    if (dtab != ctx->tours_dev || blob != ctx->tours_blob) {
-      char* stage = static_cast<char*>(ctx->pinned_tables(blob.size()));
-      std::memcpy(stage, blob.data(), blob.size());
-      ctx->copy(dtab, stage, blob.size(), cudaMemcpyHostToDevice);
+    char* stage = static_cast<char*>(ctx->pinned_tables(L.bytes));
+    build_tables(inst, tours, k, L, stage, tt);
+    const size_t used = tt.intv ? L.o_tab + static_cast<size_t>(k) * 2 * L.npad * 4 : L.bytes;
+    char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, L.bytes));
+    constexpr size_t kCacheBytes = 256 << 10;
+    const bool cacheable = used <= kCacheBytes;
+    if (!cacheable || dtab != ctx->tours_dev || ctx->tours_blob.size() != used ||
+        std::memcmp(ctx->tours_blob.data(), stage, used) != 0) {
+      ctx->copy(dtab, stage, used, cudaMemcpyHostToDevice);
       ctx->tables_uploaded();
-      ctx->tours_blob = blob;
-      ctx->tours_dev = dtab;
+      if (cacheable) {
+        ctx->tours_blob.assign(stage, stage + used);
+        ctx->tours_dev = dtab;
+      } else {
+        ctx->tours_blob.clear();
+        ctx->tours_dev = nullptr;
+      }
     }
+    const size_t o_dist = L.o_dist, o_ret = L.o_ret, o_c0 = L.o_c0, o_col = L.o_col,
+                 o_ccol = L.o_ccol, o_f0d = L.o_f0d, o_f0i = L.o_f0i;
+    const size_t o_itab = L.o_tab, o_dtab = L.o_tab;
     const double* d_dist = reinterpret_cast<const double*>(dtab + o_dist);
     const double* d_ret = reinterpret_cast<const double*>(dtab + o_ret);
     const double* d_c0 = reinterpret_cast<const double*>(dtab + o_c0);
@@ -840,7 +863,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ret = d_ret;
       a.c0 = d_c0;
       a.col = d_col;
-      a.npad = tt.npad;
+      a.npad = L.npad;
       a.ident = tt.ident ? 1 : 0;
       // K2-int eligibility: integral tour costs (tt.intv) and an integral
       // beta; loads up to pen_lmax keep every sum exact and inside int32
