@@ -464,10 +464,12 @@ def secondary(ctx, d: Dist, args):
         path = os.path.join(td, "c2.scnb")
         ctx.scnb_write(path, arr)
         ctx.scnb_load(path).free()  # warm the page cache and staging buffers
-        t0 = time.perf_counter()
-        buf = ctx.scnb_load(path)
-        wall = time.perf_counter() - t0
-        buf.free()
+        wall = float("inf")
+        for _ in range(3):  # best of 3 (the host page cache is shared)
+            t0 = time.perf_counter()
+            buf = ctx.scnb_load(path)
+            wall = min(wall, time.perf_counter() - t0)
+            buf.free()
     out["scnb_ingest"] = {"value": arr.nbytes / wall / 1e9, "unit": "GB/s (file -> tiled HBM)",
                           "bytes": arr.nbytes, "wall_ms": wall * 1e3,
                           "note": "page-cached file, pread -> pinned -> H2D -> to_tiled"}
