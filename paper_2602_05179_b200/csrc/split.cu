@@ -638,8 +638,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   if (!linear && !a.hard && a.pen_lmax > 0 && small_tables) {
     const int T = kPenThreads;
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + 2 * 4) +
-                        static_cast<size_t>(T) * (kRing * (8 + (FULL ? 4 : 0)) +
-                                                  kPosRing * (8 + (FULL ? 8 : 0)));
+                        static_cast<size_t>(T) * penal_ring_bytes(FULL);
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {
       set_smem(kernel, smem);
@@ -870,7 +869,9 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       // (|values| <= 2 (costbound + beta * L) < 2^30); larger loads are
       // detected per scenario and re-run on the generic fp64 path
       a.pen_lmax = 0;
-      if (!inst->hard && tt.intv && !(flags & SCENDP_QUADRATIC) &&
+      // (the kernel's 16-bit rings need Q < 2^15 and n < 2^16)
+      if (!inst->hard && tt.intv && !(flags & SCENDP_QUADRATIC) && inst->capacity < 32768 &&
+          n < 65536 &&
           inst->penalty_beta == std::floor(inst->penalty_beta) && inst->penalty_beta >= 0.0 &&
           inst->penalty_beta <= 1048576.0) {
         const double room = static_cast<double>(1 << 29) - tt.costbound;

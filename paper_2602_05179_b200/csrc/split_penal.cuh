@@ -21,9 +21,11 @@
 // mode never produces +inf (every p is admissible), so no masking is needed.
 //
 // Per thread: the deque ring (f, position) and a position ring holding
-// (L_p, PM(p)) for p in [lo-1, i]; per position the window start advances
-// with one shared load per step and the B candidate is one more load.  All
-// ring counters are byte offsets (slot * 4T), masked on access.  The kernel
+// (L_p mod 2^16, PM(p)) for p in [lo-1, i]; per position the window start
+// advances with one shared load per step and the B candidate is one more
+// load.  Ring counters are byte offsets of 2-byte slots, masked on access
+// (see kH below); 16-bit loads and positions keep the CTA at 6 per SM
+// (host: Q < 2^15, so every tested window difference <= 2Q fits).  The kernel
 // assumes d_i <= Q (the window never empties, so the deque is never empty
 // after the front evictions); a larger demand, a window longer than the
 // position ring, a deque overflow or a load beyond the exact int32 range
@@ -33,13 +35,28 @@
 
 constexpr int kPenThreads = 128;
 constexpr int kPosRing = 32;                  // positions per thread
-constexpr int kPosStep = kPenThreads * 4;     // bytes per ring slot (all threads)
-constexpr int kPosMask = kPosRing * kPosStep - 1;
+// Ring counters are byte offsets of 2-byte slots (slot * 2T): 2-byte
+// elements (loads mod 2^16, deque positions) sit at (c & mask), 4-byte ones
+// at (c & mask) << 1 (one LOP3 + LEA either way).  Shared memory per thread:
+// deque 16 x (4 + 2) B, positions 32 x (2 + 4) B = 288 B (6 CTAs/SM) -- the
+// kernel is latency-bound, so occupancy is worth the narrower slots.
+constexpr int kH = kPenThreads * 2;           // bytes per 2-byte slot (all threads)
+constexpr int kDqMaskH = kRing * kH - 1;
+constexpr int kPosMaskH = kPosRing * kH - 1;
 constexpr int32_t kPenInf = 0x7fffffff;
 
 template <typename E>
-__device__ __forceinline__ E& pos_at(E* base, int c) {
-  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + (c & kPosMask));
+__device__ __forceinline__ E& at16(E* base, int c, int mask) {  // 2-byte element
+  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + (c & mask));
+}
+template <typename E>
+__device__ __forceinline__ E& at32(E* base, int c, int mask) {  // 4-byte element
+  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + ((c & mask) << 1));
+}
+
+// Host side: bytes of the K2-int rings per thread (split.cu sizes the CTA).
+__host__ __device__ constexpr int penal_ring_bytes(bool full) {
+  return kRing * (4 + 2 + (full ? 4 : 0)) + kPosRing * (2 + 4 + (full ? 8 : 0));
 }
 
 template <bool FULL, int SRC, bool IDENT>
@@ -51,7 +68,17 @@ split_penal_kernel(SplitArgs a) {
   const uint32_t k = blockIdx.y;
   const int n = a.n;
   const int npad = a.npad;
-  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem);
+  const int tid = threadIdx.x;
+  // thread-minor rings, 4-byte arrays first: deque f [| rc], positions PM
+  // [| PM index | PM rc]; then the 2-byte arrays: deque positions, loads
+  int32_t* dq_f = reinterpret_cast<int32_t*>(smem) + tid;
+  int32_t* dq_r = dq_f + kRing * T;                                            // FULL
+  int32_t* ps_pm = dq_f + (FULL ? 2 : 1) * kRing * T;
+  int32_t* ps_pi = ps_pm + kPosRing * T;                                       // FULL
+  int32_t* ps_pr = ps_pi + kPosRing * T;                                       // FULL
+  uint16_t* dq_p = reinterpret_cast<uint16_t*>(ps_pm - tid + (FULL ? 3 : 1) * kPosRing * T) + tid;
+  uint16_t* ps_l = dq_p + kRing * T;
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + T * penal_ring_bytes(FULL));
   int32_t* s_tab = reinterpret_cast<int32_t*>(s_col + (IDENT ? 0 : npad));  // A | B
   {
     const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
@@ -60,23 +87,13 @@ split_penal_kernel(SplitArgs a) {
     const int32_t* g = a.itab + static_cast<uint64_t>(k) * 2 * npad;
     for (int x = threadIdx.x; x < 2 * npad; x += T) s_tab[x] = g[x];
   }
-  const int tid = threadIdx.x;
-  // thread-minor rings: deque [kRing][T] f | position (| rc);
-  // positions [kPosRing][T] L | PM (| PM index | PM rc)
-  int32_t* dq_f = s_tab + 2 * npad + tid;
-  int32_t* dq_p = dq_f + kRing * T;
-  int32_t* dq_r = dq_p + kRing * T;                                          // FULL
-  uint32_t* ps_l = reinterpret_cast<uint32_t*>(dq_f + (FULL ? 3 : 2) * kRing * T);
-  int32_t* ps_pm = reinterpret_cast<int32_t*>(ps_l + kPosRing * T);
-  int32_t* ps_pi = ps_pm + kPosRing * T;                                     // FULL
-  int32_t* ps_pr = ps_pi + kPosRing * T;                                     // FULL
   agg_cta_init(s_agg);
   __syncthreads();
 
   const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;
   const bool active = wl < a.m_wave;
   const uint64_t w = a.w_base + wl;
-  uint32_t Qc = static_cast<uint32_t>(a.Q);
+  uint32_t Qc = static_cast<uint32_t>(a.Q);  // host: Q < 2^15 (16-bit window differences)
   Qc += static_cast<uint32_t>(a.m_total >> 62);  // + 0, keeps Q in a register
   const int32_t beta = static_cast<int32_t>(a.beta);
   const uint32_t lmax = a.pen_lmax;  // loads above this leave the exact range
@@ -100,7 +117,7 @@ split_penal_kernel(SplitArgs a) {
     }
     // position 0: f(0) = (0.0 + c(0, s_1)) - dist[1], L_0 = 0, g(0) = f(0)
     const int32_t f0 = a.f0i[k];
-    ps_l[0] = 0u;
+    ps_l[0] = 0;
     ps_pm[0] = f0;
     if (FULL) {
       ps_pi[0] = 0;
@@ -111,18 +128,22 @@ split_penal_kernel(SplitArgs a) {
     dq_f[T] = f0;
     dq_p[T] = 0;
     if (FULL) dq_r[T] = 0;
-    int head = kStep, tail = 2 * kStep;  // deque slot counters (bytes)
+    int head = kH, tail = 2 * kH;       // deque slot counters
     int32_t front_f = f0, back_f = f0;
-    int front_c = 0;                    // position counter (bytes) of the front
+    int front_p = 0;                    // position of the deque front
     int32_t front_rc = 0;
-    int lo_c = 0;                       // window start lo, as a position counter
+    int lo_c = 0;                       // window start lo, as a position counter (lo * kH)
     int32_t bmin = kPenInf;             // PM(lo - 1); kPenInf while lo == 0
     int32_t bidx = -1, brc = 0;
     int32_t pm = f0, pm_i = 0, pm_rc = 0;  // running prefix minimum of g
     uint32_t load = 0;
+    // window test on 16-bit loads: exact, every tested difference is <= 2Q
+    auto out_of_window = [&](int c) {
+      return static_cast<uint32_t>(static_cast<uint16_t>(load - at16(ps_l, c, kPosMaskH))) > Qc;
+    };
 
-    // one DP position (i_c = i * kPosStep); ring capacities are checked per
-    // chunk by the caller (room for the chunk's pushes)
+    // one DP position (i_c = i * kH); ring capacities are checked per chunk
+    // by the caller (room for the chunk's pushes)
     auto step = [&](int i, int i_c, uint32_t d, auto push_tag) {
       constexpr bool PUSH = decltype(push_tag)::value;
       const int sl = i - 1;
@@ -130,26 +151,27 @@ split_penal_kernel(SplitArgs a) {
       load += d;
       // the window start advances past positions whose route (p, i]
       // overflows; d_i <= Q keeps p = i-1 inside, so no bound test is needed
-      if (load - pos_at(ps_l, lo_c) > Qc) {
+      if (out_of_window(lo_c)) {
         do {
-          lo_c += kPosStep;
-        } while (load - pos_at(ps_l, lo_c) > Qc);
-        const int pc = lo_c - kPosStep;  // lo - 1
-        bmin = pos_at(ps_pm, pc);
+          lo_c += kH;
+        } while (out_of_window(lo_c));
+        const int pc = lo_c - kH;  // lo - 1
+        bmin = at32(ps_pm, pc, kPosMaskH);
         if (FULL) {
-          bidx = pos_at(ps_pi, pc);
-          brc = pos_at(ps_pr, pc);
+          bidx = at32(ps_pi, pc, kPosMaskH);
+          brc = at32(ps_pr, pc, kPosMaskH);
         }
         // deque entries before lo leave from the front (entry i-1 stays);
         // the vacated slot becomes the -inf sentinel below the head
-        if (front_c < lo_c) {
+        const int lo = lo_c / kH;
+        if (front_p < lo) {
           do {
-            ring_at(dq_f, head) = INT32_MIN;
-            head += kStep;
-            front_c = ring_at(dq_p, head);
-          } while (front_c < lo_c);
-          front_f = ring_at(dq_f, head);
-          if (FULL) front_rc = ring_at(dq_r, head);
+            at32(dq_f, head, kDqMaskH) = INT32_MIN;
+            head += kH;
+            front_p = at16(dq_p, head, kDqMaskH);
+          } while (front_p < lo);
+          front_f = at32(dq_f, head, kDqMaskH);
+          if (FULL) front_rc = at32(dq_r, head, kDqMaskH);
         }
       }
       // candidates: window A (deque front) and prefix B (prefix minimum)
@@ -160,7 +182,7 @@ split_penal_kernel(SplitArgs a) {
       if (FULL) {
         rc = (useB ? brc : front_rc) + 1;
         Vout[static_cast<uint64_t>(i) * kTile] = static_cast<double>(v);
-        Cout[static_cast<uint64_t>(i) * kTile] = useB ? bidx : front_c / kPosStep;
+        Cout[static_cast<uint64_t>(i) * kTile] = useB ? bidx : front_p;
       }
       if constexpr (PUSH) {
         const int32_t fi = v + Bi;
@@ -172,29 +194,29 @@ split_penal_kernel(SplitArgs a) {
             pm_rc = rc;
           }
         }
-        pos_at(ps_l, i_c) = load;
-        pos_at(ps_pm, i_c) = pm;
+        at16(ps_l, i_c, kPosMaskH) = static_cast<uint16_t>(load);
+        at32(ps_pm, i_c, kPosMaskH) = pm;
         if (FULL) {
-          pos_at(ps_pi, i_c) = pm_i;
-          pos_at(ps_pr, i_c) = pm_rc;
+          at32(ps_pi, i_c, kPosMaskH) = pm_i;
+          at32(ps_pr, i_c, kPosMaskH) = pm_rc;
         }
         // strict pop (sentinel-terminated), then push (K1 deque); the deque
         // is non-empty here, so it can only empty by popping
         if (back_f > fi) {
           do {
-            tail -= kStep;
-            back_f = ring_at(dq_f, tail - kStep);
+            tail -= kH;
+            back_f = at32(dq_f, tail - kH, kDqMaskH);
           } while (back_f > fi);
           if (tail == head) {
             front_f = fi;
-            front_c = i_c;
+            front_p = i;
             if (FULL) front_rc = rc;
           }
         }
-        ring_at(dq_f, tail) = fi;
-        ring_at(dq_p, tail) = i_c;
-        if (FULL) ring_at(dq_r, tail) = rc;
-        tail += kStep;
+        at32(dq_f, tail, kDqMaskH) = fi;
+        at16(dq_p, tail, kDqMaskH) = static_cast<uint16_t>(i);
+        if (FULL) at32(dq_r, tail, kDqMaskH) = rc;
+        tail += kH;
         back_f = fi;
       }
     };
@@ -213,8 +235,8 @@ split_penal_kernel(SplitArgs a) {
     // room for 4 pushes: the position ring must hold [lo-1, i] for every i
     // of the chunk, the deque its live entries + 4 + the sentinel slot
     auto room = [&](int s0) {
-      return (s0 + 4) * kPosStep - lo_c <= (kPosRing - 2) * kPosStep &&
-             (tail - head) + 4 * kStep <= (kRing - 1) * kStep;
+      return (s0 + 4) * kH - lo_c <= (kPosRing - 2) * kH &&
+             (tail - head) + 4 * kH <= (kRing - 1) * kH;
     };
     // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
     const int npush = n - 1;
@@ -229,7 +251,7 @@ split_penal_kernel(SplitArgs a) {
         break;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) step(s0 + j + 1, (s0 + j + 1) * kPosStep, dc[j], Push{});
+      for (int j = 0; j < 4; ++j) step(s0 + j + 1, (s0 + j + 1) * kH, dc[j], Push{});
 #pragma unroll
       for (int j = 0; j < 4; ++j) dc[j] = dn[j];
     }
@@ -242,8 +264,8 @@ split_penal_kernel(SplitArgs a) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int i = s0 + j + 1;
-          if (i < n) step(i, i * kPosStep, dc[j], Push{});
-          else if (i == n) step(i, i * kPosStep, dc[j], Last{});
+          if (i < n) step(i, i * kH, dc[j], Push{});
+          else if (i == n) step(i, i * kH, dc[j], Last{});
         }
       }
     }
