@@ -315,7 +315,7 @@ class Context:
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    quadratic: bool = False, out_kind: str = "host",
                    device_out: Optional[dict] = None, sync: bool = True,
-                   host_totals: Optional[np.ndarray] = None) -> dict:
+                   host_totals: Optional[np.ndarray] = None, raw: bool = False) -> dict:
         """Evaluate tours (k x n, 1-based ids) on a scenario set.
 
         Returns totals [k][m] (host), V/cuts [m][n+1], route_count, feasible
@@ -353,6 +353,10 @@ class Context:
             ptr = lambda key: dv[key].ptr if key in dv else None  # noqa: E731
             o = A.SplitOut(kind, ptr("totals"), ptr("values"), ptr("cuts"), ptr("route_count"),
                            ptr("feasible"), agg if sync else None, None)
+        if raw:
+            raws = (A.AggRaw * k)()
+            o.agg_raw = raws
+            res["agg_raw"] = raws
         A.check(self.lib.scendp_split_eval(self.handle, C.byref(rinst), tours.ctypes.data, k,
                                            C.byref(sc), flags, C.byref(o)))
         if sync or out_kind == "host":
@@ -365,7 +369,7 @@ class Context:
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    out_kind: str = "host", device_out: Optional[dict] = None,
                    sync: bool = True, fp64: bool = False,
-                   host_totals: Optional[np.ndarray] = None) -> dict:
+                   host_totals: Optional[np.ndarray] = None, raw: bool = False) -> dict:
         nc = len(customers)
         H = customers[0].H
         carr = (A.Customer * nc)(*[c.as_c() for c in customers])
@@ -394,6 +398,10 @@ class Context:
             o = A.DsirpOut(kind, ptr("totals"), ptr("evaluated"), ptr("deliver"),
                            ptr("quantity"), ptr("end_inventory"), ptr("route_option"),
                            agg if sync else None, None)
+        if raw:
+            raws = (A.AggRaw * nc)()
+            o.agg_raw = raws
+            res["agg_raw"] = raws
         A.check(self.lib.scendp_dsirp_eval(self.handle, carr, nc, C.byref(sc), flags,
                                            C.byref(o)))
         if sync or out_kind == "host":
