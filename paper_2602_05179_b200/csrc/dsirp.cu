@@ -189,6 +189,7 @@ void append_customer_key(const scendp_customer& s, int H, std::vector<char>& key
 extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_customer* customers,
                                            uint32_t n_customers, const scendp_scenarios* sc,
                                            uint32_t flags, const scendp_dsirp_out* out) {
+  NvtxRange nvtx("scendp_dsirp_eval");
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (!customers || n_customers == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one customer");

@@ -11,7 +11,18 @@
 
 #include "scendp_cuda.h"
 
+// NVTX (header-only v3; a no-op unless a profiler attaches): one range per
+// C-ABI call, so nsys/ncu timelines show the engine's phases by name.
+#include <nvtx3/nvToolsExt.h>
+
 namespace scendp_host {
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Thrown inside the library, converted to a status at the C-ABI boundary.
 struct Error {

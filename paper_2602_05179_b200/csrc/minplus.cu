@@ -6,9 +6,10 @@
 //
 // with the reference's scan order (option r ascending, then predecessor i
 // ascending, extended_min keeping the incumbent on ties).  The values are
-// order-independent except for the sign of a zero tie, so the kernel uses the
-// FP64 min (DMNMX) unless an input holds -0.0, in which case the exact
-// compare-and-select form runs (EXACT_TIES).
+// order-independent except for the sign of a zero tie, so the kernel uses
+// fmin (DSETP.MIN + selects; sm_100 has no FP64 min instruction) unless an
+// input holds -0.0, in which case the exact compare-and-select form runs
+// (EXACT_TIES).
 //
 // Execution model: a min-plus "GEMM" (no tensor-core form exists for the
 // (min,+) semiring).  A CTA owns a tile of kTB frontiers x kTJ columns; the
@@ -115,6 +116,7 @@ extern "C" scendp_status scendp_minplus_sweep(scendp_ctx* ctx, const scendp_minp
                                               uint32_t n_stages, const double* init,
                                               uint64_t init_size, uint64_t batch,
                                               uint32_t mem_kind, uint32_t flags, double* out) {
+  NvtxRange nvtx("scendp_minplus_sweep");
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (mem_kind != SCENDP_MEM_HOST && mem_kind != SCENDP_MEM_DEVICE)

@@ -282,6 +282,7 @@ uint64_t scendp_tiled_bytes(uint64_t rows, uint64_t count) {
 scendp_status scendp_gen_scenarios(scendp_ctx* ctx, const scendp_dist* dist, uint64_t rows,
                                    uint64_t w0, uint64_t count, uint32_t layout,
                                    uint32_t* out) {
+  NvtxRange nvtx("scendp_gen_scenarios");
   return guard([&] {
     if (!ctx || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "null ctx or output");
     check_dist(dist);

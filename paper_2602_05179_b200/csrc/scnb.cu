@@ -112,6 +112,7 @@ scendp_status scendp_scnb_header_read(const char* path, scendp_scnb_header* hdr)
 
 scendp_status scendp_scnb_load(scendp_ctx* ctx, const char* path, uint64_t first,
                                uint64_t count, uint32_t layout, uint32_t* out) {
+  NvtxRange nvtx("scendp_scnb_load");
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (layout != SCENDP_MEM_DEVICE && layout != SCENDP_MEM_DEVICE_TILED)

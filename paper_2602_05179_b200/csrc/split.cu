@@ -719,6 +719,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
                                            const scendp_scenarios* sc, uint32_t flags,
                                            const scendp_split_out* out) {
   HostTrace trace;
+  NvtxRange nvtx("scendp_split_eval");
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (!sc || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenarios/out is null");
