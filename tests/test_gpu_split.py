@@ -258,3 +258,26 @@ def test_pinned_host_totals_are_written_in_place(ctx, oracle):
     pin2 = pinned_empty(2 * 999, np.float64)
     ctx.dsirp_eval(custs, dd, host_totals=pin2)
     np.testing.assert_array_equal(pin2.reshape(2, 999), want["totals"])
+
+
+@pytest.mark.parametrize("mode", ["hard", "penalized"])
+def test_c1_poisson_generated_in_kernel(ctx, oracle, reference, mode):
+    """BASELINE C1: n=50, Q=100, 1,024 seeded Poisson(5) scenarios generated
+    inside the DP kernel (GENERATED source) == the reference evaluating the
+    same scenarios (the restated sampler over the same streams)."""
+    from paper_2602_05179_b200 import poisson_hi
+    n, m, lam = 50, 1024, 5.0
+    hi = poisson_hi(lam)
+    seed = oracle.derive_stream(1, TAG_SCENARIO, 0)
+    hard = mode == "hard"
+    costs = oracle.make_random_instance(n, 1)
+    inst = RoutingInstance(n, 100, hard, 0.0 if hard else 10.0, costs)
+    tours = [np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 3)]
+    dist = Distribution("poisson", 0, hi, mean=lam, seed=seed)
+    dem = oracle.generate(POISSON, 0, hi, seed, n, m, mean=lam)
+    for tour in tours:
+        got = ctx.split_eval(inst, tour, dist, count=m)
+        tot, (mean, fc, ic) = reference.split_costs(n, 100, 1 if hard else 0, inst.penalty_beta,
+                                                    costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        assert got["agg"][0]["mean"] == mean
