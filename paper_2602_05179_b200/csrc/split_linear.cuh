@@ -83,7 +83,9 @@ __device__ __forceinline__ VT k1_neg_inf() {
 // deque is non-empty before the pops, it can only become empty by popping,
 // so the "popped empty" front update lives inside the (rarer) pop branch.
 // SAFE = true handles any d_i (window emptied when d_i > Q).
-template <typename VT, bool FULL, bool PUSH, bool SAFE = true>
+// NOEVICT (with SAFE = false): the caller proved no eviction can happen at
+// this position (see the chunk loop), so the window test is skipped.
+template <typename VT, bool FULL, bool PUSH, bool SAFE = true, bool NOEVICT = false>
 __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
                                         VT t1, VT t2, VT t3, VT* __restrict__ rf,
                                         uint32_t* __restrict__ rl, int32_t* __restrict__ ri,
@@ -116,7 +118,7 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
         s.front_rc = ring_at(rr, hs);
       }
     }
-  } else {
+  } else if constexpr (!NOEVICT) {
     if (s.load - s.front_l > Qc) {
       do {
         ring_at(rf, s.head) = k1_neg_inf<VT>();
@@ -323,12 +325,27 @@ split_linear_kernel(SplitArgs a) {
           t3[2 * h] = y3.x; t3[2 * h + 1] = y3.y;
         }
       }
-      // fast form unless a demand of this chunk exceeds Q (window may empty)
+      // fast form unless a demand of this chunk exceeds Q (window may empty);
+      // front_l only grows, so if the chunk's last load stays within Q of
+      // the current front no position of the chunk evicts -- decided for
+      // the converged lanes together (a warp-uniform branch, no per-position
+      // window test; taken for most chunks since evictions are rare)
       if (max(max(d0, d1), max(d2, d3)) <= Qc) {
-        k1_step<VT, FULL, true, false>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
-        k1_step<VT, FULL, true, false>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
-        k1_step<VT, FULL, true, false>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
-        k1_step<VT, FULL, true, false>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+        // (measured: pays off for the fp64 and full-solution forms; the lean
+        // int32 cost-only form is faster with its per-position test)
+        constexpr bool kSplitEvict = !std::is_same<VT, int32_t>::value || FULL;
+        const uint64_t last = static_cast<uint64_t>(s.load) + d0 + d1 + d2 + d3;
+        if (kSplitEvict && __all_sync(__activemask(), last - s.front_l <= Qc)) {
+          k1_step<VT, FULL, true, false, true>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false, true>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false, true>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false, true>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+        } else {
+          k1_step<VT, FULL, true, false>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false>(s, s0 + 3, d2, Qc, t0[2], t1[2], t2[2], t3[2], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, false>(s, s0 + 4, d3, Qc, t0[3], t1[3], t2[3], t3[3], rf, rl, ri, rr, Vout, Cout);
+        }
       } else {
         k1_step<VT, FULL, true>(s, s0 + 1, d0, Qc, t0[0], t1[0], t2[0], t3[0], rf, rl, ri, rr, Vout, Cout);
         k1_step<VT, FULL, true>(s, s0 + 2, d1, Qc, t0[1], t1[1], t2[1], t3[1], rf, rl, ri, rr, Vout, Cout);
