@@ -3,6 +3,7 @@
 
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -228,14 +229,61 @@ void scendp_ctx::timing_resolve() {
 
 void scendp_ctx::sync() {
   CUDA_CHECK(cudaStreamSynchronize(stream));
+  if (comm_pending) {
+    CUDA_CHECK(cudaStreamSynchronize(comm_stream));
+    comm_pending = false;
+  }
   timing_resolve();
 }
 
+void* scendp_ctx::agg_buffer(uint64_t bytes) {
+  if (!overlapped()) return scratch_get(scendp_host::kScrAgg, bytes);
+  if (!comm_stream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_dp, cudaEventDisableTiming));
+    for (auto& e : ev_ar) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  agg_slot ^= 1;
+  if (agg_bufs_bytes < bytes) {
+    CUDA_CHECK(cudaStreamSynchronize(comm_stream));
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    for (auto& b : agg_bufs) {
+      if (b) CUDA_CHECK(cudaFree(b));
+      b = nullptr;
+    }
+    const uint64_t want = (bytes + 4095) & ~uint64_t{4095};
+    for (auto& b : agg_bufs) CUDA_CHECK(cudaMalloc(&b, want));
+    agg_bufs_bytes = want;
+    ev_ar_used[0] = ev_ar_used[1] = false;
+  }
+  // the all-reduce that last read this buffer (two calls ago) must be done
+  // before the kernels of this call clear and fill it
+  if (ev_ar_used[agg_slot]) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_ar[agg_slot], 0));
+  return agg_bufs[agg_slot];
+}
+
 void scendp_ctx::allreduce_agg(void* dev_raw, uint64_t words) {
-  if (!nccl_comm || nranks <= 1) return;
+  if (!overlapped()) return;
+  CUDA_CHECK(cudaEventRecord(ev_dp, stream));
+  CUDA_CHECK(cudaStreamWaitEvent(comm_stream, ev_dp, 0));
   nccl_check(nccl().AllReduce(dev_raw, dev_raw, words, kNcclUint64, kNcclSum,
-                              nccl_comm, stream),
+                              nccl_comm, comm_stream),
              "ncclAllReduce");
+  CUDA_CHECK(cudaEventRecord(ev_ar[agg_slot], comm_stream));
+  ev_ar_used[agg_slot] = true;
+  comm_pending = true;
+}
+
+void scendp_ctx::agg_readback(void* host, const void* dev, uint64_t bytes) {
+  if (overlapped()) {
+    // read the reduced buffer after the all-reduce, on the comm stream
+    scendp_host::cuda_check(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, comm_stream),
+                            "cudaMemcpyAsync");
+    stats.d2h_bytes += bytes;
+    comm_pending = true;
+  } else {
+    copy(host, dev, bytes, cudaMemcpyDeviceToHost);
+  }
 }
 
 // ---- C-ABI -------------------------------------------------------------------
@@ -291,6 +339,15 @@ void scendp_ctx_destroy(scendp_ctx* ctx) {
     if (p) cudaFreeHost(p);
   if (ctx->tables_pinned) cudaFreeHost(ctx->tables_pinned);
   if (ctx->tables_done) cudaEventDestroy(ctx->tables_done);
+  if (ctx->comm_stream) {
+    cudaStreamSynchronize(ctx->comm_stream);
+    cudaStreamDestroy(ctx->comm_stream);
+  }
+  if (ctx->ev_dp) cudaEventDestroy(ctx->ev_dp);
+  for (auto& e : ctx->ev_ar)
+    if (e) cudaEventDestroy(e);
+  for (void* b : ctx->agg_bufs)
+    if (b) cudaFree(b);
   for (auto& p : ctx->event_pool) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
@@ -409,6 +466,7 @@ scendp_status scendp_comm_init_rank(scendp_ctx* ctx,
     nccl_check(nccl().CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
     ctx->nccl_comm = comm;
     ctx->nranks = nranks;
+    ctx->force_overlap = std::getenv("SCENDP_OVERLAP_ALLREDUCE") != nullptr;
     ctx->rank = rank;
   });
 }
@@ -423,6 +481,7 @@ scendp_status scendp_comm_init_all(scendp_ctx** ctxs, int32_t n) {
     for (int i = 0; i < n; ++i) {
       ctxs[i]->nccl_comm = comms[i];
       ctxs[i]->nranks = n;
+      ctxs[i]->force_overlap = std::getenv("SCENDP_OVERLAP_ALLREDUCE") != nullptr;
       ctxs[i]->rank = i;
     }
   });
@@ -430,6 +489,7 @@ scendp_status scendp_comm_init_all(scendp_ctx** ctxs, int32_t n) {
 
 scendp_status scendp_comm_destroy(scendp_ctx* ctx) {
   return guard([&] {
+    ctx->sync();
     if (ctx->nccl_comm) nccl().CommDestroy(ctx->nccl_comm);
     ctx->nccl_comm = nullptr;
     ctx->nranks = 1;
@@ -447,6 +507,9 @@ scendp_status scendp_timer_start(scendp_ctx* ctx) {
 scendp_status scendp_timer_stop(scendp_ctx* ctx, double* ms) {
   return guard([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
+    // the timed region ends after the last all-reduce as well
+    if (ctx->comm_pending && ctx->ev_ar_used[ctx->agg_slot])
+      CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_ar[ctx->agg_slot], 0));
     CUDA_CHECK(cudaEventRecord(ctx->t1, ctx->stream));
     ctx->sync();
     float f = 0.f;

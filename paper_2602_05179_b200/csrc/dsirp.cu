@@ -283,7 +283,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     const int32_t* d_ipool = reinterpret_cast<const int32_t*>(dcust + ctx->dsirp_o_ipool);
     const size_t smem = static_cast<size_t>(H) * maxR * 2 * sizeof(double);
 
-    auto* d_agg = static_cast<unsigned long long*>(ctx->scratch_get(kScrAgg, nc * sizeof(scendp_agg_raw)));
+    auto* d_agg = static_cast<unsigned long long*>(ctx->agg_buffer(nc * sizeof(scendp_agg_raw)));
     CUDA_CHECK(cudaMemsetAsync(d_agg, 0, nc * sizeof(scendp_agg_raw), ctx->stream));
 
     const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
@@ -393,7 +393,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
       h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(nc * sizeof(scendp_agg_raw)));
-      ctx->copy(h_raw, d_agg, nc * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost);
+      ctx->agg_readback(h_raw, d_agg, nc * sizeof(scendp_agg_raw));
     }
     if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
     if (want_agg) {

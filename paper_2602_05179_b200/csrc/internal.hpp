@@ -97,7 +97,26 @@ struct scendp_ctx {
     else if (kind == cudaMemcpyDeviceToHost) stats.d2h_bytes += bytes;
   }
   void sync();
+  // Multi-GPU aggregates.  With a communicator of > 1 rank the raw
+  // aggregates alternate between two device buffers and the all-reduce runs
+  // on comm_stream after the DP kernels (event-ordered), so it overlaps the
+  // next call's kernels; a call waits for the all-reduce only when it reads
+  // the aggregate back (agg_readback) or reuses the buffer two calls later.
+  void* agg_buffer(uint64_t bytes);      // this call's aggregate buffer
   void allreduce_agg(void* dev_raw, uint64_t words);  // NCCL, if attached
+  void agg_readback(void* host, const void* dev, uint64_t bytes);  // after the all-reduce
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_dp = nullptr;
+  cudaEvent_t ev_ar[2] = {nullptr, nullptr};
+  bool ev_ar_used[2] = {false, false};
+  void* agg_bufs[2] = {nullptr, nullptr};
+  uint64_t agg_bufs_bytes = 0;
+  int agg_slot = 0;
+  bool comm_pending = false;  // an all-reduce is queued on comm_stream
+  // SCENDP_OVERLAP_ALLREDUCE=1 at communicator creation forces the
+  // overlapped path for a 1-rank communicator too (tests on one GPU)
+  bool force_overlap = false;
+  bool overlapped() const { return nccl_comm != nullptr && (nranks > 1 || force_overlap); }
   void* pinned_agg(uint64_t bytes);
   // DSIRP customer tables resident in kScrCustomers: the serialized customer
   // set they were built from (calls with an identical set skip the host

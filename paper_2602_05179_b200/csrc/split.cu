@@ -784,7 +784,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     // aggregates
     // raw aggregates [k] followed by the overflow counter of the first wave:
     // one memset clears both
-    char* aggbuf = static_cast<char*>(ctx->scratch_get(kScrAgg, k * sizeof(scendp_agg_raw) + 16));
+    char* aggbuf = static_cast<char*>(ctx->agg_buffer(k * sizeof(scendp_agg_raw) + 16));
     auto* d_agg = reinterpret_cast<unsigned long long*>(aggbuf);
     unsigned int* d_ovf_count = reinterpret_cast<unsigned int*>(aggbuf + k * sizeof(scendp_agg_raw));
     CUDA_CHECK(cudaMemsetAsync(aggbuf, 0, k * sizeof(scendp_agg_raw) + 16, ctx->stream));
@@ -935,7 +935,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
       h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(k * sizeof(scendp_agg_raw)));
-      ctx->copy(h_raw, d_agg, k * sizeof(scendp_agg_raw), cudaMemcpyDeviceToHost);
+      ctx->agg_readback(h_raw, d_agg, k * sizeof(scendp_agg_raw));
     }
     if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
     trace.mark("sync");

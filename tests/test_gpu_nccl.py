@@ -57,3 +57,56 @@ def test_in_process_communicator(oracle):
         A.check(lib.scendp_comm_destroy(ctx.handle))
     finally:
         ctx.close()
+
+
+def test_overlapped_allreduce_path(oracle):
+    """The multi-rank aggregate path (double-buffered aggregates, NCCL
+    all-reduce on a second stream overlapping the next call's kernels),
+    forced on a one-rank communicator: chains of asynchronous calls and
+    interleaved synchronous ones give the plain results."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, ".")
+from oracle import Oracle, TAG_SCENARIO, UNIFORM
+from paper_2602_05179_b200 import Context, Customer, RoutingInstance
+from paper_2602_05179_b200 import _capi as A
+o = Oracle()
+n, m = 50, 3000
+inst = RoutingInstance(n, 100, True, 0.0, o.make_random_instance(n, 1))
+tours = np.stack([np.arange(1, n + 1, dtype=np.int32), (np.random.default_rng(2).permutation(n) + 1).astype(np.int32)])
+dem = o.generate(UNIFORM, 1, 10, o.derive_stream(1, TAG_SCENARIO, 0), n, m)
+with Context(0) as plain:
+    want = plain.split_eval(inst, tours, dem)
+    H = 6
+    cust = [Customer(U=60, I0=30, H=H, fixed=np.full((H, 2), 20.0), unit=np.full((H, 2), 0.5))]
+    dd = o.generate(UNIFORM, 0, 25, 3, H, 777)
+    wantd = plain.dsirp_eval(cust, dd)
+with Context(0) as ctx:
+    ctx.comm_init_rank(Context.nccl_unique_id(), 1, 0)
+    scen = ctx.alloc(m * n * 4); scen.upload(dem)
+    tot = ctx.alloc(2 * m * 8)
+    for rep in range(3):
+        for _ in range(7):   # asynchronous chain: all-reduces overlap the next kernels
+            ctx.split_eval(inst, tours, (scen, A.MEM_DEVICE), count=m, out_kind="device",
+                           device_out={"totals": tot}, sync=False)
+        got = ctx.split_eval(inst, tours, dem)
+        assert got["agg"] == want["agg"], (got["agg"], want["agg"])
+        assert np.array_equal(got["totals"], want["totals"])
+        gd = ctx.dsirp_eval(cust, dd)
+        assert gd["agg"] == wantd["agg"]
+    ctx.timer_start()
+    for _ in range(5):
+        ctx.split_eval(inst, tours, (scen, A.MEM_DEVICE), count=m, out_kind="device",
+                       device_out={"totals": tot}, sync=False)
+    assert ctx.timer_stop() > 0
+    ctx.comm_destroy()
+print("overlap ok")
+'''
+    import os
+    env = dict(os.environ, SCENDP_OVERLAP_ALLREDUCE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "overlap ok" in r.stdout, r.stdout + r.stderr
