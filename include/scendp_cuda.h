@@ -130,9 +130,11 @@ typedef struct {
   uint64_t rows;            /* n (split) or n_customers*H (dsirp) */
   uint64_t count;           /* scenarios in this call (this shard) */
   uint64_t first_index;     /* global index of scenario 0 of this call: the
-                               generator stream index for GENERATED, and the
-                               tile alignment origin (must be a multiple of 32
-                               for DEVICE_TILED shards) */
+                               generator stream index for GENERATED (other
+                               kinds: informational).  A DEVICE_TILED `data`
+                               holds this call's scenario 0 in lane 0 of its
+                               first tile (a tile-aligned shard of a larger
+                               tiled set is a byte range of it) */
   const scendp_dist* dist;  /* GENERATED only */
 } scendp_scenarios;
 

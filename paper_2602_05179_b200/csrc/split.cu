@@ -736,8 +736,6 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     if (full && k_tours != 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "full solutions need k_tours == 1");
     if (full && (!out->values || !out->cuts || !out->route_count || !out->feasible))
       fail(SCENDP_ERR_INVALID_ARGUMENT, "full mode needs values, cuts, route_count, feasible");
-    if (sc->mem_kind == SCENDP_MEM_DEVICE_TILED && (sc->first_index & 31) && false)
-      fail(SCENDP_ERR_INVALID_ARGUMENT, "tiled shards must start on a tile");
     // hard mode follows the deque form (batched_expected_split, split.cpp:
     // 316-318); penalized or SCENDP_QUADRATIC -> quadratic form
     const bool linear = inst->hard && !(flags & SCENDP_QUADRATIC);
