@@ -21,7 +21,7 @@
 // mode never produces +inf (every p is admissible), so no masking is needed.
 //
 // Per thread: the deque ring (f, position) and a position ring holding
-// (L_p mod 2^16, PM(p)) for p in [lo-1, i]; per position the window start
+// (-L_p mod 2^16, PM(p)) for p in [lo-1, i]; per position the window start
 // advances with one shared load per step and the B candidate is one more
 // load.  Ring counters are byte offsets of 2-byte slots, masked on access
 // (see kH below); 16-bit loads and positions keep the CTA at 6 per SM
@@ -117,7 +117,7 @@ split_penal_kernel(SplitArgs a) {
     }
     // position 0: f(0) = (0.0 + c(0, s_1)) - dist[1], L_0 = 0, g(0) = f(0)
     const int32_t f0 = a.f0i[k];
-    ps_l[0] = 0;
+    ps_l[0] = 0;  // -L_0 mod 2^16
     ps_pm[0] = f0;
     if (FULL) {
       ps_pi[0] = 0;
@@ -138,8 +138,10 @@ split_penal_kernel(SplitArgs a) {
     int32_t pm = f0, pm_i = 0, pm_rc = 0;  // running prefix minimum of g
     uint32_t load = 0;
     // window test on 16-bit loads: exact, every tested difference is <= 2Q
+    // (the ring holds -L mod 2^16, so the test is one add and one mask)
     auto out_of_window = [&](int c) {
-      return static_cast<uint32_t>(static_cast<uint16_t>(load - at16(ps_l, c, kPosMaskH))) > Qc;
+      const uint32_t nl16 = at16(ps_l, c, kPosMaskH);  // zero-extended
+      return ((load + nl16) & 0xffffu) > Qc;
     };
 
     // one DP position (i_c = i * kH); ring capacities are checked per chunk
@@ -194,7 +196,7 @@ split_penal_kernel(SplitArgs a) {
             pm_rc = rc;
           }
         }
-        at16(ps_l, i_c, kPosMaskH) = static_cast<uint16_t>(load);
+        at16(ps_l, i_c, kPosMaskH) = static_cast<uint16_t>(0u - load);
         at32(ps_pm, i_c, kPosMaskH) = pm;
         if (FULL) {
           at32(ps_pi, i_c, kPosMaskH) = pm_i;
