@@ -146,10 +146,8 @@ split_penal_kernel(SplitArgs a) {
 
     // one DP position (i_c = i * kH); ring capacities are checked per chunk
     // by the caller (room for the chunk's pushes)
-    auto step = [&](int i, int i_c, uint32_t d, auto push_tag) {
+    auto step = [&](int i, int i_c, uint32_t d, int32_t Ai, int32_t Bi, auto push_tag) {
       constexpr bool PUSH = decltype(push_tag)::value;
-      const int sl = i - 1;
-      const int32_t Ai = s_tab[sl], Bi = s_tab[npad + sl];
       load += d;
       // the window start advances past positions whose route (p, i]
       // overflows; d_i <= Q keeps p = i-1 inside, so no bound test is needed
@@ -226,11 +224,20 @@ split_penal_kernel(SplitArgs a) {
     // ahead of their use: the gathers hit L2 (C5 reuses each scenario tile
     // for every tour), and without the prefetch every position waits on one
     auto load4 = [&](int s0, uint32_t (&dd)[4]) {
+      // the column table is padded (npad >= n + 4, multiple of 4): one
+      // 128-bit load for the chunk's rows
+      uint4 cr = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
+      if (!IDENT) cr = *reinterpret_cast<const uint4*>(s_col + s0);
+      const uint32_t rows[4] = {cr.x, cr.y, cr.z, cr.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int sl = s0 + j;
-        dd[j] = sl < n ? demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]) : 0u;
-      }
+      for (int j = 0; j < 4; ++j)
+        dd[j] = s0 + j < n ? demand_at(a, SRC, stream, tile_base, rows[j]) : 0u;
+    };
+    // tour constants of slots s0..s0+3 (A = dist+ret, B = c0 - dist_next):
+    // two 128-bit broadcast loads per chunk
+    auto tab4 = [&](int s0, int4& A4, int4& B4) {
+      A4 = *reinterpret_cast<const int4*>(s_tab + s0);
+      B4 = *reinterpret_cast<const int4*>(s_tab + npad + s0);
     };
     using Push = std::true_type;
     using Last = std::false_type;
@@ -252,8 +259,12 @@ split_penal_kernel(SplitArgs a) {
         ok = false;
         break;
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) step(s0 + j + 1, (s0 + j + 1) * kH, dc[j], Push{});
+      int4 A4, B4;
+      tab4(s0, A4, B4);
+      step(s0 + 1, (s0 + 1) * kH, dc[0], A4.x, B4.x, Push{});
+      step(s0 + 2, (s0 + 2) * kH, dc[1], A4.y, B4.y, Push{});
+      step(s0 + 3, (s0 + 3) * kH, dc[2], A4.z, B4.z, Push{});
+      step(s0 + 4, (s0 + 4) * kH, dc[3], A4.w, B4.w, Push{});
 #pragma unroll
       for (int j = 0; j < 4; ++j) dc[j] = dn[j];
     }
@@ -266,8 +277,9 @@ split_penal_kernel(SplitArgs a) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int i = s0 + j + 1;
-          if (i < n) step(i, i * kH, dc[j], Push{});
-          else if (i == n) step(i, i * kH, dc[j], Last{});
+          const int32_t Ai = s_tab[i - 1], Bi = s_tab[npad + i - 1];
+          if (i < n) step(i, i * kH, dc[j], Ai, Bi, Push{});
+          else if (i == n) step(i, i * kH, dc[j], Ai, Bi, Last{});
         }
       }
     }
