@@ -298,9 +298,12 @@ class Context:
         """scen: host ndarray (count, rows) | (DeviceBuffer, kind) | Distribution."""
         keep = []
         if isinstance(scen, np.ndarray):
-            arr = np.ascontiguousarray(scen, np.uint32)
+            arr = np.ascontiguousarray(np.atleast_2d(scen), np.uint32)
             keep.append(arr)
-            sc = A.Scenarios(A.MEM_HOST, arr.ctypes.data, rows, arr.shape[0], first_index, None)
+            # the array's own row count: the C-ABI rejects a mismatch with the
+            # instance (split.cpp:128-138, oudp.cpp:402-407)
+            sc = A.Scenarios(A.MEM_HOST, arr.ctypes.data, arr.shape[1], arr.shape[0],
+                             first_index, None)
         elif isinstance(scen, Distribution):
             d = scen.as_c()
             keep.append(d)
