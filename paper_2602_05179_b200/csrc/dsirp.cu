@@ -335,6 +335,8 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       a.ipool = d_ipool;
       a.nc = nc;
       a.H = H;
+      a.all_std_hold = 1;
+      for (uint32_t c = 0; c < nc; ++c) a.all_std_hold &= customers[c].holding_tabular ? 0 : 1;
       a.rows = sc->rows;
       a.m_wave = mw;
       a.w_base = w0;

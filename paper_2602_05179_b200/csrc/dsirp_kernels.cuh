@@ -35,6 +35,7 @@ struct DsirpArgs {
   const int32_t* ipool;  // integer tables (gkeys, scaled holding tables)
   uint32_t nc;
   int32_t H;
+  int32_t all_std_hold;  // every customer uses the standard holding model
   uint64_t rows;         // nc * H
   uint64_t m_wave, w_base, m_total;
   const uint32_t* tiled; // wave-local tiled demands
@@ -290,7 +291,9 @@ dsirp_kernel(DsirpArgs a) {
 // packed keys with strict < over states in ascending order yields the
 // reference's (value, option, state) order.  A demand above `dlim` (bounds)
 // sends the unit through dsirp_unit_fp64 instead (global parameters).
-template <int HMAX, bool FULL>
+// STDHOLD: every customer of the launch uses the standard holding model
+// h*J + rho*h*s (no per-evaluation table test).
+template <int HMAX, bool FULL, bool STDHOLD = false>
 __global__ void __launch_bounds__(kDsirpThreads)
 dsirp_int_kernel(DsirpArgs a) {
   constexpr int K = HMAX + 1;
@@ -332,7 +335,7 @@ dsirp_int_kernel(DsirpArgs a) {
                                           w, dem, ok);
     } else {
       auto hold = [&](int j, int s) -> int32_t {
-        if (htabular) return __ldg(htab + j);
+        if (!STDHOLD && htabular) return __ldg(htab + j);
         return hI * j + rhI * s;
       };
       int st[K];
@@ -470,8 +473,13 @@ void launch_exact(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_pat
 template <int HMAX>
 void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
   if (int_path) {
-    if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0);
-    else launch_kernel(ctx, dsirp_int_kernel<HMAX, false>, a, 0);
+    if (a.all_std_hold) {
+      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true, true>, a, 0);
+      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false, true>, a, 0);
+    } else {
+      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0);
+      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false>, a, 0);
+    }
   } else {
     if (full) launch_kernel(ctx, dsirp_kernel<HMAX, true>, a, smem);
     else launch_kernel(ctx, dsirp_kernel<HMAX, false>, a, smem);
