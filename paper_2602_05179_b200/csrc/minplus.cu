@@ -6,10 +6,9 @@
 //
 // with the reference's scan order (option r ascending, then predecessor i
 // ascending, extended_min keeping the incumbent on ties).  The values are
-// order-independent except for the sign of a zero tie, so the kernel uses
-// fmin (DSETP.MIN + selects; sm_100 has no FP64 min instruction) unless an
-// input holds -0.0, in which case the exact compare-and-select form runs
-// (EXACT_TIES).
+// order-independent except for the sign of a zero tie; the kernel runs the
+// reference's own compare-and-select (extended_min, exact for signed zeros
+// and NaN alike), which on sm_100 is also cheaper than fmin.
 //
 // Execution model: a min-plus "GEMM" (no tensor-core form exists for the
 // (min,+) semiring).  A CTA owns a tile of kTB frontiers x kTJ columns; the
@@ -104,12 +103,6 @@ minplus_stage_kernel(const double* __restrict__ in, uint64_t in_stride,
   }
 }
 
-bool has_neg_zero(const double* p, uint64_t n) {
-  for (uint64_t k = 0; k < n; ++k)
-    if (p[k] == 0.0 && std::signbit(p[k])) return true;
-  return false;
-}
-
 }  // namespace
 
 extern "C" scendp_status scendp_minplus_sweep(scendp_ctx* ctx, const scendp_minplus_stage* stages,
@@ -143,12 +136,11 @@ extern "C" scendp_status scendp_minplus_sweep(scendp_ctx* ctx, const scendp_minp
     if (!init || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "init/out is null");
     CUDA_CHECK(cudaSetDevice(ctx->device));
     const bool host = mem_kind == SCENDP_MEM_HOST;
-    bool exact = (flags & SCENDP_MINPLUS_EXACT_TIES) != 0;
-    if (host && !exact) {
-      exact = has_neg_zero(init, batch * init_size);
-      for (uint32_t s = 0; s < n_stages && !exact; ++s)
-        exact = has_neg_zero(stages[s].entries, stages[s].depth * stages[s].rows * stages[s].cols);
-    }
+    // The compare-select form is extended_min itself (cost.hpp:39-41: NaN and
+    // signed-zero semantics included) and it is also the cheaper one on
+    // sm_100 (DSETP + 2 selects; fmin lowers to DSETP.MIN + selects + NaN
+    // quieting), so it always runs; the flag is kept for ABI compatibility.
+    const bool exact = true;
     // device staging: stage matrices (host kind), input frontiers, outputs
     std::vector<const double*> dA(n_stages);
     if (host) {
