@@ -8,9 +8,9 @@
 // contiguous file range and a prefix of m scenarios is a file prefix.
 //
 // B200 path: no host ScenarioBatch is materialized.  The shard is streamed in
-// chunks of whole 32-scenario tiles: pread() fills one of two page-locked
-// staging buffers while the previous chunk's H2D copy runs on the context
-// stream; each chunk then lands in device memory either as is (reference
+// chunks of whole 32-scenario tiles: pread() (split over up to 8 host
+// threads) fills one of two page-locked staging buffers while the previous
+// chunk's H2D copy runs on the context stream; each chunk then lands in device memory either as is (reference
 // layout) or through to_tiled_kernel into its tile range of the native layout
 // (tile t of the shard depends only on chunk t*32/C, so chunks never overlap).
 // The reference's error messages and exception class (runtime_error) are kept.
@@ -22,6 +22,8 @@
 #include <cerrno>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -56,6 +58,11 @@ uint32_t le32(const unsigned char* b) {
          (static_cast<uint32_t>(b[2]) << 16) | (static_cast<uint32_t>(b[3]) << 24);
 }
 
+// pread of `bytes` at `off` split over up to `threads` host threads (the
+// page-cache copy is the bottleneck of the pipeline, not PCIe).
+void read_parallel(int fd, void* dst, uint64_t bytes, uint64_t off, const std::string& name,
+                   const char* what, int threads);
+
 void read_full(int fd, void* dst, uint64_t bytes, uint64_t off, const std::string& name,
                const char* what) {
   char* p = static_cast<char*>(dst);
@@ -67,6 +74,31 @@ void read_full(int fd, void* dst, uint64_t bytes, uint64_t off, const std::strin
     off += static_cast<uint64_t>(r);
     bytes -= static_cast<uint64_t>(r);
   }
+}
+
+void read_parallel(int fd, void* dst, uint64_t bytes, uint64_t off, const std::string& name,
+                   const char* what, int threads) {
+  constexpr uint64_t kMinPart = 8ull << 20;
+  const int parts = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(threads), bytes / kMinPart)));
+  if (parts == 1) return read_full(fd, dst, bytes, off, name, what);
+  const uint64_t per = ((bytes + parts - 1) / parts + 4095) & ~uint64_t{4095};
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(parts);
+  for (int p = 0; p < parts; ++p) {
+    const uint64_t lo = std::min(bytes, per * p), hi = std::min(bytes, per * (p + 1));
+    if (lo >= hi) break;
+    pool.emplace_back([&, p, lo, hi] {
+      try {
+        read_full(fd, static_cast<char*>(dst) + lo, hi - lo, off + lo, name, what);
+      } catch (const Error& e) {
+        errs[p] = e.msg;
+      }
+    });
+  }
+  for (auto& t : pool) t.join();
+  for (const auto& e : errs)
+    if (!e.empty()) fail(SCENDP_ERR_RUNTIME, e);
 }
 
 // Header checks in the reference's order and wording (io.cpp:316-333).
@@ -132,6 +164,7 @@ scendp_status scendp_scnb_load(scendp_ctx* ctx, const char* path, uint64_t first
     uint64_t chunk = std::max<uint64_t>(32, (kChunkBytes / col_bytes) & ~uint64_t{31});
     chunk = std::min(chunk, (count + 31) & ~uint64_t{31});
     const uint64_t stage_bytes = chunk * col_bytes;
+    const int readers = static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
     char* pin[2] = {static_cast<char*>(ctx->pinned_stage(0, stage_bytes)),
                     static_cast<char*>(ctx->pinned_stage(1, stage_bytes))};
     uint32_t* dstage = layout == SCENDP_MEM_DEVICE_TILED
@@ -145,8 +178,8 @@ scendp_status scendp_scnb_load(scendp_ctx* ctx, const char* path, uint64_t first
         const uint64_t cn = std::min(chunk, count - c0);
         const int b = static_cast<int>(j & 1);
         if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));  // buffer b drained
-        read_full(f.fd, pin[b], cn * col_bytes, kScnbHeader + (first + c0) * col_bytes,
-                  path, "truncated scenario payload");
+        read_parallel(f.fd, pin[b], cn * col_bytes, kScnbHeader + (first + c0) * col_bytes,
+                      path, "truncated scenario payload", readers);
         if (layout == SCENDP_MEM_DEVICE) {
           ctx->copy(out + c0 * rows, pin[b], cn * col_bytes, cudaMemcpyHostToDevice);
         } else {
