@@ -8,7 +8,10 @@
 // is element-parallel and writes the tiled layout with coalesced 128-byte
 // rows.  tnormal rejection-samples a variable number of draws per value and
 // is generated sequentially per column (one thread per scenario).
+#include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -232,6 +235,51 @@ template void launch_from_tiled<int32_t>(scendp_ctx*, const int32_t*, uint64_t, 
 template void launch_from_tiled<uint8_t>(scendp_ctx*, const uint8_t*, uint64_t, uint64_t, uint8_t*);
 template void launch_from_tiled<uint32_t>(scendp_ctx*, const uint32_t*, uint64_t, uint64_t, uint32_t*);
 
+// A pageable host scenario set (the reference's ScenarioBatch vector) into
+// the tiled layout: a driver-staged cudaMemcpy from pageable memory runs at
+// ~11 GB/s, so whole-tile chunks are copied by up to 8 host threads into two
+// page-locked buffers (alternating, event-guarded) while the previous
+// chunk's H2D copy and tiling run on the stream (~PCIe speed).
+void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, uint64_t count,
+                           uint32_t* dst) {
+  constexpr uint64_t kChunkBytes = 64ull << 20;
+  const uint64_t col_bytes = rows * 4;
+  uint64_t chunk = std::max<uint64_t>(32, (kChunkBytes / col_bytes) & ~uint64_t{31});
+  chunk = std::min(chunk, (count + 31) & ~uint64_t{31});
+  const uint64_t stage_bytes = chunk * col_bytes;
+  char* pin[2] = {static_cast<char*>(ctx->pinned_stage(0, stage_bytes)),
+                  static_cast<char*>(ctx->pinned_stage(1, stage_bytes))};
+  uint32_t* dstage = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, stage_bytes));
+  const int threads = static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+  cudaEvent_t done[2];
+  for (auto& e : done) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  const char* s = reinterpret_cast<const char*>(src);
+  for (uint64_t c0 = 0, j = 0; c0 < count; c0 += chunk, ++j) {
+    const uint64_t cn = std::min(chunk, count - c0);
+    const int b = static_cast<int>(j & 1);
+    if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));
+    const uint64_t bytes = cn * col_bytes;
+    const uint64_t per = ((bytes + threads - 1) / threads + 4095) & ~uint64_t{4095};
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads && per * t < bytes; ++t)
+      pool.emplace_back([&, t] {
+        const uint64_t lo = per * t, hi = std::min(bytes, per * (t + 1));
+        std::memcpy(pin[b] + lo, s + c0 * col_bytes + lo, hi - lo);
+      });
+    std::memcpy(pin[b], s + c0 * col_bytes, std::min(bytes, per));
+    for (auto& t : pool) t.join();
+    ctx->copy(dstage, pin[b], bytes, cudaMemcpyHostToDevice);
+    launch_to_tiled<uint32_t>(ctx, dstage, rows, cn, dst + (c0 / 32) * rows * 32);
+    CUDA_CHECK(cudaEventRecord(done[b], ctx->stream));
+    used[b] = true;
+  }
+  // the staging buffers are reused by the next call: drain before returning
+  for (int b = 0; b < 2; ++b)
+    if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));
+  for (auto& e : done) CUDA_CHECK(cudaEventDestroy(e));
+}
+
 const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
                                 bool allow_fused, void* gen_params_out, bool* fused) {
   *fused = false;
@@ -254,10 +302,15 @@ const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
     }
     case SCENDP_MEM_HOST: {
       if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
-      uint32_t* stg = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, rows * count * 4));
-      ctx->copy(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice);
       uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
-      launch_to_tiled<uint32_t>(ctx, stg, rows, count, dst);
+      if (mapped_host_alias(const_cast<uint32_t*>(sc->data)) || rows * count * 4 <= (16ull << 20)) {
+        // page-locked (DMA straight from it) or small: one copy
+        uint32_t* stg = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, rows * count * 4));
+        ctx->copy(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice);
+        launch_to_tiled<uint32_t>(ctx, stg, rows, count, dst);
+      } else {
+        upload_pageable_tiled(ctx, sc->data, rows, count, dst);
+      }
       return dst;
     }
     case SCENDP_MEM_DEVICE: {
