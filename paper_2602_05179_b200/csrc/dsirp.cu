@@ -360,7 +360,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     if (host_out) {
       if (out->totals) {
         if (zc_totals) ctx->stats.d2h_bytes += nc * m * 8;  // stored by the kernels
-        else ctx->copy(out->totals, d_totals, nc * m * 8, cudaMemcpyDeviceToHost);
+        else download(ctx, out->totals, d_totals, nc * m * 8);
       }
       if (out->evaluated)
         ctx->copy(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost);
@@ -385,10 +385,10 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
         }
       }
       if (host_out) {
-        ctx->copy(out->deliver, r_dl, nc * m * H, cudaMemcpyDeviceToHost);
-        ctx->copy(out->quantity, r_q, nc * m * H * 4, cudaMemcpyDeviceToHost);
-        ctx->copy(out->end_inventory, r_ei, nc * m * H * 4, cudaMemcpyDeviceToHost);
-        ctx->copy(out->route_option, r_ro, nc * m * H * 4, cudaMemcpyDeviceToHost);
+        download(ctx, out->deliver, r_dl, nc * m * H);
+        download(ctx, out->quantity, r_q, nc * m * H * 4);
+        download(ctx, out->end_inventory, r_ei, nc * m * H * 4);
+        download(ctx, out->route_option, r_ro, nc * m * H * 4);
       }
     }
     const bool want_agg = out->agg || out->agg_raw;

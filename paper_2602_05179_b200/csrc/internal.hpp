@@ -146,6 +146,13 @@ namespace scendp_host {
 void finalize_agg(const scendp_agg_raw* raw, uint32_t n, uint32_t k,
                   scendp_agg* out);
 
+// Device -> host copy of a large result into pageable memory: whole chunks
+// go D2H into two page-locked buffers (alternating) and are copied out by
+// host threads while the next chunk transfers.  Small or page-locked
+// destinations take one plain async copy.  Returns after the data is in
+// `dst` for the pipelined form (the caller synchronises the stream anyway).
+void download(scendp_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
 // Device alias of a page-locked, UVA-mapped host buffer (cudaMallocHost /
 // cudaHostAlloc / cudaHostRegister), or nullptr for pageable memory.  Per-
 // scenario totals bound for such a buffer are stored by the DP kernels

@@ -235,6 +235,19 @@ template void launch_from_tiled<int32_t>(scendp_ctx*, const int32_t*, uint64_t, 
 template void launch_from_tiled<uint8_t>(scendp_ctx*, const uint8_t*, uint64_t, uint64_t, uint8_t*);
 template void launch_from_tiled<uint32_t>(scendp_ctx*, const uint32_t*, uint64_t, uint64_t, uint32_t*);
 
+// memcpy of `bytes` split over up to `threads` host threads
+static void parallel_copy(char* dst, const char* src, uint64_t bytes, int threads) {
+  const uint64_t per = ((bytes + threads - 1) / threads + 4095) & ~uint64_t{4095};
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads && per * t < bytes; ++t)
+    pool.emplace_back([=] {
+      const uint64_t lo = per * t, hi = std::min(bytes, per * (t + 1));
+      std::memcpy(dst + lo, src + lo, hi - lo);
+    });
+  std::memcpy(dst, src, std::min(bytes, per));
+  for (auto& th : pool) th.join();
+}
+
 // A pageable host scenario set (the reference's ScenarioBatch vector) into
 // the tiled layout: a driver-staged cudaMemcpy from pageable memory runs at
 // ~11 GB/s, so whole-tile chunks are copied by up to 8 host threads into two
@@ -260,15 +273,7 @@ void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, 
     const int b = static_cast<int>(j & 1);
     if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));
     const uint64_t bytes = cn * col_bytes;
-    const uint64_t per = ((bytes + threads - 1) / threads + 4095) & ~uint64_t{4095};
-    std::vector<std::thread> pool;
-    for (int t = 1; t < threads && per * t < bytes; ++t)
-      pool.emplace_back([&, t] {
-        const uint64_t lo = per * t, hi = std::min(bytes, per * (t + 1));
-        std::memcpy(pin[b] + lo, s + c0 * col_bytes + lo, hi - lo);
-      });
-    std::memcpy(pin[b], s + c0 * col_bytes, std::min(bytes, per));
-    for (auto& t : pool) t.join();
+    parallel_copy(pin[b], s + c0 * col_bytes, bytes, threads);
     ctx->copy(dstage, pin[b], bytes, cudaMemcpyHostToDevice);
     launch_to_tiled<uint32_t>(ctx, dstage, rows, cn, dst + (c0 / 32) * rows * 32);
     CUDA_CHECK(cudaEventRecord(done[b], ctx->stream));
@@ -277,6 +282,36 @@ void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, 
   // the staging buffers are reused by the next call: drain before returning
   for (int b = 0; b < 2; ++b)
     if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));
+  for (auto& e : done) CUDA_CHECK(cudaEventDestroy(e));
+}
+
+
+void download(scendp_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  constexpr uint64_t kChunk = 64ull << 20;
+  if (bytes <= (16ull << 20) || mapped_host_alias(dst)) {
+    ctx->copy(dst, src, bytes, cudaMemcpyDeviceToHost);
+    return;
+  }
+  const int threads = static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+  char* pin[2] = {static_cast<char*>(ctx->pinned_stage(0, kChunk)),
+                  static_cast<char*>(ctx->pinned_stage(1, kChunk))};
+  cudaEvent_t done[2];
+  for (auto& e : done) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  char* d = static_cast<char*>(dst);
+  const char* sp = static_cast<const char*>(src);
+  const uint64_t nchunks = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](uint64_t j) {
+    const uint64_t off = j * kChunk, len = std::min(kChunk, bytes - off);
+    ctx->copy(pin[j & 1], sp + off, len, cudaMemcpyDeviceToHost);
+    CUDA_CHECK(cudaEventRecord(done[j & 1], ctx->stream));
+  };
+  issue(0);
+  for (uint64_t j = 0; j < nchunks; ++j) {
+    if (j + 1 < nchunks) issue(j + 1);  // the other buffer is free: drained below
+    CUDA_CHECK(cudaEventSynchronize(done[j & 1]));
+    const uint64_t off = j * kChunk, len = std::min(kChunk, bytes - off);
+    parallel_copy(d + off, pin[j & 1], len, threads);
+  }
   for (auto& e : done) CUDA_CHECK(cudaEventDestroy(e));
 }
 

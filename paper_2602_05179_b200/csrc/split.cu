@@ -914,17 +914,17 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
     if (out->totals && host_out) {
       if (zc_totals) ctx->stats.d2h_bytes += k * m * 8;  // stored by the kernels
-      else ctx->copy(out->totals, d_totals, k * m * 8, cudaMemcpyDeviceToHost);
+      else download(ctx, out->totals, d_totals, k * m * 8);
     }
     if (full && !out_dev_tiled) {
       // tiled -> reference layout [m][n+1]
       double* V_ref = out_dev_ref ? out->values : static_cast<double*>(ctx->scratch_get(kScrOut5, m * n1 * 8));
       launch_from_tiled<double>(ctx, d_V, n1, m, V_ref);
-      if (host_out) ctx->copy(out->values, V_ref, m * n1 * 8, cudaMemcpyDeviceToHost);
+      if (host_out) download(ctx, out->values, V_ref, m * n1 * 8);
       int32_t* C_ref = out_dev_ref ? out->cuts : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, m * n1 * 4));
       launch_from_tiled<int32_t>(ctx, d_cuts, n1, m, C_ref);
       if (host_out) {
-        ctx->copy(out->cuts, C_ref, m * n1 * 4, cudaMemcpyDeviceToHost);
+        download(ctx, out->cuts, C_ref, m * n1 * 4);
         ctx->copy(out->route_count, d_rc, m * 4, cudaMemcpyDeviceToHost);
         ctx->copy(out->feasible, d_feas, m, cudaMemcpyDeviceToHost);
       }
