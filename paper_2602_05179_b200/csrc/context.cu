@@ -412,7 +412,10 @@ scendp_status scendp_memcpy(scendp_ctx* ctx, void* dst, const void* src,
     const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
                              : kind == 1 ? cudaMemcpyDeviceToHost
                                          : cudaMemcpyDeviceToDevice;
-    ctx->copy(dst, src, bytes, k);
+    if (k == cudaMemcpyDeviceToHost && !(flags & SCENDP_ASYNC))
+      download(ctx, dst, src, bytes);  // pipelined when large and pageable
+    else
+      ctx->copy(dst, src, bytes, k);
     if (!(flags & SCENDP_ASYNC)) ctx->sync();
   });
 }

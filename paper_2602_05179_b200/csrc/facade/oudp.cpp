@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 
@@ -208,9 +209,11 @@ scendp_customer to_c(const CustomerSpec& spec, const DeliveryCostModel& del,
 void schedules(scendp_ctx* ctx, const scendp_customer& c, const std::uint32_t* data,
                std::size_t count, ScheduleResult* dst, std::uint8_t* evaluated) {
   const std::size_t H = static_cast<std::size_t>(c.horizon);
-  std::vector<double> totals(count);
-  std::vector<std::uint8_t> dl(count * H);
-  std::vector<std::int32_t> q(count * H), ei(count * H), ro(count * H);
+  // scratch filled entirely by the evaluator: default-initialized
+  std::unique_ptr<double[]> totals(new double[count]);
+  std::unique_ptr<std::uint8_t[]> dl(new std::uint8_t[count * H]);
+  std::unique_ptr<std::int32_t[]> q(new std::int32_t[count * H]), ei(new std::int32_t[count * H]),
+      ro(new std::int32_t[count * H]);
   scendp_scenarios sc{};
   sc.mem_kind = SCENDP_MEM_HOST;
   sc.data = data;
@@ -218,22 +221,24 @@ void schedules(scendp_ctx* ctx, const scendp_customer& c, const std::uint32_t* d
   sc.count = count;
   scendp_dsirp_out o{};
   o.mem_kind = SCENDP_MEM_HOST;
-  o.totals = totals.data();
+  o.totals = totals.get();
   o.evaluated = evaluated;
-  o.deliver = dl.data();
-  o.quantity = q.data();
-  o.end_inventory = ei.data();
-  o.route_option = ro.data();
+  o.deliver = dl.get();
+  o.quantity = q.get();
+  o.end_inventory = ei.get();
+  o.route_option = ro.get();
   detail::check(scendp_dsirp_eval(ctx, &c, 1, &sc, SCENDP_DSIRP_FULL, &o));
-  for (std::size_t w = 0; w < count; ++w) {
-    if (!evaluated[w]) continue;
-    ScheduleResult& r = dst[w];
-    r.total = ExtendedCost{totals[w]};
-    r.deliver.assign(dl.begin() + w * H, dl.begin() + (w + 1) * H);
-    r.quantity.assign(q.begin() + w * H, q.begin() + (w + 1) * H);
-    r.end_inventory.assign(ei.begin() + w * H, ei.begin() + (w + 1) * H);
-    r.route_option.assign(ro.begin() + w * H, ro.begin() + (w + 1) * H);
-  }
+  detail::parallel_for(count, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t w = lo; w < hi; ++w) {
+      if (!evaluated[w]) continue;
+      ScheduleResult& r = dst[w];
+      r.total = ExtendedCost{totals[w]};
+      r.deliver.assign(dl.get() + w * H, dl.get() + (w + 1) * H);
+      r.quantity.assign(q.get() + w * H, q.get() + (w + 1) * H);
+      r.end_inventory.assign(ei.get() + w * H, ei.get() + (w + 1) * H);
+      r.route_option.assign(ro.get() + w * H, ro.get() + (w + 1) * H);
+    }
+  });
 }
 
 constexpr const char* kAllInfinite = "inventory DP produced an all-infinite frontier";

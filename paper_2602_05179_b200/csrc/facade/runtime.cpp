@@ -3,6 +3,7 @@
 // proj/src/engine.cpp:7-30) and ValueFrontier::initial (minplus.cpp:8-21).
 #include "runtime.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <exception>
 #include <limits>
@@ -51,6 +52,30 @@ ValueFrontier ValueFrontier::initial(int stage, std::size_t state_count,
 }
 
 namespace detail {
+
+void parallel_for(std::size_t count, const std::function<void(std::size_t, std::size_t)>& fn,
+                  unsigned threads, std::size_t min_per_thread) {
+  if (threads == 0) threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const std::size_t parts = std::max<std::size_t>(
+      1, std::min<std::size_t>(threads, count / std::max<std::size_t>(1, min_per_thread)));
+  if (parts <= 1) {
+    fn(0, count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(parts);
+  for (std::size_t p = 0; p < parts; ++p)
+    pool.emplace_back([&, p] {
+      try {
+        fn(count * p / parts, count * (p + 1) / parts);
+      } catch (...) {
+        errs[p] = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
 
 void check(scendp_status s) {
   if (s == SCENDP_OK) return;

@@ -65,6 +65,12 @@ void sequential_aggregate(BatchResultSet<R>& out, CostOf cost_of) {
 
 ExactAggregate to_exact(const scendp_agg& a);
 
+// fn(lo, hi) over [0, count) split across up to `threads` host threads
+// (result objects of the batched evaluators are built in parallel, like the
+// reference's worker threads build theirs).
+void parallel_for(std::size_t count, const std::function<void(std::size_t, std::size_t)>& fn,
+                  unsigned threads = 0, std::size_t min_per_thread = 4096);
+
 double ms_since(std::uint64_t t0_ns);
 std::uint64_t now_ns();
 
