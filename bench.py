@@ -21,7 +21,10 @@ uniform:1:10 demands (the reference default), 10^6 scenarios per GPU
          host threads.
 
 Secondary lines (DSIRP C3/C4, SAA C5 candidate sweep, penalized and
-float-cost split) ride in the same JSON object under "secondary".
+float-cost split, full solutions, K5 min-plus, SCNB ingestion) ride in the
+same JSON object under "secondary"; at N = 1 each split/DSIRP line carries
+"cpu_reference", the reference's own evaluator (oracle/_ref) on a bounded
+sample of that workload with all host threads.
 """
 from __future__ import annotations
 
@@ -347,6 +350,15 @@ def run_ours(args, d: Dist):
         line["cpu_baseline"] = cpu_baseline()
     if not args.no_secondary:
         line["secondary"] = secondary(ctx, d, args)
+        if d.world == 1 and not args.no_cpu_baseline:
+            try:
+                for k, v in cpu_reference_secondary().items():
+                    if k in line["secondary"]:
+                        v["unit"] = line["secondary"][k]["unit"]
+                        line["secondary"][k]["cpu_reference"] = v
+            except Exception as e:  # reference library missing on this box
+                line["secondary_cpu_reference"] = f"unavailable: {e}"
+
     if d.rank == 0:
         print(json.dumps(line), flush=True)
     scen.free()
@@ -508,6 +520,63 @@ def secondary(ctx, d: Dist, args):
         sc.free()
         t3.free()
     return out
+
+
+def cpu_reference_secondary():
+    """The reference's own evaluators (oracle/_ref) on bounded samples of the
+    secondary workloads (SURVEY 8d "CPU reference timing"), all host threads;
+    rate = units of the sample / wall time of one call after a warm-up."""
+    from oracle import UNIFORM, Customer as RefCust, Reference
+    R = Reference()
+    threads = os.cpu_count() or 1
+    out = {}
+
+    def rate(fn, units):
+        fn()  # warm-up (saa.cpp:364-368)
+        t0 = time.perf_counter()
+        fn()
+        return units / (time.perf_counter() - t0)
+
+    n = N_C2
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    ms = 20_000
+    dem = R.generate(UNIFORM, 1, 10, 77, n, 1, ms)
+    rng = np.random.default_rng(1)
+    c = rng.random((n + 2, n + 2)) * 20.0
+    c = np.triu(c, 1)
+    c = c + c.T
+    out["split_c2_float_costs"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, c, tour, dem,
+                                                               threads), ms),
+                                   f"batched_split_costs, float-cost twin, {ms} scenarios")
+    icost = R.make_random_instance(n, 1)
+    out["split_c2_full_solution"] = (rate(lambda: R.expected_split(n, Q_C2, 1, 0.0, icost, tour,
+                                                                    dem, threads), ms),
+                                     f"batched_expected_split, {ms} scenarios")
+    mp = 2_000
+    out["split_c2_penalized"] = (rate(lambda: R.split_costs(n, Q_C2, 0, 10.0, icost, tour,
+                                                             dem[:mp], threads), mp),
+                                 f"batched_split_costs penalized beta=10, {mp} scenarios")
+    # C5: K calls of batched_split_costs (saa.cpp:127-131), timed on 4 tours
+    n5, m5, k5 = 50, 100_000, 4
+    cost5 = R.make_random_instance(n5, 5)
+    dem5 = R.generate(UNIFORM, 1, 10, 55, n5, 1, m5)
+    rng5 = np.random.default_rng(5)
+    tours5 = [(rng5.permutation(n5) + 1).astype(np.int32) for _ in range(k5)]
+    out["saa_c5_candidates"] = (rate(lambda: [R.split_costs(n5, Q_C2, 0, 10.0, cost5, t, dem5,
+                                                            threads) for t in tours5], k5 * m5),
+                                f"{k5} tours x batched_split_costs (n=50, beta=10, 10^5 scenarios)")
+    # DSIRP: batched_expected_cost per customer (the reference has no
+    # multi-customer call), 4 customers x 10^5 scenarios
+    H, m3, nc = 6, 100_000, 4
+    cust = RefCust(U=100, I0=50, H=H, h=1.0, rho=2.0,
+                   fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                   unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1)))
+    d3 = R.generate(UNIFORM, 0, 33, 7, 1, H, m3)
+    r3 = rate(lambda: [R.expected_cost(cust, d3, threads) for _ in range(nc)], nc * m3)
+    for name in ("dsirp_c3", "dsirp_c4"):
+        out[name] = (r3, f"{nc} customers x batched_expected_cost (U=100, H=6, R=3, 10^5)")
+    return {k: {"value": v, "cores": threads, "kind": "reference", "sample": smp}
+            for k, (v, smp) in out.items()}
 
 
 def main():
