@@ -79,7 +79,7 @@ def summarize(rep, name, rnd):
     return rd + wr
 
 
-def launches(csv_path, rnd):
+def launches(csv_path, rnd, suffix=""):
     rows = list(csv.reader(open(csv_path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
@@ -99,7 +99,7 @@ def launches(csv_path, rnd):
              f"{'kernel':70s} {'launches':>8s} {'total':>12s} {'share':>7s}"]
     for k, t in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"{k[:70]:70s} {cnt[k]:8d} {t:12.0f} {100 * t / allt:6.1f}%")
-    with open(os.path.join(HERE, f"r{rnd:02d}_launches.txt"), "w") as f:
+    with open(os.path.join(HERE, f"r{rnd:02d}_launches{suffix}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
 
 
@@ -107,7 +107,8 @@ def main():
     rnd = int(sys.argv[1])
     args = sys.argv[2:]
     if args and args[0] == "--launches":
-        launches(args[1], rnd)
+        # optional third argument: file suffix (e.g. _headline)
+        launches(args[1], rnd, args[2] if len(args) > 2 else "")
         return
     tj = os.path.join(HERE, "ncu_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
