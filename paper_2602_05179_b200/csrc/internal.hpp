@@ -67,6 +67,9 @@ struct NcclApi;
 struct scendp_ctx {
   int device = 0;
   int sm_count = 0;
+  // split overflow bitmap: scratch base it lives at, bytes known all-zero
+  void* ovf_base = nullptr;
+  uint64_t ovf_clean = 0;
   cudaStream_t stream = nullptr;
   scendp_opts opts{};
   void* scratch[scendp_host::kScrCount] = {};

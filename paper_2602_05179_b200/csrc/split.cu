@@ -95,6 +95,7 @@ struct SplitArgs {
   unsigned int* ovf_count;
   unsigned long long* ovf_items;
   uint32_t ovf_cap;
+  uint32_t* ovf_bits;   // [k * m_wave / 32]: items beyond the list (all-zero at rest)
 };
 
 __device__ __forceinline__ uint32_t demand_at(const SplitArgs& a, int src, uint64_t stream,
@@ -133,9 +134,16 @@ __host__ __device__ constexpr size_t tour_smem_bytes(int n) {
   return static_cast<size_t>(n + 1) * (3 * sizeof(double) + sizeof(uint32_t));
 }
 
+// A (tour, scenario) item for the generic kernel: into the list while it has
+// room, else flagged in the bitmap (correct for any overflow count).
 __device__ __forceinline__ void push_overflow(const SplitArgs& a, uint32_t k, uint64_t wl) {
   const unsigned int slot = atomicAdd(a.ovf_count, 1u);
-  if (slot < a.ovf_cap) a.ovf_items[slot] = (static_cast<unsigned long long>(k) << 40) | wl;
+  if (slot < a.ovf_cap) {
+    a.ovf_items[slot] = (static_cast<unsigned long long>(k) << 40) | wl;
+  } else {
+    const uint64_t item = static_cast<uint64_t>(k) * a.m_wave + wl;
+    atomicOr(a.ovf_bits + (item >> 5), 1u << (item & 31));
+  }
 }
 
 #include "split_linear.cuh"
@@ -253,13 +261,7 @@ template <bool FULL, int SRC>
 __global__ void __launch_bounds__(64)
 split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
                      char* scratch, uint64_t scratch_stride) {
-  __shared__ unsigned long long s_agg[kAggSlots];
-  agg_cta_init(s_agg);
-  __syncthreads();
   const int n = a.n;
-  const uint64_t n_items = list_mode ? min(static_cast<uint64_t>(*a.ovf_count),
-                                           static_cast<uint64_t>(a.ovf_cap))
-                                     : n_range_items;
   const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   char* my = scratch + gtid * scratch_stride;
@@ -267,162 +269,171 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
   int64_t* ld = reinterpret_cast<int64_t*>(f + n + 1);    // [n+1]
   int32_t* dq = reinterpret_cast<int32_t*>(ld + n + 1);   // [n+1]
   int32_t* rcs = dq + n + 1;                              // [n+1]
-  // round-robin over items; every lane runs the same number of rounds so the
-  // warp-level aggregate stays convergent
-  const uint64_t rounds = (n_items + nthreads - 1) / nthreads;
-  for (uint64_t rd = 0; rd < rounds; ++rd) {
-    const uint64_t item = rd * nthreads + gtid;
-    const bool active = item < n_items;
+  // one (tour, scenario) item: the reference's algorithm, totals / full
+  // outputs, and its aggregate straight to global (items of one warp may
+  // belong to different tours; integer atomics keep the sum exact)
+  auto run_item = [&](uint32_t k, uint64_t wl) {
     double v = 0.0;
-    uint32_t k = 0;
-    if (active) {
-      uint64_t wl;
-      if (list_mode) {
-        const unsigned long long it = a.ovf_items[item];
-        k = static_cast<uint32_t>(it >> 40);
-        wl = it & ((1ULL << 40) - 1);
-      } else {
-        k = static_cast<uint32_t>(item / a.m_wave);
-        wl = item % a.m_wave;
-      }
-      const uint64_t w = a.w_base + wl;
-      const uint64_t toff = static_cast<uint64_t>(k) * (n + 1);
-      const double* dist = a.dist + toff;
-      const double* ret = a.ret + toff;
-      const double* c0 = a.c0 + toff;
-      const uint32_t* col = a.col + toff;
-      const uint32_t* tile_base = nullptr;
-      uint64_t stream = 0;
-      if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
-      else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
-      double* Vout = nullptr;
-      int32_t* Cout = nullptr;
-      if (FULL) {
-        const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
-        Vout = a.V + base;
-        Cout = a.cuts + base;
-        Vout[0] = 0.0;
-        Cout[0] = 0;
-      }
-      ld[0] = 0;
-      for (int i = 1; i <= n; ++i)
-        ld[i] = ld[i - 1] + static_cast<int64_t>(demand_at(a, SRC, stream, tile_base, col[i]));
-      f[0] = __dsub_rn(__dadd_rn(0.0, c0[0]), dist[1]);
-      rcs[0] = 0;
-      if (a.linear) {
-        int head = 0, tail = 0;
-        dq[tail++] = 0;
-        for (int i = 1; i <= n; ++i) {
-          while (head < tail && ld[i] - ld[dq[head]] > a.Q) ++head;
-          int32_t cut = -1;
-          if (head >= tail) {
-            v = kInfD;
-            rcs[i] = 0;
-          } else {
-            const int p = dq[head];
-            v = __dadd_rn(__dadd_rn(f[p], dist[i]), ret[i]);
-            cut = v < kInfD ? p : -1;
-            rcs[i] = v < kInfD ? rcs[p] + 1 : 0;
-          }
-          if (FULL) {
-            Vout[static_cast<uint64_t>(i) * kTile] = v;
-            Cout[static_cast<uint64_t>(i) * kTile] = cut;
-          }
-          if (i < n) {
-            const double fi = __dsub_rn(__dadd_rn(v, c0[i]), dist[i + 1]);
-            while (tail > head && f[dq[tail - 1]] > fi) --tail;
-            dq[tail++] = i;
-            f[i] = fi;
-          }
+    const uint64_t w = a.w_base + wl;
+    const uint64_t toff = static_cast<uint64_t>(k) * (n + 1);
+    const double* dist = a.dist + toff;
+    const double* ret = a.ret + toff;
+    const double* c0 = a.c0 + toff;
+    const uint32_t* col = a.col + toff;
+    const uint32_t* tile_base = nullptr;
+    uint64_t stream = 0;
+    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+    double* Vout = nullptr;
+    int32_t* Cout = nullptr;
+    if (FULL) {
+      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+      Vout = a.V + base;
+      Cout = a.cuts + base;
+      Vout[0] = 0.0;
+      Cout[0] = 0;
+    }
+    ld[0] = 0;
+    for (int i = 1; i <= n; ++i)
+      ld[i] = ld[i - 1] + static_cast<int64_t>(demand_at(a, SRC, stream, tile_base, col[i]));
+    f[0] = __dsub_rn(__dadd_rn(0.0, c0[0]), dist[1]);
+    rcs[0] = 0;
+    if (a.linear) {
+      int head = 0, tail = 0;
+      dq[tail++] = 0;
+      for (int i = 1; i <= n; ++i) {
+        while (head < tail && ld[i] - ld[dq[head]] > a.Q) ++head;
+        int32_t cut = -1;
+        if (head >= tail) {
+          v = kInfD;
+          rcs[i] = 0;
+        } else {
+          const int p = dq[head];
+          v = __dadd_rn(__dadd_rn(f[p], dist[i]), ret[i]);
+          cut = v < kInfD ? p : -1;
+          rcs[i] = v < kInfD ? rcs[p] + 1 : 0;
         }
-      } else if (!a.hard && a.pen_lmax > 0 && ld[n] <= static_cast<int64_t>(a.pen_lmax)) {
-        // penalized, exact integral data: the O(n) decomposition of
-        // split_penal.cuh without its ring limits -- window A = {L_i - L_p
-        // <= Q} (deque of f, earliest minimum) and prefix B before it (running
-        // minimum of g(p) = f(p) - beta L_p); B wins ties (earlier indices).
-        // Every value is an integer below 2^31, so each fp64 op is exact and
-        // equals the reference's ((f + dist_i) + ret_i) + beta * excess.
-        int head = 0, tail = 0, lo = 0, bidx = -1;
-        double bmin = kInfD;
-        dq[tail++] = 0;
-        const double beta = a.beta;
-        for (int i = 1; i <= n; ++i) {
-          while (lo < i && ld[i] - ld[lo] > a.Q) {
-            const double g = f[lo] - beta * static_cast<double>(ld[lo]);
-            if (g < bmin) {
-              bmin = g;
-              bidx = lo;
-            }
-            ++lo;
-          }
-          while (head < tail && dq[head] < lo) ++head;
-          const double candA = head < tail ? (f[dq[head]] + dist[i]) + ret[i] : kInfD;
-          const double candB = bidx >= 0 ? ((bmin + dist[i]) + ret[i]) +
-                                               beta * static_cast<double>(ld[i] - a.Q)
-                                         : kInfD;
-          const bool useB = candB <= candA;
-          v = useB ? candB : candA;
-          const int32_t bestp = useB ? bidx : dq[head];
-          rcs[i] = rcs[bestp] + 1;
-          if (FULL) {
-            Vout[static_cast<uint64_t>(i) * kTile] = v;
-            Cout[static_cast<uint64_t>(i) * kTile] = bestp;
-          }
-          if (i < n) {
-            const double fi = (v + c0[i]) - dist[i + 1];
-            while (tail > head && f[dq[tail - 1]] > fi) --tail;
-            dq[tail++] = i;
-            f[i] = fi;
-          }
+        if (FULL) {
+          Vout[static_cast<uint64_t>(i) * kTile] = v;
+          Cout[static_cast<uint64_t>(i) * kTile] = cut;
         }
-      } else {
-        for (int i = 1; i <= n; ++i) {
-          double best = kInfD;
-          int32_t bestp = -1;
-          for (int p = 0; p < i; ++p) {
-            const double fp = f[p];
-            if (!(fp < kInfD)) continue;
-            const int64_t excess = ld[i] - ld[p] - a.Q;
-            double cand = __dadd_rn(__dadd_rn(fp, dist[i]), ret[i]);
-            if (excess > 0) {
-              if (a.hard) continue;
-              cand = __dadd_rn(cand, __dmul_rn(a.beta, static_cast<double>(excess)));
-            }
-            if (cand < best) {
-              best = cand;
-              bestp = p;
-            }
-          }
-          v = best;
-          rcs[i] = bestp >= 0 ? rcs[bestp] + 1 : 0;
-          if (FULL) {
-            Vout[static_cast<uint64_t>(i) * kTile] = best;
-            Cout[static_cast<uint64_t>(i) * kTile] = bestp;
-          }
-          if (i < n) f[i] = __dsub_rn(__dadd_rn(best, c0[i]), dist[i + 1]);
+        if (i < n) {
+          const double fi = __dsub_rn(__dadd_rn(v, c0[i]), dist[i + 1]);
+          while (tail > head && f[dq[tail - 1]] > fi) --tail;
+          dq[tail++] = i;
+          f[i] = fi;
         }
       }
-      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
-      if (FULL) {
-        const bool fin = v < kInfD;
-        a.route_count[w] = fin ? rcs[n] : 0;
-        a.feasible[w] = fin ? 1 : 0;
+    } else if (!a.hard && a.pen_lmax > 0 && ld[n] <= static_cast<int64_t>(a.pen_lmax)) {
+      // penalized, exact integral data: the O(n) decomposition of
+      // split_penal.cuh without its ring limits -- window A = {L_i - L_p
+      // <= Q} (deque of f, earliest minimum) and prefix B before it (running
+      // minimum of g(p) = f(p) - beta L_p); B wins ties (earlier indices).
+      // Every value is an integer below 2^31, so each fp64 op is exact and
+      // equals the reference's ((f + dist_i) + ret_i) + beta * excess.
+      int head = 0, tail = 0, lo = 0, bidx = -1;
+      double bmin = kInfD;
+      dq[tail++] = 0;
+      const double beta = a.beta;
+      for (int i = 1; i <= n; ++i) {
+        while (lo < i && ld[i] - ld[lo] > a.Q) {
+          const double g = f[lo] - beta * static_cast<double>(ld[lo]);
+          if (g < bmin) {
+            bmin = g;
+            bidx = lo;
+          }
+          ++lo;
+        }
+        while (head < tail && dq[head] < lo) ++head;
+        const double candA = head < tail ? (f[dq[head]] + dist[i]) + ret[i] : kInfD;
+        const double candB = bidx >= 0 ? ((bmin + dist[i]) + ret[i]) +
+                                             beta * static_cast<double>(ld[i] - a.Q)
+                                       : kInfD;
+        const bool useB = candB <= candA;
+        v = useB ? candB : candA;
+        const int32_t bestp = useB ? bidx : dq[head];
+        rcs[i] = rcs[bestp] + 1;
+        if (FULL) {
+          Vout[static_cast<uint64_t>(i) * kTile] = v;
+          Cout[static_cast<uint64_t>(i) * kTile] = bestp;
+        }
+        if (i < n) {
+          const double fi = (v + c0[i]) - dist[i + 1];
+          while (tail > head && f[dq[tail - 1]] > fi) --tail;
+          dq[tail++] = i;
+          f[i] = fi;
+        }
+      }
+    } else {
+      for (int i = 1; i <= n; ++i) {
+        double best = kInfD;
+        int32_t bestp = -1;
+        for (int p = 0; p < i; ++p) {
+          const double fp = f[p];
+          if (!(fp < kInfD)) continue;
+          const int64_t excess = ld[i] - ld[p] - a.Q;
+          double cand = __dadd_rn(__dadd_rn(fp, dist[i]), ret[i]);
+          if (excess > 0) {
+            if (a.hard) continue;
+            cand = __dadd_rn(cand, __dmul_rn(a.beta, static_cast<double>(excess)));
+          }
+          if (cand < best) {
+            best = cand;
+            bestp = p;
+          }
+        }
+        v = best;
+        rcs[i] = bestp >= 0 ? rcs[bestp] + 1 : 0;
+        if (FULL) {
+          Vout[static_cast<uint64_t>(i) * kTile] = best;
+          Cout[static_cast<uint64_t>(i) * kTile] = bestp;
+        }
+        if (i < n) f[i] = __dsub_rn(__dadd_rn(best, c0[i]), dist[i + 1]);
       }
     }
-    // per-item aggregate straight to global (items of one warp may belong to
-    // different tours; integer atomics keep the sum exact)
+    if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
+    if (FULL) {
+      const bool fin = v < kInfD;
+      a.route_count[w] = fin ? rcs[n] : 0;
+      a.feasible[w] = fin ? 1 : 0;
+    }
     const AggPieces pc = agg_pieces(v, true);
-    if (active) {
-      unsigned long long* g = a.agg + static_cast<uint64_t>(k) * kAggWords;
-      if (pc.kind == 0) {
-        atomicAdd(g + pc.li, static_cast<unsigned long long>(pc.p0));
-        atomicAdd(g + pc.li + 1, static_cast<unsigned long long>(pc.p1));
-        if (pc.p2) atomicAdd(g + pc.li + 2, static_cast<unsigned long long>(pc.p2));
-        atomicAdd(g + 12, 1ULL);
-      } else if (pc.kind == 1) {
-        atomicAdd(g + 13, 1ULL);
-      } else if (pc.kind == 3) {
-        atomicAdd(g + 15, 1ULL);
+    unsigned long long* g = a.agg + static_cast<uint64_t>(k) * kAggWords;
+    if (pc.kind == 0) {
+      atomicAdd(g + pc.li, static_cast<unsigned long long>(pc.p0));
+      atomicAdd(g + pc.li + 1, static_cast<unsigned long long>(pc.p1));
+      if (pc.p2) atomicAdd(g + pc.li + 2, static_cast<unsigned long long>(pc.p2));
+      atomicAdd(g + 12, 1ULL);
+    } else if (pc.kind == 1) {
+      atomicAdd(g + 13, 1ULL);
+    } else if (pc.kind == 3) {
+      atomicAdd(g + 15, 1ULL);
+    }
+  };
+  if (!list_mode) {
+    for (uint64_t item = gtid; item < n_range_items; item += nthreads)
+      run_item(static_cast<uint32_t>(item / a.m_wave), item % a.m_wave);
+    return;
+  }
+  const uint64_t cnt = *a.ovf_count;
+  const uint64_t n_list = min(cnt, static_cast<uint64_t>(a.ovf_cap));
+  for (uint64_t item = gtid; item < n_list; item += nthreads) {
+    const unsigned long long it = a.ovf_items[item];
+    run_item(static_cast<uint32_t>(it >> 40), it & ((1ULL << 40) - 1));
+  }
+  if (cnt > a.ovf_cap) {
+    // the list was full: the remaining items are flagged in the bitmap
+    // (bit = k * m_wave + wl); each word is cleared once processed, so the
+    // bitmap is all-zero again for the next wave / call
+    const uint64_t words = (static_cast<uint64_t>(a.k) * a.m_wave + 31) / 32;
+    for (uint64_t wd = gtid; wd < words; wd += nthreads) {
+      uint32_t bits = a.ovf_bits[wd];
+      if (!bits) continue;
+      a.ovf_bits[wd] = 0u;
+      while (bits) {
+        const uint64_t item = wd * 32 + (__ffs(bits) - 1);
+        bits &= bits - 1;
+        run_item(static_cast<uint32_t>(item / a.m_wave), item % a.m_wave);
       }
     }
   }
@@ -823,18 +834,34 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       }
     }
 
-    // overflow list + generic-path scratch
-    const uint32_t ovf_cap = 1u << 16;
-    char* ovf = static_cast<char*>(ctx->scratch_get(kScrOverflow, 16 + ovf_cap * 8ull));
-    auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + 16);
+    // waves (BackendConfig::batch_size / memory_budget analogue)
+    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
+    if (wave == 0) wave = 32;
+
+    // overflow items for the generic kernel: a list sized for ~1% of the
+    // wave's items (the rates seen at the BASELINE shapes are <= 0.3%), and a
+    // bitmap of every item for the rest -- kept all-zero at rest (the generic
+    // kernel clears what it processes; the bytes after it hold the list, so
+    // only the part known clean is skipped when it grows)
+    const uint64_t wave_items = static_cast<uint64_t>(k) * std::min(wave, std::max<uint64_t>(m, 1));
+    const uint32_t ovf_cap = static_cast<uint32_t>(
+        std::min<uint64_t>(std::max<uint64_t>(wave_items / 128, 1u << 16), 1u << 26));
+    const uint64_t bits_bytes = (((wave_items + 31) / 32) * 4 + 15) & ~uint64_t{15};
+    char* ovf = static_cast<char*>(ctx->scratch_get(kScrOverflow, bits_bytes + ovf_cap * 8ull));
+    if (ovf != ctx->ovf_base) {
+      ctx->ovf_base = ovf;
+      ctx->ovf_clean = 0;
+    }
+    if (ctx->ovf_clean < bits_bytes)
+      CUDA_CHECK(cudaMemsetAsync(ovf + ctx->ovf_clean, 0, bits_bytes - ctx->ovf_clean, ctx->stream));
+    ctx->ovf_clean = bits_bytes;
+    auto* d_ovf_bits = reinterpret_cast<uint32_t*>(ovf);
+    auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + bits_bytes);
     const int generic_blocks = ctx->sm_count * kGenericBlocksPerSm;
     const uint64_t generic_stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
     char* gen_scratch = static_cast<char*>(
         ctx->scratch_get(kScrFallback, generic_stride * generic_blocks * kGenericThreads));
 
-    // waves (BackendConfig::batch_size / memory_budget analogue)
-    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
-    if (wave == 0) wave = 32;
     for (uint64_t w0 = 0; w0 < m || (m == 0 && w0 == 0); w0 += wave) {
       if (m == 0) break;
       const uint64_t mw = std::min(wave, m - w0);
@@ -893,6 +920,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ovf_count = d_ovf_count;
       a.ovf_items = d_ovf_items;
       a.ovf_cap = ovf_cap;
+      a.ovf_bits = d_ovf_bits;
       if (w0 > 0) CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
       const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
       if (full) {

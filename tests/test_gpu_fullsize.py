@@ -1,0 +1,112 @@
+"""GPU parity at the BASELINE shapes, against the real
+reference (oracle/_ref) on the same box.
+
+* C2 (split n=200, 10^6 scenarios, uniform:1:10): the reference's own
+  generate_scenarios + batched_split_costs over all 10^6 columns; every total
+  bit-exact, for the materialized (tiled) and the in-kernel-generated paths;
+  the aggregate equals the exact mean of the totals.
+* C3 (DSIRP 50 customers x 10^5, H=6): every customer's totals against the
+  reference's per-customer batched_expected_cost on a sample of customers
+  (first, last, and a mixed fp64 one), all 10^5 scenarios each.
+* C4 (200 customers x 10^6): prefix stability -- the first 20,000 scenarios
+  of sampled customers equal the reference's.
+* C5 (1000 tours x 10^5, n=50, penalized beta=10): sampled tours' totals
+  bit-exact and the first-minimum argmin consistent with the per-tour means.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import TAG_SCENARIO, UNIFORM
+from oracle import Customer as RefCustomer
+from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance
+from paper_2602_05179_b200 import _capi as A
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+
+
+def test_c2_full_size_bit_exact(ctx, reference):
+    n, m, Q = 200, 1_000_000, 100
+    seed = reference.derive_stream(1, TAG_SCENARIO, 0)
+    costs = reference.make_random_instance(n, 1)
+    inst = RoutingInstance(n, Q, True, 0.0, costs)
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    dem = reference.generate(UNIFORM, 1, 10, seed, n, 1, m)  # the reference's own batch
+    ref_tot, (ref_mean, fc, ic) = reference.split_costs(n, Q, 1, 0.0, costs, tour, dem, THREADS)
+    dist = Distribution("uniform", 1, 10, seed=seed)
+    got_g = ctx.split_eval(inst, tour, dist, count=m)
+    np.testing.assert_array_equal(got_g["totals"][0], ref_tot)
+    got_h = ctx.split_eval(inst, tour, dem)
+    np.testing.assert_array_equal(got_h["totals"][0], ref_tot)
+    for got in (got_g, got_h):
+        a = got["agg"][0]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        assert a["mean"] == ref_mean  # integral costs: every partial sum exact
+    # the device-generated set is the reference's batch, byte for byte
+    scen = ctx.gen_scenarios(dist, n, m, tiled=False)
+    np.testing.assert_array_equal(scen.download(np.uint32, n * m).reshape(m, n), dem)
+    scen.free()
+
+
+def _c3_customers(nc, H):
+    """C3 pins (U=100, I0=50, h=1, rho=2, R=3, fixed 40+5r, unit 0.5+0.25r),
+    perturbed per customer by dyadic offsets; customer 1 gets non-dyadic
+    costs, which moves the launch onto the fp64 kernel path for it."""
+    ours, refs = [], []
+    for c in range(nc):
+        fixed = np.tile(40 + 5 * np.arange(3.0), (H, 1)) + (c % 7)
+        unit = np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1)) + 0.25 * (c % 3)
+        h = 1.0
+        if c == 1:
+            fixed = fixed + 0.1
+            h = 0.7
+        kw = dict(U=100, I0=50, H=H, h=h, rho=2.0, fixed=fixed, unit=unit)
+        ours.append(Customer(**kw))
+        refs.append(RefCustomer(**kw))
+    return ours, refs
+
+
+@pytest.mark.parametrize("nc,m,sample,prefix", [(50, 100_000, (0, 1, 27, 49), None),
+                                                (200, 1_000_000, (0, 1, 199), 20_000)])
+def test_dsirp_c3_c4_bit_exact(ctx, reference, nc, m, sample, prefix):
+    H = 6
+    ours, refs = _c3_customers(nc, H)
+    dist = Distribution("uniform", 0, 33, seed=7)
+    scen = ctx.gen_scenarios(dist, nc * H, m)
+    got = ctx.dsirp_eval(ours, (scen, A.MEM_DEVICE_TILED), count=m)
+    scen.free()
+    assert got["evaluated"].all()
+    mref = prefix or m
+    dem = reference.generate(UNIFORM, 0, 33, 7, nc, H, mref)  # rows c*H + t
+    for c in sample:
+        cols = dem[:, c * H:(c + 1) * H]
+        tot, _, _, _, _, ev, (mean, fc, ic) = reference.expected_cost(refs[c], cols, THREADS)
+        assert ev.all()
+        np.testing.assert_array_equal(got["totals"][c][:mref], tot)
+        if prefix is None:
+            a = got["agg"][c]
+            assert a["finite_count"] == fc and a["infeasible_count"] == ic
+            assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
+
+
+def test_c5_saa_sweep_bit_exact(ctx, reference):
+    n, m, K, Q, beta = 50, 100_000, 1000, 100, 10.0
+    costs = reference.make_random_instance(n, 5)
+    inst = RoutingInstance(n, Q, False, beta, costs)
+    rng = np.random.default_rng(5)
+    tours = np.stack([rng.permutation(n) + 1 for _ in range(K)]).astype(np.int32)
+    seed = reference.derive_stream(5, TAG_SCENARIO, 0)
+    dist = Distribution("uniform", 1, 10, seed=seed)
+    scen = ctx.gen_scenarios(dist, n, m)
+    got = ctx.split_eval(inst, tours, (scen, A.MEM_DEVICE_TILED), count=m)
+    scen.free()
+    means = np.array([a["mean"] for a in got["agg"]])
+    best = got["best"]
+    assert best == int(np.argmin(means))  # first minimum, saa.cpp:134
+    dem = reference.generate(UNIFORM, 1, 10, seed, n, 1, m)
+    for t in sorted({0, 1, 500, K - 1, best}):
+        tot, (mean, fc, ic) = reference.split_costs(n, Q, 0, beta, costs, tours[t], dem, THREADS)
+        np.testing.assert_array_equal(got["totals"][t], tot)
+        assert got["agg"][t]["mean"] == mean

@@ -281,3 +281,37 @@ def test_c1_poisson_generated_in_kernel(ctx, oracle, reference, mode):
                                                     costs, tour, dem)
         np.testing.assert_array_equal(got["totals"][0], tot)
         assert got["agg"][0]["mean"] == mean
+
+
+@pytest.mark.parametrize("hard", [False, True])
+def test_overflow_beyond_list_capacity(ctx, oracle, reference, hard):
+    """Every scenario leaves the fast kernels (demands 1..2 with Q = 100: the
+    penalized capacity window outgrows the 32-position ring; hard: the
+    window-start test on a 50-customer tour with tiny demands never evicts
+    and the deque outgrows its ring on increasing f) -- 2 x 60,000 items, far
+    beyond the 65,536-entry overflow list, so most take the bitmap path."""
+    n, m, Q = 50, 60_000, 100
+    costs = oracle.make_random_instance(n, 9)
+    if hard:
+        # f(p) increasing along the tour: every predecessor stays in the deque
+        c = np.zeros((n + 2, n + 2))
+        for i in range(n + 2):
+            for j in range(n + 2):
+                c[i, j] = abs(i - j) if i != j else 0.0
+        costs = c
+    inst = RoutingInstance(n, Q, hard, 0.0 if hard else 10.0, costs)
+    tours = np.stack([np.arange(1, n + 1), np.random.default_rng(2).permutation(n) + 1])
+    tours = tours.astype(np.int32)
+    dem = oracle.generate(UNIFORM, 1, 2, 99, n, m)
+    got = ctx.split_eval(inst, tours, dem)
+    for t in range(2):
+        tot, (mean, fc, ic) = reference.split_costs(n, Q, int(hard), inst.penalty_beta, costs, tours[t],
+                                                    dem, 16)
+        np.testing.assert_array_equal(got["totals"][t], tot)
+        a = got["agg"][t]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        check_mean(a, mean)
+    # a second call reuses the (cleared) bitmap
+    again = ctx.split_eval(inst, tours, dem)
+    np.testing.assert_array_equal(again["totals"], got["totals"])
+    assert again["agg"] == got["agg"]
