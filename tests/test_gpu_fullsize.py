@@ -12,6 +12,9 @@ reference (oracle/_ref) on the same box.
   of sampled customers equal the reference's.
 * C5 (1000 tours x 10^5, n=50, penalized beta=10): sampled tours' totals
   bit-exact and the first-minimum argmin consistent with the per-tour means.
+* C2 float-cost twin over 10^6 (one launch and 300,000-scenario waves), C2
+  full solutions and penalized totals on 200,000 scenarios, C3 full
+  schedules, and K5 at the bench shape against forward_sweep.
 """
 import os
 
@@ -110,3 +113,98 @@ def test_c5_saa_sweep_bit_exact(ctx, reference):
         tot, (mean, fc, ic) = reference.split_costs(n, Q, 0, beta, costs, tours[t], dem, THREADS)
         np.testing.assert_array_equal(got["totals"][t], tot)
         assert got["agg"][t]["mean"] == mean
+
+
+def _float_costs(n, seed):
+    rng = np.random.default_rng(seed)
+    c = rng.random((n + 2, n + 2)) * 20.0
+    c = np.triu(c, 1)
+    return c + c.T
+
+
+def test_c2_float_costs_and_waves_bit_exact(ctx, reference):
+    """C2 with non-integral costs (K1 fp64: the reference's association
+    verbatim) over all 10^6 scenarios, in one launch and in waves of 300,000
+    (BackendConfig::batch_size; not a multiple of the 32-scenario tile)."""
+    n, m, Q = 200, 1_000_000, 100
+    costs = _float_costs(n, 200)
+    inst = RoutingInstance(n, Q, True, 0.0, costs)
+    tour = (np.random.default_rng(4).permutation(n) + 1).astype(np.int32)
+    seed = reference.derive_stream(3, TAG_SCENARIO, 0)
+    dem = reference.generate(UNIFORM, 1, 10, seed, n, 1, m)
+    ref_tot, (ref_mean, fc, ic) = reference.split_costs(n, Q, 1, 0.0, costs, tour, dem, THREADS)
+    dist = Distribution("uniform", 1, 10, seed=seed)
+    got = ctx.split_eval(inst, tour, dist, count=m)
+    np.testing.assert_array_equal(got["totals"][0], ref_tot)
+    a = got["agg"][0]
+    assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+    assert abs(a["mean"] - ref_mean) <= 1e-9 * abs(ref_mean)
+    ctx.set_max_batch(300_000)
+    try:
+        waves = ctx.split_eval(inst, tour, dist, count=m)
+    finally:
+        ctx.set_max_batch(0)
+    np.testing.assert_array_equal(waves["totals"], got["totals"])
+    assert waves["agg"] == got["agg"]
+
+
+def test_c2_full_solutions_and_penalized_bit_exact(ctx, reference):
+    """Full solutions (V, cuts, route counts) on 200,000 C2 scenarios, and the
+    penalized (beta = 10) C2 totals -- K2-int -- on the same set."""
+    n, m, Q = 200, 200_000, 100
+    costs = reference.make_random_instance(n, 1)
+    tour = np.arange(1, n + 1, dtype=np.int32)
+    seed = reference.derive_stream(1, TAG_SCENARIO, 0)
+    dem = reference.generate(UNIFORM, 1, 10, seed, n, 1, m)
+    inst = RoutingInstance(n, Q, True, 0.0, costs)
+    got = ctx.split_eval(inst, tour, dem, full=True)
+    tot, V, cuts, rc, feas, _ = reference.expected_split(n, Q, 1, 0.0, costs, tour, dem, THREADS)
+    np.testing.assert_array_equal(got["totals"][0], tot)
+    np.testing.assert_array_equal(got["V"], V)
+    np.testing.assert_array_equal(got["cuts"], cuts)
+    np.testing.assert_array_equal(got["route_count"], rc)
+    np.testing.assert_array_equal(got["feasible"], feas)
+    pinst = RoutingInstance(n, Q, False, 10.0, costs)
+    gp = ctx.split_eval(pinst, tour, dem)
+    ptot, (pmean, _, _) = reference.split_costs(n, Q, 0, 10.0, costs, tour, dem, THREADS)
+    np.testing.assert_array_equal(gp["totals"][0], ptot)
+    assert gp["agg"][0]["mean"] == pmean
+
+
+def test_c3_full_schedules_bit_exact(ctx, reference):
+    """DSIRP schedules (deliver, quantity, end inventory, route option) for
+    every scenario of two C3 customers, one of them on the fp64 path."""
+    H, nc, m = 6, 50, 100_000
+    ours, refs = _c3_customers(nc, H)
+    dist = Distribution("uniform", 0, 33, seed=7)
+    scen = ctx.gen_scenarios(dist, nc * H, m)
+    got = ctx.dsirp_eval(ours, (scen, A.MEM_DEVICE_TILED), count=m, full=True)
+    scen.free()
+    dem = reference.generate(UNIFORM, 0, 33, 7, nc, H, m)
+    for c in (0, 1):
+        tot, dl, q, ei, ro, ev, _ = reference.expected_cost(refs[c], dem[:, c * H:(c + 1) * H],
+                                                            THREADS)
+        np.testing.assert_array_equal(got["totals"][c], tot)
+        np.testing.assert_array_equal(got["deliver"][c], dl)
+        np.testing.assert_array_equal(got["quantity"][c], q)
+        np.testing.assert_array_equal(got["end_inventory"][c], ei)
+        np.testing.assert_array_equal(got["route_option"][c], ro)
+
+
+def test_k5_bench_shape_matches_forward_sweep(ctx, reference):
+    """K5 at the bench shape (6 stages x 3 options x 101 x 101, 10^5
+    frontiers): every final frontier entry against the reference's
+    forward_sweep on 200 sampled frontiers (the frontiers are independent)."""
+    rng = np.random.default_rng(11)
+    stages = []
+    for _ in range(6):
+        st = np.floor(rng.random((3, 101, 101)) * 100.0)
+        st[rng.random(st.shape) < 0.5] = np.inf
+        stages.append(st)
+    B = 100_000
+    init = np.full((B, 101), np.inf)
+    init[np.arange(B), rng.integers(0, 101, B)] = 0.0
+    out = ctx.minplus_sweep(stages, init)
+    for b in rng.choice(B, 200, replace=False):
+        ref = reference.forward_sweep(stages, init[b])
+        np.testing.assert_array_equal(out[b], ref[-101:])
