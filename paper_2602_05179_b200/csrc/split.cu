@@ -857,8 +857,13 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     ctx->ovf_clean = bits_bytes;
     auto* d_ovf_bits = reinterpret_cast<uint32_t*>(ovf);
     auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + bits_bytes);
-    const int generic_blocks = ctx->sm_count * kGenericBlocksPerSm;
+    // generic path: latency-bound (dependent global-scratch accesses), so as
+    // many threads as ~64 MB of scratch allows, 2..8 CTAs per SM
     const uint64_t generic_stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
+    const uint64_t per_sm = static_cast<uint64_t>(ctx->sm_count) * kGenericThreads * generic_stride;
+    const int generic_blocks =
+        ctx->sm_count * static_cast<int>(std::clamp<uint64_t>((64ull << 20) / per_sm,
+                                                              kGenericBlocksPerSm, 8));
     char* gen_scratch = static_cast<char*>(
         ctx->scratch_get(kScrFallback, generic_stride * generic_blocks * kGenericThreads));
 
