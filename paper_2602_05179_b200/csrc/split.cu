@@ -252,6 +252,14 @@ split_quadratic_kernel(SplitArgs a) {
   agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
 }
 
+// Element i of a per-thread array interleaved across the grid.
+template <typename T>
+struct Strided {
+  T* p;
+  uint64_t s;
+  __device__ __forceinline__ T& operator[](int64_t i) const { return p[i * static_cast<int64_t>(s)]; }
+};
+
 // ---------------------------------------------------------------------------
 // Generic path: one thread per item with O(n) global-memory scratch and
 // 64-bit loads -- the reference algorithm verbatim for any n, Q or demand
@@ -264,11 +272,15 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
   const int n = a.n;
   const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  char* my = scratch + gtid * scratch_stride;
-  double* f = reinterpret_cast<double*>(my);             // [n+1]
-  int64_t* ld = reinterpret_cast<int64_t*>(f + n + 1);    // [n+1]
-  int32_t* dq = reinterpret_cast<int32_t*>(ld + n + 1);   // [n+1]
-  int32_t* rcs = dq + n + 1;                              // [n+1]
+  // per-thread arrays [n+1], interleaved across the grid ([i][thread]): the
+  // lanes of a warp step through positions together, so the writes at i
+  // (and most reads) coalesce instead of touching 32 lines
+  (void)scratch_stride;
+  const uint64_t plane = static_cast<uint64_t>(n + 1) * nthreads;
+  const Strided<double> f{reinterpret_cast<double*>(scratch) + gtid, nthreads};
+  const Strided<int64_t> ld{reinterpret_cast<int64_t*>(scratch) + plane + gtid, nthreads};
+  const Strided<int32_t> dq{reinterpret_cast<int32_t*>(scratch + plane * 16) + gtid, nthreads};
+  const Strided<int32_t> rcs{reinterpret_cast<int32_t*>(scratch + plane * 20) + gtid, nthreads};
   // one (tour, scenario) item: the reference's algorithm, totals / full
   // outputs, and its aggregate straight to global (items of one warp may
   // belong to different tours; integer atomics keep the sum exact)
