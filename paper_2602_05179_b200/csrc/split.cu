@@ -24,6 +24,7 @@
 // penalized cand = ((f + dist[i]) + ret) + beta*(double)excess.  Ties keep
 // the earliest predecessor (strict <), as the reference.
 #include <algorithm>
+#include <thread>
 #include <map>
 #include <mutex>
 #include <chrono>
@@ -533,6 +534,16 @@ void validate_tour(const int32_t* tour, int n) {
 // The integer-path check: all tour costs integral and every partial sum
 // < 2^29, so each fp64 op of the reference is exact and integer adds
 // reproduce it bit for bit.
+// x (finite, >= 0) is an integer.  Branch-free and inline: std::floor is a
+// libm call on the baseline x86-64 target, and it dominated the table build
+// for large K (3 calls per position).  Below 2^52, adding and removing 2^52
+// rounds x to an integer (round-to-nearest), unchanged iff x was one; every
+// double from 2^52 up is an integer.
+inline bool is_whole(double x) {
+  constexpr double k52 = 4503599627370496.0;
+  return (x >= k52) | (((x + k52) - k52) == x);  // IEEE: not folded without -ffast-math
+}
+
 void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
                   const TableLayout& L, char* blob, TourTables& t) {
   const int n = inst->n, side = n + 2, npad = L.npad;
@@ -546,69 +557,106 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
   uint32_t* ccol_all = reinterpret_cast<uint32_t*>(blob + L.o_ccol);
   double* f0d = D(L.o_f0d);
   int32_t* f0i = reinterpret_cast<int32_t*>(blob + L.o_f0i);
+  // tours are independent: large K (the SAA candidate sweeps) is split over
+  // host threads, each with its own flags, combined after the join
+  const unsigned parts = static_cast<unsigned>(std::min<uint64_t>(
+      std::max(1u, std::min(8u, std::thread::hardware_concurrency())),
+      std::max<uint64_t>(1, static_cast<uint64_t>(k) * n1 / 16384)));
+  auto for_tours = [&](auto&& body) {
+    if (parts <= 1) {
+      body(0u, k, 0u);
+      return;
+    }
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < parts; ++t)
+      pool.emplace_back([&, t] { body(static_cast<uint32_t>(uint64_t{k} * t / parts),
+                                      static_cast<uint32_t>(uint64_t{k} * (t + 1) / parts), t); });
+    body(0u, static_cast<uint32_t>(k / parts), 0u);
+    for (auto& th : pool) th.join();
+  };
+  // an all-integer matrix makes every prefix integral (a rounded sum of
+  // integers is an integer): one scan of (n+2)^2 entries instead of 3 tests
+  // per tour position
+  bool matrix_whole = true;
+  for (size_t e = 0; e < static_cast<size_t>(side) * side; ++e) matrix_whole &= is_whole(c[e]);
+  std::vector<char> p_intv(parts, 1), p_ident(parts, 1);
+  std::vector<double> p_bound(parts, 0.0);
+  for_tours([&](uint32_t q0, uint32_t q1, unsigned part) {
+    bool intv = true, ident = true;
+    double costbound = 0.0;
+    for (uint32_t q = q0; q < q1; ++q) {
+      const int32_t* sq = tours + static_cast<size_t>(q) * n;
+      double* dist = dist_all + q * n1;
+      double* ret = ret_all + q * n1;
+      double* c0 = c0_all + q * n1;
+      uint32_t* col = col_all + q * n1;
+      uint32_t* ccol = ccol_all + static_cast<size_t>(q) * npad;
+      dist[0] = 0.0;
+      dist[1] = 0.0;
+      for (int i = 2; i <= n; ++i) dist[i] = dist[i - 1] + c[sq[i - 2] * side + sq[i - 1]];
+      ret[0] = 0.0;
+      col[0] = 0u;
+      for (int i = 1; i <= n; ++i) {
+        ret[i] = c[sq[i - 1] * side + (n + 1)];
+        col[i] = static_cast<uint32_t>(sq[i - 1] - 1);
+        ccol[i - 1] = col[i];
+        ident &= sq[i - 1] == i;
+      }
+      for (int i = n; i < npad; ++i) ccol[i] = 0u;
+      for (int i = 0; i < n; ++i) c0[i] = c[0 * side + sq[i]];
+      c0[n] = 0.0;
+      double bound = dist[n], cmax = 0.0;
+      bool integral = true;
+      for (int i = 0; i <= n; ++i) {
+        if (!matrix_whole) integral &= is_whole(dist[i]) & is_whole(ret[i]) & is_whole(c0[i]);
+        bound += ret[i] + c0[i];
+        cmax = std::max(cmax, c0[i]);
+      }
+      bound += cmax;
+      intv &= integral && bound < static_cast<double>(1 << 29);
+      costbound = std::max(costbound, bound);
+      f0d[q] = (0.0 + c0[0]) - dist[1];
+    }
+    p_intv[part] = intv;
+    p_ident[part] = ident;
+    p_bound[part] = costbound;
+  });
   bool intv = true, ident = true;
   double costbound = 0.0;
-  for (uint32_t q = 0; q < k; ++q) {
-    const int32_t* sq = tours + static_cast<size_t>(q) * n;
-    double* dist = dist_all + q * n1;
-    double* ret = ret_all + q * n1;
-    double* c0 = c0_all + q * n1;
-    uint32_t* col = col_all + q * n1;
-    uint32_t* ccol = ccol_all + static_cast<size_t>(q) * npad;
-    dist[0] = 0.0;
-    dist[1] = 0.0;
-    for (int i = 2; i <= n; ++i) dist[i] = dist[i - 1] + c[sq[i - 2] * side + sq[i - 1]];
-    ret[0] = 0.0;
-    col[0] = 0u;
-    for (int i = 1; i <= n; ++i) {
-      ret[i] = c[sq[i - 1] * side + (n + 1)];
-      col[i] = static_cast<uint32_t>(sq[i - 1] - 1);
-      ccol[i - 1] = col[i];
-      ident &= sq[i - 1] == i;
-    }
-    for (int i = n; i < npad; ++i) ccol[i] = 0u;
-    for (int i = 0; i < n; ++i) c0[i] = c[0 * side + sq[i]];
-    c0[n] = 0.0;
-    double bound = dist[n], cmax = 0.0;
-    bool integral = true;
-    for (int i = 0; i <= n; ++i) {
-      integral &= std::floor(dist[i]) == dist[i] && std::floor(ret[i]) == ret[i] &&
-                  std::floor(c0[i]) == c0[i];
-      bound += ret[i] + c0[i];
-      cmax = std::max(cmax, c0[i]);
-    }
-    bound += cmax;
-    intv &= integral && bound < static_cast<double>(1 << 29);
-    costbound = std::max(costbound, bound);
-    f0d[q] = (0.0 + c0[0]) - dist[1];
+  for (unsigned t = 0; t < parts; ++t) {
+    intv &= p_intv[t] != 0;
+    ident &= p_ident[t] != 0;
+    costbound = std::max(costbound, p_bound[t]);
   }
   // per-position K1/K2 tables: integer A/B when every tour admits it, else
   // the fp64 quadruple
-  for (uint32_t q = 0; q < k; ++q) {
-    const double* dist = dist_all + q * n1;
-    const double* ret = ret_all + q * n1;
-    const double* c0 = c0_all + q * n1;
-    if (intv) {
-      f0i[q] = static_cast<int32_t>(f0d[q]);
-      int32_t* it = reinterpret_cast<int32_t*>(blob + L.o_tab) + static_cast<size_t>(q) * 2 * npad;
-      for (int i = 1; i <= n; ++i) {
-        it[0 * npad + (i - 1)] = static_cast<int32_t>(dist[i] + ret[i]);
-        it[1 * npad + (i - 1)] = i < n ? static_cast<int32_t>(c0[i] - dist[i + 1]) : 0;
+  for_tours([&](uint32_t q0, uint32_t q1, unsigned) {
+    for (uint32_t q = q0; q < q1; ++q) {
+      const double* dist = dist_all + q * n1;
+      const double* ret = ret_all + q * n1;
+      const double* c0 = c0_all + q * n1;
+      if (intv) {
+        f0i[q] = static_cast<int32_t>(f0d[q]);
+        int32_t* it = reinterpret_cast<int32_t*>(blob + L.o_tab) + static_cast<size_t>(q) * 2 * npad;
+        for (int i = 1; i <= n; ++i) {
+          it[0 * npad + (i - 1)] = static_cast<int32_t>(dist[i] + ret[i]);
+          it[1 * npad + (i - 1)] = i < n ? static_cast<int32_t>(c0[i] - dist[i + 1]) : 0;
+        }
+        for (int i = n; i < npad; ++i) it[i] = it[npad + i] = 0;
+      } else {
+        f0i[q] = 0;
+        double* dt = D(L.o_tab) + static_cast<size_t>(q) * 4 * npad;
+        for (int i = 1; i <= n; ++i) {
+          const size_t sidx = static_cast<size_t>(i - 1);
+          dt[0 * npad + sidx] = dist[i];
+          dt[1 * npad + sidx] = ret[i];
+          dt[2 * npad + sidx] = c0[i];
+          dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
+        }
+        for (int i = n; i < npad; ++i) dt[i] = dt[npad + i] = dt[2 * npad + i] = dt[3 * npad + i] = 0.0;
       }
-      for (int i = n; i < npad; ++i) it[i] = it[npad + i] = 0;
-    } else {
-      f0i[q] = 0;
-      double* dt = D(L.o_tab) + static_cast<size_t>(q) * 4 * npad;
-      for (int i = 1; i <= n; ++i) {
-        const size_t sidx = static_cast<size_t>(i - 1);
-        dt[0 * npad + sidx] = dist[i];
-        dt[1 * npad + sidx] = ret[i];
-        dt[2 * npad + sidx] = c0[i];
-        dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
-      }
-      for (int i = n; i < npad; ++i) dt[i] = dt[npad + i] = dt[2 * npad + i] = dt[3 * npad + i] = 0.0;
     }
-  }
+  });
   t.intv = intv;
   t.ident = ident;
   t.costbound = costbound;
@@ -716,7 +764,8 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
 }  // namespace
 
 // SCENDP_HOST_TRACE=1: per-call host-side phase times (microseconds) on
-// stderr -- validation, tables + upload, launches, completion.
+// stderr -- validation, staging buffer, table build, upload, launches,
+// completion.
 struct HostTrace {
   bool on;
   std::chrono::steady_clock::time_point t0, last;
@@ -776,7 +825,9 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const TableLayout L(n, k);
     const size_t n1 = static_cast<size_t>(n) + 1;
     char* stage = static_cast<char*>(ctx->pinned_tables(L.bytes));
+    trace.mark("stage");
     build_tables(inst, tours, k, L, stage, tt);
+    trace.mark("build");
     const size_t used = tt.intv ? L.o_tab + static_cast<size_t>(k) * 2 * L.npad * 4 : L.bytes;
     char* dtab = static_cast<char*>(ctx->scratch_get(kScrTours, L.bytes));
     constexpr size_t kCacheBytes = 256 << 10;
