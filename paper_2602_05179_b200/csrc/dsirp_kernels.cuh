@@ -15,6 +15,7 @@ using namespace scendp_dev;
 
 constexpr double kInfD = __builtin_huge_val();
 constexpr int kDsirpThreads = 128;
+constexpr int kDsirpIntUnits = 4;  // 128-scenario blocks per CTA (exact-integer kernel)
 
 struct CustDev {
   int32_t U, I0, H, R;
@@ -311,152 +312,159 @@ dsirp_int_kernel(DsirpArgs a) {
   const CustDev cd = a.cust[c];
   agg_cta_init(s_agg);
   __syncthreads();
-  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  const bool active = wl < a.m_wave;
-  const uint64_t w = a.w_base + wl;
   const int U = cd.U, H = kExact ? HMAX : cd.H;
   const int32_t* gkey = a.ipool + cd.off_gkey;     // [H][U+1]
   const int32_t* htab = a.ipool + cd.off_htab_i;   // [U+1]
   const bool htabular = cd.hold_tab != 0;
   const int32_t hI = cd.h_i, rhI = cd.rh_i;
   const double inv_scale = __longlong_as_double(static_cast<long long>(1023 - cd.shift) << 52);
+  // kDsirpIntUnits consecutive 128-scenario blocks per CTA: one customer
+  // record, aggregate init and flush per CTA instead of per block (the unit
+  // itself is short; the prologue/epilogue barriers were a visible stall)
+  for (int rep = 0; rep < kDsirpIntUnits; ++rep) {
+    const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(kDsirpIntUnits) + rep) * blockDim.x +
+                        threadIdx.x;
+    const bool active = wl < a.m_wave;
+    const uint64_t w = a.w_base + wl;
 
-  double total = kInfD;
-  bool ok = false;
-  if (active) {
-    int dem[HMAX];
-    dsirp_load_demands<HMAX>(a, c, wl, H, dem);
-    bool in_range = true;
-#pragma unroll
-    for (int t = 0; t < HMAX; ++t)
-      if (t < H) in_range &= static_cast<unsigned>(dem[t]) <= static_cast<unsigned>(cd.dlim);
-    if (!in_range) {
-      total = dsirp_unit_fp64<HMAX, FULL>(a, cd, a.pool + cd.off_fixed, a.pool + cd.off_unit, c,
-                                          w, dem, ok);
-    } else {
-      auto hold = [&](int j, int s) -> int32_t {
-        if (!STDHOLD && htabular) return __ldg(htab + j);
-        return hI * j + rhI * s;
-      };
-      int st[K];
-      int32_t vl[K];
-      uint32_t dm[K];
-      int opt[HMAX];
-#pragma unroll
-      for (int e = 0; e < K; ++e) {
-        st[e] = 0;
-        vl[e] = 0;
-        dm[e] = 0u;
-      }
-#pragma unroll
-      for (int t = 0; t < HMAX; ++t) opt[t] = 0;
-      st[0] = cd.I0;
-      Mask live = 1u;  // K = HMAX+1 slots can exceed 32
-#pragma unroll kUnr
-      for (int t = 0; t < HMAX; ++t) {
-        if (t < H) {
-          const int d = dem[t];
-          const int j1 = max(0, U - d), s1 = max(0, d - U);
-          const int32_t hold1 = hold(j1, s1);
-          const int32_t* grow = gkey + t * (U + 1) + U;  // grow[-i] = key for q = U - i
-          // (1) delivery candidate: packed (cand << 8 | r), first minimum
-          int32_t bk = INT32_MAX;
-          int be = -1;
-#pragma unroll kUnr
-          for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
-            if (((live >> e) & 1u) && st[e] < U) {
-              const int32_t key = __ldg(grow - st[e]) + ((vl[e] + hold1) << 8);
-              if (key < bk) {
-                bk = key;
-                be = e;
+    double total = kInfD;
+    bool ok = false;
+    if (active) {
+      int dem[HMAX];
+      dsirp_load_demands<HMAX>(a, c, wl, H, dem);
+      bool in_range = true;
+  #pragma unroll
+      for (int t = 0; t < HMAX; ++t)
+        if (t < H) in_range &= static_cast<unsigned>(dem[t]) <= static_cast<unsigned>(cd.dlim);
+      if (!in_range) {
+        total = dsirp_unit_fp64<HMAX, FULL>(a, cd, a.pool + cd.off_fixed, a.pool + cd.off_unit, c,
+                                            w, dem, ok);
+      } else {
+        auto hold = [&](int j, int s) -> int32_t {
+          if (!STDHOLD && htabular) return __ldg(htab + j);
+          return hI * j + rhI * s;
+        };
+        int st[K];
+        int32_t vl[K];
+        uint32_t dm[K];
+        int opt[HMAX];
+  #pragma unroll
+        for (int e = 0; e < K; ++e) {
+          st[e] = 0;
+          vl[e] = 0;
+          dm[e] = 0u;
+        }
+  #pragma unroll
+        for (int t = 0; t < HMAX; ++t) opt[t] = 0;
+        st[0] = cd.I0;
+        Mask live = 1u;  // K = HMAX+1 slots can exceed 32
+  #pragma unroll kUnr
+        for (int t = 0; t < HMAX; ++t) {
+          if (t < H) {
+            const int d = dem[t];
+            const int j1 = max(0, U - d), s1 = max(0, d - U);
+            const int32_t hold1 = hold(j1, s1);
+            const int32_t* grow = gkey + t * (U + 1) + U;  // grow[-i] = key for q = U - i
+            // (1) delivery candidate: packed (cand << 8 | r), first minimum
+            int32_t bk = INT32_MAX;
+            int be = -1;
+  #pragma unroll kUnr
+            for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+              if (((live >> e) & 1u) && st[e] < U) {
+                const int32_t key = __ldg(grow - st[e]) + ((vl[e] + hold1) << 8);
+                if (key < bk) {
+                  bk = key;
+                  be = e;
+                }
               }
             }
-          }
-          // (2) no delivery
-          int32_t b0 = INT32_MAX;
-          int k0 = -1, tgt = -1;
-#pragma unroll kUnr
-          for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
-            if ((live >> e) & 1u) {
-              const int i = st[e];
-              const int j = max(0, i - d), s = max(0, d - i);
-              const int32_t nv = vl[e] + hold(j, s);
-              if (i == U && j1 > 0) tgt = e;
-              st[e] = j;
-              vl[e] = nv;
-              if (i <= d) {
-                if (nv < b0) {
-                  if (k0 >= 0) live &= ~(Mask{1} << k0);
-                  b0 = nv;
-                  k0 = e;
-                } else {
-                  live &= ~(Mask{1} << e);
+            // (2) no delivery
+            int32_t b0 = INT32_MAX;
+            int k0 = -1, tgt = -1;
+  #pragma unroll kUnr
+            for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+              if ((live >> e) & 1u) {
+                const int i = st[e];
+                const int j = max(0, i - d), s = max(0, d - i);
+                const int32_t nv = vl[e] + hold(j, s);
+                if (i == U && j1 > 0) tgt = e;
+                st[e] = j;
+                vl[e] = nv;
+                if (i <= d) {
+                  if (nv < b0) {
+                    if (k0 >= 0) live &= ~(Mask{1} << k0);
+                    b0 = nv;
+                    k0 = e;
+                  } else {
+                    live &= ~(Mask{1} << e);
+                  }
+                }
+              }
+            }
+            if (j1 == 0) tgt = k0;
+            // (3) merge (strict <)
+            if (be >= 0) {
+              const int32_t bv = bk >> 8;
+              const int br = bk & 0xff;
+              const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
+              if (tgt >= 0) {
+                int32_t tv = INT32_MAX;
+  #pragma unroll kUnr
+                for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e)
+                  if (e == tgt && ((live >> e) & 1u)) tv = vl[e];
+                if (bv < tv) {
+  #pragma unroll kUnr
+                  for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
+                    const bool hit = e == tgt;  // per-slot selects (see above)
+                    vl[e] = hit ? bv : vl[e];
+                    if (FULL) dm[e] = hit ? nm : dm[e];
+                  }
+                  live |= Mask{1} << tgt;
+                  if (FULL) opt[t] = br;
+                }
+              } else {
+                st[t + 1] = j1;
+                vl[t + 1] = bv;
+                live |= Mask{1} << (t + 1);
+                if (FULL) {
+                  dm[t + 1] = nm;
+                  opt[t] = br;
                 }
               }
             }
           }
-          if (j1 == 0) tgt = k0;
-          // (3) merge (strict <)
-          if (be >= 0) {
-            const int32_t bv = bk >> 8;
-            const int br = bk & 0xff;
-            const uint32_t nm = FULL ? (sel_u<K>(dm, be) | (1u << t)) : 0u;
-            if (tgt >= 0) {
-              int32_t tv = INT32_MAX;
-#pragma unroll kUnr
-              for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e)
-                if (e == tgt && ((live >> e) & 1u)) tv = vl[e];
-              if (bv < tv) {
-#pragma unroll kUnr
-                for (int e = 0; e < (kSlotsExact ? K : t + 1); ++e) if (e <= t) {
-                  const bool hit = e == tgt;  // per-slot selects (see above)
-                  vl[e] = hit ? bv : vl[e];
-                  if (FULL) dm[e] = hit ? nm : dm[e];
-                }
-                live |= Mask{1} << tgt;
-                if (FULL) opt[t] = br;
-              }
-            } else {
-              st[t + 1] = j1;
-              vl[t + 1] = bv;
-              live |= Mask{1} << (t + 1);
-              if (FULL) {
-                dm[t + 1] = nm;
-                opt[t] = br;
-              }
-            }
+        }
+        int32_t tv = INT32_MAX;
+        int ts = -1;
+  #pragma unroll
+        for (int e = 0; e < K; ++e) {
+          if (((live >> e) & 1u) && vl[e] < tv) {
+            tv = vl[e];
+            ts = e;
           }
         }
+        ok = ts >= 0;  // always: the no-delivery chain keeps a state alive
+        total = ok ? static_cast<double>(tv) * inv_scale : kInfD;
+        if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
+        if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+        if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
       }
-      int32_t tv = INT32_MAX;
-      int ts = -1;
-#pragma unroll
-      for (int e = 0; e < K; ++e) {
-        if (((live >> e) & 1u) && vl[e] < tv) {
-          tv = vl[e];
-          ts = e;
-        }
-      }
-      ok = ts >= 0;  // always: the no-delivery chain keeps a state alive
-      total = ok ? static_cast<double>(tv) * inv_scale : kInfD;
-      if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-      if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
-      if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
     }
+    __syncwarp();
+    agg_warp_add(s_agg, agg_pieces(total, ok), active);
   }
-  __syncwarp();
-  agg_warp_add(s_agg, agg_pieces(total, ok), active);
   __syncthreads();
   agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
 }
 
 // Launch one HMAX instantiation (fp64 or exact-integer kernel).
 template <typename Kern>
-void launch_kernel(scendp_ctx* ctx, Kern kernel, const DsirpArgs& a, size_t smem) {
+void launch_kernel(scendp_ctx* ctx, Kern kernel, const DsirpArgs& a, size_t smem, int units = 1) {
   scendp_host::cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem < 16 ? 16 : smem)),
                           "cudaFuncSetAttribute");
-  dim3 grid(static_cast<unsigned>((a.m_wave + kDsirpThreads - 1) / kDsirpThreads), a.nc);
+  const uint64_t per_cta = static_cast<uint64_t>(kDsirpThreads) * units;
+  dim3 grid(static_cast<unsigned>((a.m_wave + per_cta - 1) / per_cta), a.nc);
   const int tok = ctx->timing_begin(0);
   kernel<<<grid, kDsirpThreads, smem, ctx->stream>>>(a);
   scendp_host::cuda_check(cudaGetLastError(), "dsirp kernel launch");
@@ -474,11 +482,11 @@ template <int HMAX>
 void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
   if (int_path) {
     if (a.all_std_hold) {
-      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true, true>, a, 0);
-      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false, true>, a, 0);
+      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true, true>, a, 0, kDsirpIntUnits);
+      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false, true>, a, 0, kDsirpIntUnits);
     } else {
-      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0);
-      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false>, a, 0);
+      if (full) launch_kernel(ctx, dsirp_int_kernel<HMAX, true>, a, 0, kDsirpIntUnits);
+      else launch_kernel(ctx, dsirp_int_kernel<HMAX, false>, a, 0, kDsirpIntUnits);
     }
   } else {
     if (full) launch_kernel(ctx, dsirp_kernel<HMAX, true>, a, smem);
