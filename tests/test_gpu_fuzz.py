@@ -1,0 +1,135 @@
+"""Seeded randomized parity sweep against the real reference (oracle/_ref):
+many small configurations that together visit every kernel form and
+hand-off -- K1 (int32 / fp64), K2-int, the quadratic and generic kernels,
+K3 (exact-integer / fp64, tabular models, horizons 1..32) -- with ragged
+scenario counts, several tours, waves, and host / generated / tiled sources.
+Every per-scenario result must be bit-identical to the reference's."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import UNIFORM
+from oracle import Customer as RefCustomer
+from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance
+from paper_2602_05179_b200 import _capi as A
+
+pytestmark = pytest.mark.gpu
+# SCENDP_FUZZ_SEEDS=N widens the sweep (the default keeps the suite short)
+N_SEEDS = int(os.environ.get("SCENDP_FUZZ_SEEDS", "40"))
+
+
+def _split_case(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([1, 2, 3, 5, 17, 50, 64, 129, 300]))
+    Q = int(rng.integers(1, 200))
+    hard = bool(rng.random() < 0.6)
+    beta = float(rng.choice([0.0, 0.5, 1.0, 10.0, 37.25]))
+    kind = rng.choice(["int", "float", "bigint"])
+    if kind == "float":
+        c = rng.random((n + 2, n + 2)) * 20.0
+    elif kind == "int":
+        c = rng.integers(1, 21, size=(n + 2, n + 2)).astype(np.float64)
+    else:
+        c = rng.integers(1, 3_000_000, size=(n + 2, n + 2)).astype(np.float64)
+    c = np.triu(c, 1)
+    c = c + c.T
+    hi = int(rng.choice([max(1, Q // 8), max(1, Q // 3), Q, Q + Q // 5 + 1]))
+    lo = int(rng.integers(0, max(1, hi // 2) + 1))
+    m = int(rng.integers(1, 3000))
+    k = int(rng.choice([1, 1, 3]))
+    tours = np.stack([rng.permutation(n) + 1 for _ in range(k)]).astype(np.int32)
+    if rng.random() < 0.3:
+        tours[0] = np.arange(1, n + 1)
+    full = bool(rng.random() < 0.5)
+    src = rng.choice(["host", "generated", "tiled"])
+    wave = int(rng.choice([0, 0, 33, 1000]))
+    dseed = int(rng.integers(1, 1 << 40))
+    return dict(n=n, Q=Q, hard=hard, beta=beta, c=c, lo=lo, hi=hi, m=m, tours=tours,
+                full=full, src=src, wave=wave, dseed=dseed)
+
+
+@pytest.mark.parametrize("seed", range(N_SEEDS))
+def test_split_fuzz(ctx, oracle, reference, seed):
+    p = _split_case(seed)
+    n, m = p["n"], p["m"]
+    inst = RoutingInstance(n, p["Q"], p["hard"], p["beta"], p["c"])
+    dem = oracle.generate(UNIFORM, p["lo"], p["hi"], p["dseed"], n, m)
+    if p["src"] == "host":
+        scen, keep = dem, None
+    else:
+        dist = Distribution("uniform", p["lo"], p["hi"], seed=p["dseed"])
+        if p["src"] == "generated":
+            scen, keep = dist, None
+        else:
+            keep = ctx.gen_scenarios(dist, n, m)
+            scen = (keep, A.MEM_DEVICE_TILED)
+    ctx.set_max_batch(p["wave"])
+    try:
+        got = ctx.split_eval(inst, p["tours"], scen, count=m, full=p["full"] and len(p["tours"]) == 1)
+    finally:
+        ctx.set_max_batch(0)
+        if keep is not None:
+            keep.free()
+    for t, tour in enumerate(p["tours"]):
+        if p["full"] and len(p["tours"]) == 1:
+            tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+                n, p["Q"], int(p["hard"]), p["beta"], p["c"], tour, dem, 8)
+            np.testing.assert_array_equal(got["V"], V)
+            np.testing.assert_array_equal(got["cuts"], cuts)
+            np.testing.assert_array_equal(got["route_count"], rc)
+            np.testing.assert_array_equal(got["feasible"], feas)
+        else:
+            tot, (mean, fc, ic) = reference.split_costs(n, p["Q"], int(p["hard"]), p["beta"],
+                                                        p["c"], tour, dem, 8)
+        np.testing.assert_array_equal(got["totals"][t], tot)
+        a = got["agg"][t]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        if fc:
+            assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
+
+
+def _dsirp_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    U = int(rng.choice([1, 2, 7, 40, 100, 300]))
+    H = int(rng.choice([1, 2, 3, 6, 8, 9, 13, 20, 32]))
+    R = int(rng.integers(1, 5))
+    I0 = int(rng.integers(0, U + 1))
+    dyadic = bool(rng.random() < 0.5)
+    q = (lambda x: np.round(x * 4) / 4) if dyadic else (lambda x: x)
+    fixed = q(rng.random((H, R)) * 50)
+    unit = q(rng.random((H, R)) * 3)
+    h = float(q(np.array(rng.random() * 2))) if rng.random() < 0.8 else 0.0
+    rho = float(rng.choice([1.5, 2.0, 3.25]))
+    kw = dict(U=U, I0=I0, H=H, h=h, rho=rho, fixed=fixed, unit=unit)
+    if rng.random() < 0.2:
+        table = q(rng.random((H, U + 1)) * 60)
+        table[:, 0] = 0.0  # F_t(0) = 0 (oudp.cpp validation)
+        kw = dict(U=U, I0=I0, H=H, h=h, rho=rho, R=1, delivery_table=table)
+    if rng.random() < 0.2:
+        kw["holding_table"] = q(rng.random(U + 1) * 5)
+    hi = int(rng.choice([max(1, U // 3), U, 2 * U + 1]))
+    m = int(rng.integers(1, 2500))
+    return kw, hi, m, int(rng.integers(1, 1 << 40)), bool(rng.random() < 0.5)
+
+
+@pytest.mark.parametrize("seed", range(N_SEEDS * 3 // 4))
+def test_dsirp_fuzz(ctx, oracle, reference, seed):
+    kw, hi, m, dseed, full = _dsirp_case(seed)
+    H = kw["H"]
+    ours, ref = Customer(**kw), RefCustomer(**kw)
+    dem = oracle.generate(UNIFORM, 0, hi, dseed, H, m)
+    got = ctx.dsirp_eval([ours, ours], np.concatenate([dem, dem], axis=1), full=full)
+    tot, dl, qt, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(ref, dem, 8)
+    for c in range(2):
+        np.testing.assert_array_equal(got["evaluated"][c], ev)
+        np.testing.assert_array_equal(got["totals"][c], tot)
+        if full:
+            np.testing.assert_array_equal(got["deliver"][c], dl)
+            np.testing.assert_array_equal(got["quantity"][c], qt)
+            np.testing.assert_array_equal(got["end_inventory"][c], ei)
+            np.testing.assert_array_equal(got["route_option"][c], ro)
+        a = got["agg"][c]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        if fc:
+            assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
