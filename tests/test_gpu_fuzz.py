@@ -1,6 +1,7 @@
 """Seeded randomized parity sweep against the real reference (oracle/_ref):
 many small configurations that together visit every kernel form and
-hand-off -- K1 (int32 / fp64), K2-int, the quadratic and generic kernels,
+hand-off -- K1 (int32 / fp64, tiled or with uniform / Poisson generation
+fused), K2-int, the quadratic and generic kernels,
 K3 (exact-integer / fp64, tabular models, horizons 1..32) -- with ragged
 scenario counts, several tours, waves, and host / generated / tiled sources.
 Every per-scenario result must be bit-identical to the reference's."""
@@ -9,9 +10,9 @@ import os
 import numpy as np
 import pytest
 
-from oracle import UNIFORM
+from oracle import POISSON, UNIFORM
 from oracle import Customer as RefCustomer
-from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance
+from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance, poisson_hi
 from paper_2602_05179_b200 import _capi as A
 
 pytestmark = pytest.mark.gpu
@@ -45,8 +46,9 @@ def _split_case(seed):
     src = rng.choice(["host", "generated", "tiled"])
     wave = int(rng.choice([0, 0, 33, 1000]))
     dseed = int(rng.integers(1, 1 << 40))
+    lam = float(rng.random() * 20 + 0.5) if rng.random() < 0.3 else 0.0  # poisson
     return dict(n=n, Q=Q, hard=hard, beta=beta, c=c, lo=lo, hi=hi, m=m, tours=tours,
-                full=full, src=src, wave=wave, dseed=dseed)
+                full=full, src=src, wave=wave, dseed=dseed, lam=lam)
 
 
 @pytest.mark.parametrize("seed", range(N_SEEDS))
@@ -54,16 +56,20 @@ def test_split_fuzz(ctx, oracle, reference, seed):
     p = _split_case(seed)
     n, m = p["n"], p["m"]
     inst = RoutingInstance(n, p["Q"], p["hard"], p["beta"], p["c"])
-    dem = oracle.generate(UNIFORM, p["lo"], p["hi"], p["dseed"], n, m)
+    if p["lam"]:
+        hi = poisson_hi(p["lam"])
+        dem = oracle.generate(POISSON, 0, hi, p["dseed"], n, m, mean=p["lam"])
+        dist = Distribution("poisson", 0, hi, mean=p["lam"], seed=p["dseed"])
+    else:
+        dem = oracle.generate(UNIFORM, p["lo"], p["hi"], p["dseed"], n, m)
+        dist = Distribution("uniform", p["lo"], p["hi"], seed=p["dseed"])
     if p["src"] == "host":
         scen, keep = dem, None
+    elif p["src"] == "generated":
+        scen, keep = dist, None
     else:
-        dist = Distribution("uniform", p["lo"], p["hi"], seed=p["dseed"])
-        if p["src"] == "generated":
-            scen, keep = dist, None
-        else:
-            keep = ctx.gen_scenarios(dist, n, m)
-            scen = (keep, A.MEM_DEVICE_TILED)
+        keep = ctx.gen_scenarios(dist, n, m)
+        scen = (keep, A.MEM_DEVICE_TILED)
     ctx.set_max_batch(p["wave"])
     try:
         got = ctx.split_eval(inst, p["tours"], scen, count=m, full=p["full"] and len(p["tours"]) == 1)
