@@ -52,7 +52,9 @@ enum ScratchSlot {
   kScrAgg,             // raw aggregates [k]
   kScrTotals,          // per-scenario totals when the caller wants host copies
   kScrOut1, kScrOut2, kScrOut3, kScrOut4, kScrOut5, kScrOut6,
-  kScrOverflow,        // split deque overflow list
+  kScrOverflow,        // general staging (DSIRP reference-layout outputs)
+  kScrHandoff,         // split hand-off bitmap + list: owned by split_eval
+                       // only (the bitmap must stay all-zero at rest)
   kScrFallback,        // overflow-path deques
   kScrCdf,             // poisson table
   kScrCustomers,       // dsirp customer records

@@ -489,6 +489,16 @@ struct TourTables {
   double costbound = 0.0;  // max over tours of dist_n + sum(c0 + ret) + max c0
 };
 
+// x (finite, >= 0) is an integer.  Branch-free and inline: std::floor is a
+// libm call on the baseline x86-64 target, and it dominated the table build
+// for large K (3 calls per position).  Below 2^52, adding and removing 2^52
+// rounds x to an integer (round-to-nearest), unchanged iff x was one; every
+// double from 2^52 up is an integer.
+inline bool is_whole(double x) {
+  constexpr double k52 = 4503599627370496.0;
+  return (x >= k52) | (((x + k52) - k52) == x);  // IEEE: not folded without -ffast-math
+}
+
 void validate_instance(const scendp_routing* inst) {
   if (!inst) fail(SCENDP_ERR_INVALID_ARGUMENT, "instance is null");
   const int n = inst->n;
@@ -534,16 +544,6 @@ void validate_tour(const int32_t* tour, int n) {
 // The integer-path check: all tour costs integral and every partial sum
 // < 2^29, so each fp64 op of the reference is exact and integer adds
 // reproduce it bit for bit.
-// x (finite, >= 0) is an integer.  Branch-free and inline: std::floor is a
-// libm call on the baseline x86-64 target, and it dominated the table build
-// for large K (3 calls per position).  Below 2^52, adding and removing 2^52
-// rounds x to an integer (round-to-nearest), unchanged iff x was one; every
-// double from 2^52 up is an integer.
-inline bool is_whole(double x) {
-  constexpr double k52 = 4503599627370496.0;
-  return (x >= k52) | (((x + k52) - k52) == x);  // IEEE: not folded without -ffast-math
-}
-
 void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
                   const TableLayout& L, char* blob, TourTables& t) {
   const int n = inst->n, side = n + 2, npad = L.npad;
@@ -575,10 +575,14 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
     for (auto& th : pool) th.join();
   };
   // an all-integer matrix makes every prefix integral (a rounded sum of
-  // integers is an integer): one scan of (n+2)^2 entries instead of 3 tests
-  // per tour position
-  bool matrix_whole = true;
-  for (size_t e = 0; e < static_cast<size_t>(side) * side; ++e) matrix_whole &= is_whole(c[e]);
+  // integers is an integer): for many tours one scan of the (n+2)^2 entries
+  // replaces the 3 tests per tour position
+  bool matrix_whole = false;
+  if (static_cast<uint64_t>(k) * n1 * 3 > static_cast<uint64_t>(side) * side) {
+    unsigned w = 1u;
+    for (size_t e = 0; e < static_cast<size_t>(side) * side; ++e) w &= static_cast<unsigned>(is_whole(c[e]));
+    matrix_whole = w != 0u;
+  }
   std::vector<char> p_intv(parts, 1), p_ident(parts, 1);
   std::vector<double> p_bound(parts, 0.0);
   for_tours([&](uint32_t q0, uint32_t q1, unsigned part) {
@@ -692,9 +696,22 @@ void set_smem(K kernel, size_t bytes) {
   granted[key] = bytes;
 }
 
+// The overflow (hand-off) pass of a wave: list mode of the generic kernel.
+template <bool FULL, int KSRC>
+void launch_overflow_pass(scendp_ctx* ctx, const SplitArgs& a, char* generic_scratch,
+                          uint64_t generic_stride, int generic_blocks) {
+  constexpr int SRC = KSRC == kSrcGenU32 ? kSrcGen : KSRC;
+  split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
+      a, 1, 0, generic_scratch, generic_stride);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->count_launch();
+}
+
+// defer_overflow: the caller reads the hand-off counter back (it syncs
+// anyway) and runs the overflow pass only when it is non-zero.
 template <bool FULL, int KSRC>
 void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic_scratch,
-                 uint64_t generic_stride, int generic_blocks) {
+                 uint64_t generic_stride, int generic_blocks, bool defer_overflow = false) {
   // K1 takes the specialized source; every other kernel the generic one
   constexpr int SRC = KSRC == kSrcGenU32 ? kSrcGen : KSRC;
   const int n = a.n;
@@ -755,10 +772,8 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   ctx->timing_end(tok);
   ctx->count_launch();
   // scenarios whose deque overflowed (or whose u32 load wrapped)
-  split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
-      a, 1, 0, generic_scratch, generic_stride);
-  CUDA_CHECK(cudaGetLastError());
-  ctx->count_launch();
+  if (!defer_overflow)
+    launch_overflow_pass<FULL, KSRC>(ctx, a, generic_scratch, generic_stride, generic_blocks);
 }
 
 }  // namespace
@@ -910,7 +925,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const uint32_t ovf_cap = static_cast<uint32_t>(
         std::min<uint64_t>(std::max<uint64_t>(wave_items / 128, 1u << 16), 1u << 26));
     const uint64_t bits_bytes = (((wave_items + 31) / 32) * 4 + 15) & ~uint64_t{15};
-    char* ovf = static_cast<char*>(ctx->scratch_get(kScrOverflow, bits_bytes + ovf_cap * 8ull));
+    char* ovf = static_cast<char*>(ctx->scratch_get(kScrHandoff, bits_bytes + ovf_cap * 8ull));
     if (ovf != ctx->ovf_base) {
       ctx->ovf_base = ovf;
       ctx->ovf_clean = 0;
@@ -930,6 +945,15 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     char* gen_scratch = static_cast<char*>(
         ctx->scratch_get(kScrFallback, generic_stride * generic_blocks * kGenericThreads));
 
+    // a call that syncs anyway, in one wave, cost-only, on one GPU reads the
+    // hand-off counter back with the aggregates and skips the (almost
+    // always empty) overflow pass -- one launch less per call
+    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+    const bool want_agg = out->agg || out->agg_raw;
+    const bool syncs = !(flags & SCENDP_ASYNC) || (host_out && out->totals) || want_agg;
+    const bool defer_ovf = syncs && !full && wave >= m && !ctx->nccl_comm;
+    SplitArgs last_a{};
+    int last_src = kSrcTiled;
     for (uint64_t w0 = 0; w0 < m || (m == 0 && w0 == 0); w0 += wave) {
       if (m == 0) break;
       const uint64_t mw = std::min(wave, m - w0);
@@ -991,23 +1015,43 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ovf_bits = d_ovf_bits;
       if (w0 > 0) CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
       const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
+      last_a = a;
+      last_src = u32 ? kSrcGenU32 : fused ? kSrcGen : kSrcTiled;
       if (full) {
         if (u32) launch_wave<true, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
         else if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
         else launch_wave<true, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
       } else {
-        if (u32) launch_wave<false, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
-        else if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
-        else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        if (u32) launch_wave<false, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
+        else if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
+        else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
       }
     }
 
     trace.mark("launch");
+    // deferred overflow pass: aggregates + hand-off counter in one read
+    const uint64_t agg_bytes = static_cast<uint64_t>(k) * sizeof(scendp_agg_raw);
+    char* h_aggc = nullptr;
+    if (defer_ovf && m > 0) {
+      h_aggc = static_cast<char*>(ctx->pinned_agg(agg_bytes + 16));
+      ctx->copy(h_aggc, aggbuf, agg_bytes + 16, cudaMemcpyDeviceToHost);
+      ctx->sync();
+      uint32_t handed_off = 0;
+      std::memcpy(&handed_off, h_aggc + agg_bytes, 4);
+      if (handed_off > 0) {
+        if (last_src == kSrcGenU32)
+          launch_overflow_pass<false, kSrcGenU32>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+        else if (last_src == kSrcGen)
+          launch_overflow_pass<false, kSrcGen>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+        else
+          launch_overflow_pass<false, kSrcTiled>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+        h_aggc = nullptr;  // aggregates changed: read them again below
+      }
+    }
     // the single collective: per-candidate raw aggregates, K x 16 u64
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(k) * kAggWords);
 
     // copies back
-    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
     if (out->totals && host_out) {
       if (zc_totals) ctx->stats.d2h_bytes += k * m * 8;  // stored by the kernels
       else download(ctx, out->totals, d_totals, k * m * 8);
@@ -1025,13 +1069,12 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
         ctx->copy(out->feasible, d_feas, m, cudaMemcpyDeviceToHost);
       }
     }
-    const bool want_agg = out->agg || out->agg_raw;
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
-      h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(k * sizeof(scendp_agg_raw)));
-      ctx->agg_readback(h_raw, d_agg, k * sizeof(scendp_agg_raw));
+      h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(agg_bytes + 16));
+      if (!h_aggc) ctx->agg_readback(h_raw, d_agg, agg_bytes);
     }
-    if (!(flags & SCENDP_ASYNC) || host_out || want_agg) ctx->sync();
+    if (syncs || (host_out && full)) ctx->sync();
     trace.mark("sync");
     if (want_agg) {
       if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, k * sizeof(scendp_agg_raw));

@@ -300,6 +300,13 @@ def test_overflow_beyond_list_capacity(ctx, oracle, reference, hard):
                 c[i, j] = abs(i - j) if i != j else 0.0
         costs = c
     inst = RoutingInstance(n, Q, hard, 0.0 if hard else 10.0, costs)
+    # a DSIRP call with reference-layout schedules first: its staging
+    # buffers must not share memory with the hand-off bitmap (regression)
+    from paper_2602_05179_b200 import Customer
+    H = 6
+    cust = Customer(U=100, I0=50, H=H, fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                    unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1)))
+    ctx.dsirp_eval([cust], oracle.generate(UNIFORM, 0, 33, 5, H, 20_000), full=True)
     tours = np.stack([np.arange(1, n + 1), np.random.default_rng(2).permutation(n) + 1])
     tours = tours.astype(np.int32)
     dem = oracle.generate(UNIFORM, 1, 2, 99, n, m)
