@@ -187,6 +187,20 @@ __device__ __forceinline__ void agg_cta_flush(const unsigned long long* cta_acc,
   }
 }
 
+// One item's aggregate straight into a global raw aggregate (kernels whose
+// items of one warp may belong to different candidates).
+__device__ __forceinline__ void agg_item_global(unsigned long long* g, double v, bool evaluated) {
+  const AggPieces pc = agg_pieces(v, evaluated);
+  if (pc.kind == 0) {
+    atomicAdd(g + pc.li, static_cast<unsigned long long>(pc.p0));
+    atomicAdd(g + pc.li + 1, static_cast<unsigned long long>(pc.p1));
+    if (pc.p2) atomicAdd(g + pc.li + 2, static_cast<unsigned long long>(pc.p2));
+    atomicAdd(g + 12, 1ULL);
+  } else if (pc.kind < 4) {
+    atomicAdd(g + 12 + pc.kind, 1ULL);  // infeasible, error, range
+  }
+}
+
 __device__ __forceinline__ void agg_cta_init(unsigned long long* cta_acc) {
   for (int t = threadIdx.x; t < kAggSlots; t += blockDim.x) cta_acc[t] = 0ULL;
 }

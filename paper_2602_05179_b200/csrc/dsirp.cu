@@ -199,7 +199,6 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     for (uint32_t c = 0; c < n_customers; ++c) validate_customer(customers[c], H);
     if (sc->rows != static_cast<uint64_t>(n_customers) * H)
       fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario batch rows must equal customers x horizon");
-    if (H > 32) fail(SCENDP_ERR_UNSUPPORTED, "horizon H > 32 is not supported by this build");
     const bool full = (flags & SCENDP_DSIRP_FULL) != 0;
     if (full && (!out->deliver || !out->quantity || !out->end_inventory || !out->route_option))
       fail(SCENDP_ERR_INVALID_ARGUMENT, "full mode needs deliver, quantity, end_inventory, route_option");
@@ -317,6 +316,8 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       }
     }
 
+    int max_u = 0;
+    for (uint32_t c = 0; c < nc; ++c) max_u = std::max(max_u, customers[c].capacity);
     uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
     for (uint64_t w0 = 0; w0 < m; w0 += wave) {
       const uint64_t mw = std::min(wave, m - w0);
@@ -352,7 +353,8 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       a.agg = d_agg;
       if (H <= 8) launch_exact(ctx, a, smem, int_path, full);
       else if (H <= 16) launch_h16(ctx, a, smem, int_path, full);
-      else launch_h32(ctx, a, smem, int_path, full);
+      else if (H <= 32) launch_h32(ctx, a, smem, int_path, full);
+      else launch_long(ctx, a, full, max_u, H);  // the reference's dense pass
     }
 
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(nc) * kAggWords);

@@ -494,6 +494,9 @@ void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, b
   }
 }
 
+// Horizons above 32: the reference's dense forward pass (dsirp_long.cu).
+void launch_long(scendp_ctx* ctx, const DsirpArgs& a, bool full, int max_u, int H);
+
 // One translation unit per horizon bound (parallel builds).
 void launch_h16(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h16.cu
 void launch_h32(scendp_ctx*, const DsirpArgs&, size_t, bool, bool);  // dsirp_h32.cu

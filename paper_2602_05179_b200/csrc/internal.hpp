@@ -55,6 +55,7 @@ enum ScratchSlot {
   kScrOverflow,        // general staging (DSIRP reference-layout outputs)
   kScrHandoff,         // split hand-off bitmap + list: owned by split_eval
                        // only (the bitmap must stay all-zero at rest)
+  kScrLongHorizon,     // DSIRP dense fallback (H > 32): per-thread frontiers
   kScrFallback,        // overflow-path deques
   kScrCdf,             // poisson table
   kScrCustomers,       // dsirp customer records

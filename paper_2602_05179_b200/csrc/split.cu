@@ -410,18 +410,7 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
       a.route_count[w] = fin ? rcs[n] : 0;
       a.feasible[w] = fin ? 1 : 0;
     }
-    const AggPieces pc = agg_pieces(v, true);
-    unsigned long long* g = a.agg + static_cast<uint64_t>(k) * kAggWords;
-    if (pc.kind == 0) {
-      atomicAdd(g + pc.li, static_cast<unsigned long long>(pc.p0));
-      atomicAdd(g + pc.li + 1, static_cast<unsigned long long>(pc.p1));
-      if (pc.p2) atomicAdd(g + pc.li + 2, static_cast<unsigned long long>(pc.p2));
-      atomicAdd(g + 12, 1ULL);
-    } else if (pc.kind == 1) {
-      atomicAdd(g + 13, 1ULL);
-    } else if (pc.kind == 3) {
-      atomicAdd(g + 15, 1ULL);
-    }
+    agg_item_global(a.agg + static_cast<uint64_t>(k) * kAggWords, v, true);
   };
   if (!list_mode) {
     for (uint64_t item = gtid; item < n_range_items; item += nthreads)

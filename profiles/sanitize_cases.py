@@ -7,7 +7,7 @@ Covers K1 (int/fp64, cost-only/full, tiled/generated, identity/permuted
 tours, overflow to the generic kernel), K2-int and its O(n) generic
 fallback, the quadratic kernel, K3 (int/fp64, cost-only/full, several
 horizons), K4 (uniform/poisson/tnormal, both layouts), the tiled
-transforms, SCNB loading and K5.
+transforms, SCNB loading, K5 and the DSIRP long-horizon kernel.
 """
 import os
 import sys
@@ -43,7 +43,7 @@ def main():
             ctx.split_eval(pen, tours, dem)
             ctx.split_eval(pen, tours[1], dem, full=True)
             ctx.split_eval(RoutingInstance(n, 30, False, 2.5, fc), tours, dem)
-        for H in (1, 6, 11):
+        for H in (1, 6, 11, 40):  # 40: the dense long-horizon kernel
             cs = [Customer(U=20, I0=5, H=H, fixed=np.full((H, 2), 7.0), unit=np.full((H, 2), 0.5)),
                   Customer(U=15, I0=3, H=H, fixed=np.full((H, 3), 3.1), unit=np.full((H, 3), 0.3))]
             dd = rng.integers(0, 25, size=(333, 2 * H)).astype(np.uint32)

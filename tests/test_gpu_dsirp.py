@@ -128,3 +128,33 @@ def test_dsirp_generated_matches_materialized(ctx):
     np.testing.assert_array_equal(a["totals"], b["totals"])
     assert a["agg"] == b["agg"]
     buf.free()
+
+
+@pytest.mark.parametrize("H,U,full", [(33, 40, True), (48, 100, False), (60, 25, True), (120, 7, True)])
+def test_long_horizons_dense_fallback(ctx, oracle, reference, H, U, full):
+    """Horizons above the sparse kernels' 32 run the reference's dense forward
+    pass on the GPU (dsirp_long.cu): totals and schedules bit-exact, tabular
+    and linear models, two customers with different capacities."""
+    from oracle import Customer as RefCustomer
+    rng = np.random.default_rng(H)
+    kws = [dict(U=U, I0=U // 2, H=H, h=0.7, rho=2.5,
+                fixed=rng.random((H, 3)) * 40, unit=rng.random((H, 3)) * 2),
+           dict(U=U + 3, I0=1, H=H, h=1.0, rho=2.0, R=1,
+                delivery_table=np.c_[np.zeros(H), rng.random((H, U + 3)) * 50],
+                holding_table=rng.random(U + 4) * 3)]
+    m = 700
+    dem = oracle.generate(UNIFORM, 0, U, 17 + H, 2 * H, m)
+    got = ctx.dsirp_eval([Customer(**kw) for kw in kws], dem, full=full)
+    for c, kw in enumerate(kws):
+        tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(
+            RefCustomer(**kw), dem[:, c * H:(c + 1) * H], 8)
+        np.testing.assert_array_equal(got["totals"][c], tot)
+        np.testing.assert_array_equal(got["evaluated"][c], ev)
+        if full:
+            np.testing.assert_array_equal(got["deliver"][c], dl)
+            np.testing.assert_array_equal(got["quantity"][c], q)
+            np.testing.assert_array_equal(got["end_inventory"][c], ei)
+            np.testing.assert_array_equal(got["route_option"][c], ro)
+        a = got["agg"][c]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)

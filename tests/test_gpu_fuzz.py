@@ -2,7 +2,8 @@
 many small configurations that together visit every kernel form and
 hand-off -- K1 (int32 / fp64, tiled or with uniform / Poisson generation
 fused), K2-int, the quadratic and generic kernels,
-K3 (exact-integer / fp64, tabular models, horizons 1..32) -- with ragged
+K3 (exact-integer / fp64, tabular models, horizons 1..32, and the
+dense fallback above 32) -- with ragged
 scenario counts, several tours, waves, and host / generated / tiled sources.
 Every per-scenario result must be bit-identical to the reference's."""
 import os
@@ -98,7 +99,7 @@ def test_split_fuzz(ctx, oracle, reference, seed):
 def _dsirp_case(seed):
     rng = np.random.default_rng(1000 + seed)
     U = int(rng.choice([1, 2, 7, 40, 100, 300]))
-    H = int(rng.choice([1, 2, 3, 6, 8, 9, 13, 20, 32]))
+    H = int(rng.choice([1, 2, 3, 6, 8, 9, 13, 20, 32, 33, 50]))
     R = int(rng.integers(1, 5))
     I0 = int(rng.integers(0, U + 1))
     dyadic = bool(rng.random() < 0.5)
