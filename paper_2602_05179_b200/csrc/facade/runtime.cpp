@@ -92,6 +92,18 @@ void check(scendp_status s) {
   }
 }
 
+double* DeviceSlot::pinned_totals(std::size_t count) {
+  const std::size_t bytes = std::max<std::size_t>(count, 1) * sizeof(double);
+  if (pinned_bytes < bytes) {
+    if (pinned) check(scendp_host_free_pinned(pinned));
+    pinned = nullptr;
+    pinned_bytes = 0;
+    check(scendp_host_alloc_pinned(bytes, &pinned));
+    pinned_bytes = bytes;
+  }
+  return static_cast<double*>(pinned);
+}
+
 DeviceSlot& device_slot(int device) {
   static std::mutex reg_mu;
   static std::map<int, std::unique_ptr<DeviceSlot>> reg;

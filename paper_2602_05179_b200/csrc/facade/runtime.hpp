@@ -20,6 +20,11 @@ void check(scendp_status s);
 struct DeviceSlot {
   scendp_ctx* ctx = nullptr;
   std::mutex mu;
+  // page-locked staging for per-scenario totals (the kernels store into it
+  // directly); grown on demand, used under `mu`
+  void* pinned = nullptr;
+  std::size_t pinned_bytes = 0;
+  double* pinned_totals(std::size_t count);
 };
 DeviceSlot& device_slot(int device);
 

@@ -4,6 +4,7 @@
 #include "scendp/split.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -49,25 +50,59 @@ BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const Giant
     out.evaluated.clear();
     return out;
   }
-  std::vector<double> totals(count);
   const scendp_routing r = to_c(inst);
   const auto shards = detail::make_shards(count, detail::devices_of(cfg));
   std::vector<double> shard_ms(shards.size());
+  std::vector<scendp_agg_raw> raws(shards.size());
+  // the reference's mean is a sequential fp64 sum (engine.hpp:195-211); when
+  // every finite total is an integer and count * max|total| < 2^53, no
+  // partial sum rounds, so it equals the engine's exact aggregate
+  std::atomic<bool> integral{true};
+  std::atomic<double> max_abs{0.0};
   detail::run_shards(shards, [&](const detail::Shard& s, scendp_ctx* ctx) {
     const std::uint64_t t0 = detail::now_ns();
     detail::check(scendp_ctx_set_max_batch(ctx, wave));
     scendp_scenarios sc = make_sc(s);
+    // totals land in the device slot's page-locked buffer (stored by the
+    // kernels over PCIe, no copy), then become the result objects
+    double* tot = detail::device_slot(s.device).pinned_totals(s.hi - s.lo);
     scendp_split_out o{};
     o.mem_kind = SCENDP_MEM_HOST;
-    o.totals = totals.data() + s.lo;
+    o.totals = tot;
+    o.agg_raw = &raws[&s - shards.data()];
     detail::check(scendp_split_eval(ctx, &r, tour.order.data(), 1, &sc, SCENDP_SPLIT_COST_ONLY, &o));
+    detail::parallel_for(s.hi - s.lo, [&](std::size_t a, std::size_t b) {
+      bool whole = true;
+      double mx = 0.0;
+      for (std::size_t w = a; w < b; ++w) {
+        const double v = tot[w];
+        out.per_scenario[s.lo + w] = ExtendedCost{v};
+        if (v < std::numeric_limits<double>::infinity()) {
+          whole &= std::fabs(v) >= 4503599627370496.0 ||
+                   v == static_cast<double>(static_cast<std::int64_t>(v));
+          mx = std::max(mx, std::fabs(v));
+        }
+      }
+      if (!whole) integral = false;
+      double cur = max_abs.load();
+      while (mx > cur && !max_abs.compare_exchange_weak(cur, mx)) {
+      }
+    });
     shard_ms[&s - shards.data()] = detail::ms_since(t0);
   });
-  for (std::size_t w = 0; w < count; ++w) out.per_scenario[w] = ExtendedCost{totals[w]};
   for (std::size_t g = 0; g < shards.size(); ++g)
     out.timings.push_back({g, shards[g].hi - shards[g].lo, shard_ms[g],
                            (shards[g].hi - shards[g].lo) * sizeof(ExtendedCost)});
-  detail::sequential_aggregate(out, [](const ExtendedCost& c) { return c.value; });
+  scendp_agg agg{};
+  detail::check(scendp_agg_finalize(raws.data(), static_cast<std::uint32_t>(raws.size()), 1, &agg));
+  if (integral && agg.range_errors == 0 &&
+      max_abs.load() * static_cast<double>(count) < 9007199254740992.0) {
+    out.finite_count = agg.finite_count;
+    out.infeasible_count = agg.infeasible_count;
+    if (agg.finite_count > 0) out.mean_cost = agg.mean;
+  } else {
+    detail::sequential_aggregate(out, [](const ExtendedCost& c) { return c.value; });
+  }
   return out;
 }
 
