@@ -85,6 +85,30 @@ int run_split(char** a) {
   std::printf("mean %.17g finite %zu infeasible %zu\n", costs.mean_cost ? *costs.mean_cost : -1.0,
               costs.finite_count, costs.infeasible_count);
   auto full = batched_expected_split(inst, tour, batch, BackendConfig::single_thread());
+  {
+    // the same call sharded over a device list ({0, 0}: two shards on one
+    // GPU) in waves of 300 scenarios: bitwise the same results
+    BackendConfig sh = BackendConfig::gpu();
+    sh.devices = {0, 0};
+    sh.batch_size = 300;
+    auto c2 = batched_split_costs(inst, tour, batch, sh);
+    bool same = c2.finite_count == costs.finite_count &&
+                c2.infeasible_count == costs.infeasible_count &&
+                c2.mean_cost.has_value() == costs.mean_cost.has_value() &&
+                (!c2.mean_cost || *c2.mean_cost == *costs.mean_cost);
+    for (std::size_t w = 0; w < m && same; ++w)
+      same = c2.per_scenario[w].value == costs.per_scenario[w].value;
+    auto f2 = batched_expected_split(inst, tour, batch, sh);
+    same = same && f2.mean_cost == full.mean_cost;
+    for (std::size_t w = 0; w < m && same; ++w) {
+      const SplitSolution &x = f2.per_scenario[w], &y = full.per_scenario[w];
+      same = x.cuts == y.cuts && x.route_count == y.route_count && x.feasible == y.feasible &&
+             x.total.value == y.total.value && x.values.values.size() == y.values.values.size();
+      for (std::size_t i = 0; same && i < x.values.values.size(); ++i)
+        same = x.values.values[i].value == y.values.values[i].value;
+    }
+    std::printf("sharded_equal %d\n", same ? 1 : 0);
+  }
   std::vector<double> v0;
   std::vector<int> c0, rcs;
   for (std::size_t w = 0; w < m && w < 4; ++w) {

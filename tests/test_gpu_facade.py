@@ -77,6 +77,7 @@ def test_facade_split_matches_reference(reference, n, Q, hard, beta, m, tseed):
     np.testing.assert_array_equal(got["cuts4"], cuts[:4].ravel())
     np.testing.assert_array_equal(got["route_count"], rc)
     assert got["full_mean"] == mean2
+    assert got["sharded_equal"] == 1  # devices {0, 0}, batch_size 300: same bits
 
 
 def test_facade_dsirp_matches_reference(reference):
