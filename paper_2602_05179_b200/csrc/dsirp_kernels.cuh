@@ -295,7 +295,7 @@ dsirp_kernel(DsirpArgs a) {
 // STDHOLD: every customer of the launch uses the standard holding model
 // h*J + rho*h*s (no per-evaluation table test).
 template <int HMAX, bool FULL, bool STDHOLD = false>
-__global__ void __launch_bounds__(kDsirpThreads)
+__global__ void __launch_bounds__(kDsirpThreads, HMAX <= 8 ? 8 : 1)  // 8 CTAs/SM: -7 % at C3/C4
 dsirp_int_kernel(DsirpArgs a) {
   constexpr int K = HMAX + 1;
   // slot loops with a constant trip count (guarded by e <= t) unroll fully,
