@@ -283,9 +283,18 @@ def run_ours(args, d: Dist):
 
     # ---- e2e: reference-facing call with host buffers ------------------------
     host_tot = pinned_empty(m, np.float64)
+    # the C-ABI call as a C/C++ caller makes it: argument structs built once,
+    # generated scenarios, per-scenario totals into host (pinned) memory and
+    # the aggregate read back -- synchronous, like batched_split_costs_generated
+    import ctypes
+    c_inst, c_dist = inst.as_c(), dist.as_c()
+    c_sc = A.Scenarios(A.MEM_GENERATED, None, n, m, w0, ctypes.pointer(c_dist))
+    c_agg = (A.Agg * 1)()
+    c_out = A.SplitOut(A.MEM_HOST, host_tot.ctypes.data, None, None, None, None, c_agg, None)
 
     def e2e_step():
-        ctx.split_eval(inst, tour, dist, count=m, first_index=w0, host_totals=host_tot)
+        A.check(ctx.lib.scendp_split_eval(ctx.handle, ctypes.byref(c_inst), tour.ctypes.data, 1,
+                                          ctypes.byref(c_sc), 0, ctypes.byref(c_out)))
 
     e2e_steps = max(3, min(args.steps, 200))
     e_ms_max, _, est = timed(ctx, d, e2e_step, e2e_steps, 2)
