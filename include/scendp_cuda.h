@@ -65,7 +65,8 @@ typedef struct scendp_ctx scendp_ctx;
  * -> max_batch (scenarios per launch wave; 0 = whole call). */
 typedef struct {
   int32_t device;          /* CUDA ordinal; -1 = current device */
-  uint64_t scratch_limit;  /* bytes; 0 = unlimited */
+  uint64_t scratch_limit;  /* bytes of staged (tiled) scenario copy per wave:
+                              caps the wave size; 0 = unlimited */
   uint64_t max_batch;      /* scenarios per launch wave; 0 = unlimited */
   uint32_t flags;          /* SCENDP_CTX_* */
 } scendp_opts;

@@ -194,9 +194,10 @@ def _agg_dict(a: A.Agg) -> dict:
 class Context:
     """One CUDA device + stream (scendp_ctx)."""
 
-    def __init__(self, device: int = 0, timing: bool = False, max_batch: int = 0):
+    def __init__(self, device: int = 0, timing: bool = False, max_batch: int = 0,
+                 scratch_limit: int = 0):
         self.lib = A.load()
-        o = A.Opts(device, 0, max_batch, A.CTX_KERNEL_TIMING if timing else 0)
+        o = A.Opts(device, scratch_limit, max_batch, A.CTX_KERNEL_TIMING if timing else 0)
         h = C.c_void_p()
         A.check(self.lib.scendp_ctx_create(C.byref(o), C.byref(h)))
         self.handle = h.value

@@ -318,7 +318,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
 
     int max_u = 0;
     for (uint32_t c = 0; c < nc; ++c) max_u = std::max(max_u, customers[c].capacity);
-    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
+    uint64_t wave = ctx->wave_for(m, sc->mem_kind == SCENDP_MEM_DEVICE_TILED ? 0 : 4ull * sc->rows);
     for (uint64_t w0 = 0; w0 < m; w0 += wave) {
       const uint64_t mw = std::min(wave, m - w0);
       scendp_scenarios sw = *sc;

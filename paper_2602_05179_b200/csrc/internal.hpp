@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -95,6 +96,15 @@ struct scendp_ctx {
   void timing_end(int token);
   void timing_resolve();  // after a stream sync
   void count_launch(uint64_t n = 1) { stats.launches += n; }
+  // scenarios per launch wave: max_batch (tile-aligned), further capped so
+  // the wave's staged scenario copy (stage_bytes per scenario) stays within
+  // scratch_limit; 0 / unset = the whole call
+  uint64_t wave_for(uint64_t m, uint64_t stage_bytes) const {
+    uint64_t w = opts.max_batch ? ((opts.max_batch + 31) & ~uint64_t{31}) : m;
+    if (opts.scratch_limit && stage_bytes)
+      w = std::min<uint64_t>(w, std::max<uint64_t>(32, (opts.scratch_limit / stage_bytes) & ~uint64_t{31}));
+    return w;
+  }
   // stream-ordered copy with H2D / D2H byte accounting (bench e2e bytes)
   void copy(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind) {
     if (bytes == 0) return;

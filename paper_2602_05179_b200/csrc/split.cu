@@ -902,7 +902,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     }
 
     // waves (BackendConfig::batch_size / memory_budget analogue)
-    uint64_t wave = ctx->opts.max_batch ? ((ctx->opts.max_batch + 31) & ~uint64_t{31}) : m;
+    uint64_t wave = ctx->wave_for(m, sc->mem_kind == SCENDP_MEM_DEVICE_TILED ? 0 : 4ull * n);
     if (wave == 0) wave = 32;
 
     // overflow items for the generic kernel: a list sized for ~1% of the

@@ -322,3 +322,24 @@ def test_overflow_beyond_list_capacity(ctx, oracle, reference, hard):
     again = ctx.split_eval(inst, tours, dem)
     np.testing.assert_array_equal(again["totals"], got["totals"])
     assert again["agg"] == got["agg"]
+
+
+def test_scratch_limit_caps_waves(oracle):
+    """scendp_opts.scratch_limit (the memory_budget analogue) bounds the
+    per-wave staged scenario copy: results are unchanged, split and DSIRP."""
+    from paper_2602_05179_b200 import Context, Customer
+    n, m = 70, 5000
+    inst = RoutingInstance(n, 60, True, 0.0, oracle.make_random_instance(n, 4))
+    dem = oracle.generate(UNIFORM, 1, 9, 21, n, m)
+    tour = rand_tour(n, 6)
+    H = 6
+    cust = Customer(U=50, I0=20, H=H, fixed=np.full((H, 2), 9.0), unit=np.full((H, 2), 0.75))
+    dd = oracle.generate(UNIFORM, 0, 30, 8, 2 * H, m)
+    with Context(0) as a, Context(0, scratch_limit=4 * n * 100) as b:
+        ra, rb = a.split_eval(inst, tour, dem), b.split_eval(inst, tour, dem)
+        da, db = a.dsirp_eval([cust, cust], dd, full=True), b.dsirp_eval([cust, cust], dd, full=True)
+    np.testing.assert_array_equal(ra["totals"], rb["totals"])
+    assert ra["agg"] == rb["agg"]
+    for key in ("totals", "deliver", "quantity", "end_inventory", "route_option"):
+        np.testing.assert_array_equal(da[key], db[key])
+    assert da["agg"] == db["agg"]
