@@ -6,6 +6,7 @@
 // C++ symbols never interpose on the product's drop-in facade).  Used by
 // tests/ to pin the oracle restatement and as bench.py's CPU baseline
 // (`cpu_baseline.kind = "reference"`, `--impl reference`).
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <exception>
@@ -23,6 +24,7 @@
 #include "scendp/split.hpp"
 
 #include "io_dump.hpp"
+#include "run_batched_probe.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -117,6 +119,15 @@ DistributionSpec make_dist(int kind, long long lo, long long hi, double mean,
 }  // namespace
 
 REF_API const char* ref_last_error() { return g_err.c_str(); }
+
+// The reference's run_batched template on the probe workload.
+REF_API int ref_run_batched_probe(size_t count, size_t batch, unsigned threads,
+                                  unsigned long long budget, unsigned long long per_bytes,
+                                  char* out, size_t cap) {
+  const std::string s = run_batched_probe(count, batch, threads, budget, per_bytes);
+  std::snprintf(out, cap, "%s", s.c_str());
+  return 0;
+}
 
 REF_API void ref_make_random_instance(int n, unsigned long long seed,
                                       double* costs) {

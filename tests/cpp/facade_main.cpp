@@ -32,6 +32,7 @@
 #include "scendp/split.hpp"
 
 #include "../../oracle/io_dump.hpp"
+#include "../../oracle/run_batched_probe.hpp"
 
 using namespace scendp;
 
@@ -364,6 +365,14 @@ int run_dense(char** a) {
 
 }  // namespace
 
+int run_batched_cmd(char** a) {
+  std::printf("%s\n", run_batched_probe(std::strtoull(a[0], nullptr, 10), std::strtoull(a[1], nullptr, 10),
+                                         static_cast<unsigned>(std::atoi(a[2])),
+                                         std::strtoull(a[3], nullptr, 10),
+                                         std::strtoull(a[4], nullptr, 10)).c_str());
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
   const std::string mode = argv[1];
@@ -379,6 +388,7 @@ int main(int argc, char** argv) {
     if (mode == "trials" && argc == 6) return run_trials(argv + 2);
     if (mode == "dense" && argc == 8) return run_dense(argv + 2);
     if (mode == "exp" && argc >= 19) return run_exp(argv + 2, argc - 18);
+    if (mode == "batched" && argc == 7) return run_batched_cmd(argv + 2);
   } catch (const std::exception& e) {
     std::printf("exception %s\n", e.what());
     return 1;
