@@ -12,6 +12,7 @@
 #include <numeric>
 #include "scendp/split.hpp"
 #include "scendp/oudp.hpp"
+#include "scendp/saa.hpp"
 using namespace scendp;
 int main() {
   const int n = 200; const std::size_t m = 1000000;
@@ -48,6 +49,21 @@ int main() {
     q1 = batched_expected_cost(spec, del, hold, sb, BackendConfig::gpu());
     auto a2 = std::chrono::steady_clock::now();
     std::printf("batched_expected_cost C3-unit 1e5: first %.1f ms, second %.1f ms mean %.6f\n", ms(a0, a1), ms(a1, a2), *q1.mean_cost);
+  }
+  {
+    // SAA first-improvement search (saa.cpp:106-189), n = 50, beta = 10,
+    // 10^5 training scenarios, 2000 candidate evaluations
+    RoutingInstance pin = make_random_instance(50, 5, 100, false, 10.0);
+    ScenarioBatch train = generate_scenarios(DistributionSpec::parse("uniform:1:10", 11), 50, 1, 100000);
+    SearchBudget budget;
+    budget.max_evaluations = 2000;
+    (void)improve_first_stage(pin, train, BackendConfig::gpu(), SearchBudget{20, budget.max_wall_seconds});
+    auto s0 = std::chrono::steady_clock::now();
+    SearchResult r = improve_first_stage(pin, train, BackendConfig::gpu(), budget);
+    auto s1 = std::chrono::steady_clock::now();
+    std::printf("improve_first_stage n=50 m=1e5: %llu evaluations in %.1f ms (%.3f ms/evaluation), value %.6f\n",
+                static_cast<unsigned long long>(r.evaluations), ms(s0, s1),
+                ms(s0, s1) / static_cast<double>(r.evaluations), r.value);
   }
   return 0;
 }
