@@ -228,6 +228,7 @@ void schedules(scendp_ctx* ctx, const scendp_customer& c, const std::uint32_t* d
   o.end_inventory = ei.get();
   o.route_option = ro.get();
   detail::check(scendp_dsirp_eval(ctx, &c, 1, &sc, SCENDP_DSIRP_FULL, &o));
+  detail::MallocPadScope pad(std::size_t{64} << 20);
   detail::parallel_for(count, [&](std::size_t lo, std::size_t hi) {
     for (std::size_t w = lo; w < hi; ++w) {
       if (!evaluated[w]) continue;

@@ -3,6 +3,11 @@
 // proj/src/engine.cpp:7-30) and ValueFrontier::initial (minplus.cpp:8-21).
 #include "runtime.hpp"
 
+#include <cstdlib>
+#ifdef __GLIBC__
+#include <malloc.h>
+#endif
+
 #include <algorithm>
 #include <chrono>
 #include <exception>
@@ -92,6 +97,30 @@ void check(scendp_status s) {
   }
 }
 
+#ifdef __GLIBC__
+namespace {
+// glibc's top pad: DEFAULT_TOP_PAD (128 KB) unless MALLOC_TOP_PAD_ set it
+std::size_t default_top_pad() {
+  const char* e = std::getenv("MALLOC_TOP_PAD_");
+  return e ? static_cast<std::size_t>(std::strtoull(e, nullptr, 10)) : std::size_t{128} << 10;
+}
+std::mutex g_pad_mu;
+int g_pad_users = 0;
+}  // namespace
+
+MallocPadScope::MallocPadScope(std::size_t pad) {
+  std::lock_guard<std::mutex> g(g_pad_mu);
+  if (g_pad_users++ == 0) mallopt(M_TOP_PAD, static_cast<int>(std::min<std::size_t>(pad, 1u << 30)));
+}
+MallocPadScope::~MallocPadScope() {
+  std::lock_guard<std::mutex> g(g_pad_mu);
+  if (--g_pad_users == 0) mallopt(M_TOP_PAD, static_cast<int>(default_top_pad()));
+}
+#else
+MallocPadScope::MallocPadScope(std::size_t) {}
+MallocPadScope::~MallocPadScope() {}
+#endif
+
 double* DeviceSlot::pinned_totals(std::size_t count) {
   const std::size_t bytes = std::max<std::size_t>(count, 1) * sizeof(double);
   if (pinned_bytes < bytes) {
@@ -102,6 +131,19 @@ double* DeviceSlot::pinned_totals(std::size_t count) {
     pinned_bytes = bytes;
   }
   return static_cast<double*>(pinned);
+}
+
+void* DeviceSlot::pinned_chunk(int which, std::size_t bytes) {
+  if (chunk_bytes < bytes) {
+    for (auto& c : chunk) {
+      if (c) check(scendp_host_free_pinned(c));
+      c = nullptr;
+    }
+    chunk_bytes = 0;
+    for (auto& c : chunk) check(scendp_host_alloc_pinned(bytes, &c));
+    chunk_bytes = bytes;
+  }
+  return chunk[which];
 }
 
 DeviceSlot& device_slot(int device) {

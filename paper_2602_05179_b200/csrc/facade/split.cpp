@@ -4,6 +4,9 @@
 #include "scendp/split.hpp"
 
 #include <algorithm>
+#include <thread>
+#include <cstdlib>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <limits>
@@ -106,49 +109,96 @@ BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const Giant
   return out;
 }
 
-// Full solutions for host columns [lo, hi) of `scen` on one context.  One
-// evaluation of the whole range, then the SplitSolution objects are built by
-// up to 16 host threads.  (Measured at C2: chunking the range and overlapping
-// the next chunk's evaluation with object construction is 2x slower -- the
-// construction is bound by first-touch page faults of the objects' fresh
-// heap memory, which contend with the transfers' page pinning.)
+// Full solutions for host columns [lo, hi) of `scen` on one context.  The
+// evaluator leaves V and cuts on the device (reference layout); they come
+// back in chunks of scenarios through two page-locked buffers, a helper
+// thread copying chunk k+1 while the host threads turn chunk k into
+// SplitSolution objects -- no full-size pageable intermediate.  Object
+// construction runs under MallocPadScope (see runtime.hpp).
 void full_impl(scendp_ctx* ctx, const scendp_routing& r, const GiantTour& tour,
                const std::uint32_t* data, std::size_t count, bool quadratic,
-               SplitSolution* dst) {
+               SplitSolution* dst, detail::DeviceSlot& slot) {
   const int n = r.n;
   const std::size_t n1 = static_cast<std::size_t>(n) + 1;
-  // scratch filled entirely by the evaluator: default-initialized (no 2.4 GB
-  // zero fill at C2)
-  std::unique_ptr<double[]> V(new double[count * n1]), totals(new double[count]);
-  std::unique_ptr<std::int32_t[]> cuts(new std::int32_t[count * n1]), rc(new std::int32_t[count]);
-  std::unique_ptr<std::uint8_t[]> feas(new std::uint8_t[count]);
+  struct DevBuf {
+    scendp_ctx* ctx;
+    void* p = nullptr;
+    DevBuf(scendp_ctx* c, std::size_t bytes) : ctx(c) {
+      detail::check(scendp_device_alloc(ctx, std::max<std::size_t>(bytes, 1), &p));
+    }
+    ~DevBuf() { scendp_device_free(ctx, p); }
+  };
+  DevBuf dV(ctx, count * n1 * 8), dC(ctx, count * n1 * 4), dT(ctx, count * 8), dR(ctx, count * 4),
+      dF(ctx, count);
   scendp_scenarios sc{};
   sc.mem_kind = SCENDP_MEM_HOST;
   sc.data = data;
   sc.rows = static_cast<std::uint64_t>(n);
   sc.count = count;
   scendp_split_out o{};
-  o.mem_kind = SCENDP_MEM_HOST;
-  o.totals = totals.get();
-  o.values = V.get();
-  o.cuts = cuts.get();
-  o.route_count = rc.get();
-  o.feasible = feas.get();
+  o.mem_kind = SCENDP_MEM_DEVICE;
+  o.totals = static_cast<double*>(dT.p);
+  o.values = static_cast<double*>(dV.p);
+  o.cuts = static_cast<std::int32_t*>(dC.p);
+  o.route_count = static_cast<std::int32_t*>(dR.p);
+  o.feasible = static_cast<std::uint8_t*>(dF.p);
+  const std::uint64_t t0 = detail::now_ns();
   detail::check(scendp_split_eval(ctx, &r, tour.order.data(), 1, &sc,
                                   SCENDP_SPLIT_FULL | (quadratic ? SCENDP_QUADRATIC : 0u), &o));
-  detail::parallel_for(count, [&](std::size_t lo, std::size_t hi) {
-    for (std::size_t w = lo; w < hi; ++w) {
-      SplitSolution& s = dst[w];
-      s.values.stage = 1;
-      s.values.values.resize(n1);
-      const double* v = V.get() + w * n1;
-      for (std::size_t i = 0; i < n1; ++i) s.values.values[i] = ExtendedCost{v[i]};
-      s.cuts.assign(cuts.get() + w * n1, cuts.get() + (w + 1) * n1);
-      s.total = ExtendedCost{totals[w]};
-      s.route_count = rc[w];
-      s.feasible = feas[w] != 0;
+  std::unique_ptr<double[]> totals(new double[std::max<std::size_t>(count, 1)]);
+  std::unique_ptr<std::int32_t[]> rc(new std::int32_t[std::max<std::size_t>(count, 1)]);
+  std::unique_ptr<std::uint8_t[]> feas(new std::uint8_t[std::max<std::size_t>(count, 1)]);
+  detail::check(scendp_memcpy(ctx, totals.get(), dT.p, count * 8, 1, 0));
+  detail::check(scendp_memcpy(ctx, rc.get(), dR.p, count * 4, 1, 0));
+  detail::check(scendp_memcpy(ctx, feas.get(), dF.p, count, 1, 0));
+  const double eval_ms = detail::ms_since(t0);
+
+  const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, (48u << 20) / (n1 * 12)));
+  const std::size_t vbytes = chunk * n1 * 8;
+  char* buf[2] = {static_cast<char*>(slot.pinned_chunk(0, chunk * n1 * 12)),
+                  static_cast<char*>(slot.pinned_chunk(1, chunk * n1 * 12))};
+  auto fetch = [&](std::size_t lo, char* b) -> scendp_status {
+    const std::size_t c = std::min(chunk, count - lo);
+    scendp_status s = scendp_memcpy(ctx, b, static_cast<const char*>(dV.p) + lo * n1 * 8,
+                                    c * n1 * 8, 1, 0);
+    if (s == SCENDP_OK)
+      s = scendp_memcpy(ctx, b + vbytes, static_cast<const char*>(dC.p) + lo * n1 * 4, c * n1 * 4,
+                        1, 0);
+    return s;
+  };
+  detail::MallocPadScope pad(std::size_t{64} << 20);
+  if (count > 0) detail::check(fetch(0, buf[0]));
+  for (std::size_t lo = 0, k = 0; lo < count; lo += chunk, k ^= 1) {
+    const std::size_t next = lo + chunk;
+    scendp_status ns = SCENDP_OK;
+    std::thread copier;
+    if (next < count) copier = std::thread([&, next] { ns = fetch(next, buf[k ^ 1]); });
+    const double* V = reinterpret_cast<const double*>(buf[k]);
+    const std::int32_t* C = reinterpret_cast<const std::int32_t*>(buf[k] + vbytes);
+    try {
+      detail::parallel_for(std::min(chunk, count - lo), [&](std::size_t a, std::size_t e) {
+        for (std::size_t j = a; j < e; ++j) {
+          SplitSolution& s = dst[lo + j];
+          s.values.stage = 1;
+          s.values.values.resize(n1);
+          const double* v = V + j * n1;
+          for (std::size_t i = 0; i < n1; ++i) s.values.values[i] = ExtendedCost{v[i]};
+          s.cuts.assign(C + j * n1, C + (j + 1) * n1);
+          s.total = ExtendedCost{totals[lo + j]};
+          s.route_count = rc[lo + j];
+          s.feasible = feas[lo + j] != 0;
+        }
+      }, 0, 1024);
+    } catch (...) {
+      if (copier.joinable()) copier.join();
+      throw;
     }
-  });
+    if (copier.joinable()) copier.join();
+    detail::check(ns);
+  }
+  if (std::getenv("SCENDP_HOST_TRACE"))
+    std::fprintf(stderr, "facade full: evaluate %.1f ms, download + result objects %.1f ms\n",
+                 eval_ms, detail::ms_since(t0) - eval_ms);
 }
 
 SplitSolution single_scenario(const RoutingInstance& inst, const GiantTour& tour,
@@ -159,7 +209,7 @@ SplitSolution single_scenario(const RoutingInstance& inst, const GiantTour& tour
   detail::DeviceSlot& slot = detail::device_slot(-1);
   std::lock_guard<std::mutex> g(slot.mu);
   detail::check(scendp_ctx_set_max_batch(slot.ctx, 0));
-  full_impl(slot.ctx, r, tour, demand.data(), 1, quadratic, &s);
+  full_impl(slot.ctx, r, tour, demand.data(), 1, quadratic, &s, slot);
   return s;
 }
 
@@ -306,7 +356,7 @@ BatchResultSet<SplitSolution> batched_expected_split(const RoutingInstance& inst
     detail::check(scendp_ctx_set_max_batch(ctx, wave));
     // hard -> linear deque, penalized -> quadratic (split.cpp:316-318)
     full_impl(ctx, r, tour, scenarios.data.data() + s.lo * scenarios.rows, s.hi - s.lo, false,
-              out.per_scenario.data() + s.lo);
+              out.per_scenario.data() + s.lo, detail::device_slot(s.device));
     (void)t0;
   });
   detail::sequential_aggregate(out, [](const SplitSolution& s) { return s.total.value; });
