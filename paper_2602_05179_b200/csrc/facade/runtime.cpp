@@ -7,6 +7,9 @@
 #ifdef __GLIBC__
 #include <malloc.h>
 #endif
+#ifdef __linux__
+#include <sys/mman.h>
+#endif
 
 #include <algorithm>
 #include <chrono>
@@ -120,6 +123,19 @@ MallocPadScope::~MallocPadScope() {
 MallocPadScope::MallocPadScope(std::size_t) {}
 MallocPadScope::~MallocPadScope() {}
 #endif
+
+void advise_huge_pages(void* p, std::size_t bytes) {
+#ifdef __linux__
+  constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20;
+  if (bytes < 4 * kHuge) return;
+  const std::uintptr_t a = (reinterpret_cast<std::uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+  const std::uintptr_t e = (reinterpret_cast<std::uintptr_t>(p) + bytes) & ~(kHuge - 1);
+  if (e > a) (void)madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
 
 double* DeviceSlot::pinned_totals(std::size_t count) {
   const std::size_t bytes = std::max<std::size_t>(count, 1) * sizeof(double);

@@ -343,6 +343,8 @@ BatchResultSet<SplitSolution> batched_expected_split(const RoutingInstance& inst
   BatchResultSet<SplitSolution> out;
   const std::size_t m = scenarios.count;
   const std::size_t wave = detail::wave_size(cfg, m, split_per_scenario_bytes(inst.n), &out.warnings);
+  out.per_scenario.reserve(m);
+  detail::advise_huge_pages(out.per_scenario.data(), m * sizeof(SplitSolution));
   out.per_scenario.resize(m);
   out.evaluated.assign(m, 1);
   if (m == 0) {
