@@ -96,9 +96,9 @@ gen_tnormal_kernel(int64_t lo, int64_t hi, double mean, double stddev,
 
 // Reference layout [count][rows] -> tiled [count/32][rows][32] (32x32 smem
 // transpose, both sides coalesced).  Element type is 4 bytes.
-template <typename T>
+template <typename T, typename S = T>
 __global__ void __launch_bounds__(256)
-to_tiled_kernel(const T* __restrict__ src, uint64_t rows, uint64_t count,
+to_tiled_kernel(const S* __restrict__ src, uint64_t rows, uint64_t count,
                 T* __restrict__ dst) {
   __shared__ T tile[32][33];
   const uint64_t w0 = blockIdx.x * uint64_t(32);
@@ -235,6 +235,40 @@ template void launch_from_tiled<int32_t>(scendp_ctx*, const int32_t*, uint64_t, 
 template void launch_from_tiled<uint8_t>(scendp_ctx*, const uint8_t*, uint64_t, uint64_t, uint8_t*);
 template void launch_from_tiled<uint32_t>(scendp_ctx*, const uint32_t*, uint64_t, uint64_t, uint32_t*);
 
+// Narrowed host chunks (u8 per demand) widened while tiling.
+void launch_to_tiled_u8(scendp_ctx* ctx, const uint8_t* src, uint64_t rows, uint64_t count,
+                        uint32_t* dst) {
+  if (count == 0 || rows == 0) return;
+  dim3 grid(static_cast<unsigned>((count + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  to_tiled_kernel<uint32_t, uint8_t><<<grid, 256, 0, ctx->stream>>>(src, rows, count, dst);
+  CUDA_CHECK(cudaGetLastError());
+  ctx->count_launch();
+}
+
+// u32 -> u8 of `n` values split over up to `threads` host threads; false if
+// any value needs more than 8 bits (the chunk then goes as u32)
+static bool parallel_pack_u8(uint8_t* dst, const uint32_t* src, uint64_t n, int threads) {
+  const uint64_t per = ((n + threads - 1) / threads + 4095) & ~uint64_t{4095};
+  std::vector<uint32_t> wide(threads, 0u);
+  auto pack = [&](int t) {
+    const uint64_t lo = per * t, hi = std::min(n, per * (t + 1));
+    uint32_t acc = 0u;
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint32_t v = src[i];
+      acc |= v;
+      dst[i] = static_cast<uint8_t>(v);
+    }
+    wide[t] = acc >> 8;
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads && per * t < n; ++t) pool.emplace_back(pack, t);
+  pack(0);
+  for (auto& th : pool) th.join();
+  uint32_t any = 0u;
+  for (uint32_t w : wide) any |= w;
+  return any == 0u;
+}
+
 // memcpy of `bytes` split over up to `threads` host threads
 static void parallel_copy(char* dst, const char* src, uint64_t bytes, int threads) {
   const uint64_t per = ((bytes + threads - 1) / threads + 4095) & ~uint64_t{4095};
@@ -249,10 +283,12 @@ static void parallel_copy(char* dst, const char* src, uint64_t bytes, int thread
 }
 
 // A pageable host scenario set (the reference's ScenarioBatch vector) into
-// the tiled layout: a driver-staged cudaMemcpy from pageable memory runs at
-// ~11 GB/s, so whole-tile chunks are copied by up to 8 host threads into two
-// page-locked buffers (alternating, event-guarded) while the previous
-// chunk's H2D copy and tiling run on the stream (~PCIe speed).
+// the tiled layout, in whole-tile chunks: up to 16 host threads stage each
+// chunk into one of two page-locked buffers (alternating, event-guarded)
+// while the previous chunk's H2D copy and tiling run on the stream (a
+// driver-staged copy from pageable memory runs at ~11 GB/s).  Demands below
+// 256 are narrowed to one byte while staging (1/4 of the PCIe bytes, widened
+// by the tiling kernel); a chunk with a wider value is copied as is.
 void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, uint64_t count,
                            uint32_t* dst) {
   constexpr uint64_t kChunkBytes = 64ull << 20;
@@ -268,11 +304,27 @@ void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, 
   for (auto& e : done) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   bool used[2] = {false, false};
   const char* s = reinterpret_cast<const char*>(src);
+  // demands below 256 (the usual case) cross PCIe as one byte each: packed
+  // by the host threads while they stage, widened by the tiling kernel; the
+  // first chunk with a wider value switches the rest of the call to u32
+  bool narrow = true;
   for (uint64_t c0 = 0, j = 0; c0 < count; c0 += chunk, ++j) {
     const uint64_t cn = std::min(chunk, count - c0);
     const int b = static_cast<int>(j & 1);
     if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));
     const uint64_t bytes = cn * col_bytes;
+    if (narrow) {
+      uint8_t* p8 = reinterpret_cast<uint8_t*>(pin[b]);
+      if (parallel_pack_u8(p8, src + c0 * rows, cn * rows, threads)) {
+        uint8_t* d8 = reinterpret_cast<uint8_t*>(dstage);
+        ctx->copy(d8, p8, cn * rows, cudaMemcpyHostToDevice);
+        launch_to_tiled_u8(ctx, d8, rows, cn, dst + (c0 / 32) * rows * 32);
+        CUDA_CHECK(cudaEventRecord(done[b], ctx->stream));
+        used[b] = true;
+        continue;
+      }
+      narrow = false;
+    }
     parallel_copy(pin[b], s + c0 * col_bytes, bytes, threads);
     ctx->copy(dstage, pin[b], bytes, cudaMemcpyHostToDevice);
     launch_to_tiled<uint32_t>(ctx, dstage, rows, cn, dst + (c0 / 32) * rows * 32);
@@ -339,7 +391,8 @@ const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
       if (!sc->data && count) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenario data is null");
       uint32_t* dst = static_cast<uint32_t*>(ctx->scratch_get(kScrScenarios, tiled_bytes));
       if (mapped_host_alias(const_cast<uint32_t*>(sc->data)) || rows * count * 4 <= (16ull << 20)) {
-        // page-locked (DMA straight from it) or small: one copy
+        // page-locked (DMA straight from it: measured faster than narrowing
+        // it on the host) or small: one copy
         uint32_t* stg = static_cast<uint32_t*>(ctx->scratch_get(kScrStaging, rows * count * 4));
         ctx->copy(stg, sc->data, rows * count * 4, cudaMemcpyHostToDevice);
         launch_to_tiled<uint32_t>(ctx, stg, rows, count, dst);

@@ -343,3 +343,21 @@ def test_scratch_limit_caps_waves(oracle):
     for key in ("totals", "deliver", "quantity", "end_inventory", "route_option"):
         np.testing.assert_array_equal(da[key], db[key])
     assert da["agg"] == db["agg"]
+
+
+def test_pageable_upload_narrow_and_wide_chunks(ctx, oracle):
+    """Pageable host sets above 16 MB are staged in 64 MB chunks; demands
+    below 256 cross PCIe as bytes.  A wide value in a later chunk switches
+    the rest of the call to u32; a wide value in the first chunk keeps it
+    u32 throughout.  Totals equal the oracle's either way."""
+    n, m, Q = 100, 300_000, 1000
+    inst = RoutingInstance(n, Q, True, 0.0, oracle.make_random_instance(n, 12))
+    tour = rand_tour(n, 13)
+    base = oracle.generate(UNIFORM, 1, 10, 33, n, m)
+    for where in (None, m // 2, 3):
+        dem = base.copy()
+        if where is not None:
+            dem[where, 7] = 300   # needs 9 bits
+        got = ctx.split_eval(inst, tour, dem)
+        want = oracle.split_batch(n, Q, 1, 0.0, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], want)
