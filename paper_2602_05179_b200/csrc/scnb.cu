@@ -33,6 +33,8 @@ using namespace scendp_host;
 namespace scendp_host {
 template <typename T>
 void launch_to_tiled(scendp_ctx* ctx, const T* src, uint64_t rows, uint64_t count, T* dst);
+void launch_to_tiled_u8(scendp_ctx* ctx, const uint8_t* src, uint64_t rows, uint64_t count,
+                        uint32_t* dst);
 }
 
 namespace {
@@ -99,6 +101,49 @@ void read_parallel(int fd, void* dst, uint64_t bytes, uint64_t off, const std::s
   for (auto& t : pool) t.join();
   for (const auto& e : errs)
     if (!e.empty()) fail(SCENDP_ERR_RUNTIME, e);
+}
+
+// Read `n` u32 values at file offset `off` and store them narrowed to bytes
+// at dst, over up to `threads` readers, each through a small cache-resident
+// block (the page-cache copy then stays in cache; only n bytes are written
+// to the page-locked buffer).  Returns false when a value needs more than 8
+// bits (the caller then reads the chunk as u32).
+bool read_parallel_u8(int fd, uint8_t* dst, uint64_t n, uint64_t off, const std::string& name,
+                      const char* what, int threads) {
+  constexpr uint64_t kBlock = 64ull << 10;  // values per read (256 KB)
+  const int parts = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(threads), n / (2ull << 20))));
+  const uint64_t per = (n + parts - 1) / parts;
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(parts);
+  std::vector<uint32_t> wide(parts, 0u);
+  auto work = [&](int p) {
+    const uint64_t lo = std::min(n, per * p), hi = std::min(n, per * (p + 1));
+    std::vector<uint32_t> blk(kBlock);
+    uint32_t acc = 0u;
+    try {
+      for (uint64_t a = lo; a < hi; a += kBlock) {
+        const uint64_t c = std::min(kBlock, hi - a);
+        read_full(fd, blk.data(), c * 4, off + a * 4, name, what);
+        for (uint64_t i = 0; i < c; ++i) {
+          acc |= blk[i];
+          dst[a + i] = static_cast<uint8_t>(blk[i]);
+        }
+        if (acc >> 8) break;  // wide: the chunk will be re-read as u32
+      }
+    } catch (const Error& e) {
+      errs[p] = e.msg;
+    }
+    wide[p] = acc >> 8;
+  };
+  for (int p = 1; p < parts; ++p) pool.emplace_back(work, p);
+  work(0);
+  for (auto& t : pool) t.join();
+  for (const auto& e : errs)
+    if (!e.empty()) fail(SCENDP_ERR_RUNTIME, e);
+  for (uint32_t w : wide)
+    if (w) return false;
+  return true;
 }
 
 // Header checks in the reference's order and wording (io.cpp:316-333).
@@ -173,11 +218,28 @@ scendp_status scendp_scnb_load(scendp_ctx* ctx, const char* path, uint64_t first
     cudaEvent_t done[2];
     for (auto& e : done) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     bool used[2] = {false, false};
+    // tiled output: values below 256 (the usual demands) are narrowed to
+    // bytes while read and widened by the tiling kernel (1/4 of the PCIe
+    // bytes); the first chunk with a wider value switches to u32
+    bool narrow = layout == SCENDP_MEM_DEVICE_TILED;
     try {
       for (uint64_t c0 = 0, j = 0; c0 < count; c0 += chunk, ++j) {
         const uint64_t cn = std::min(chunk, count - c0);
         const int b = static_cast<int>(j & 1);
         if (used[b]) CUDA_CHECK(cudaEventSynchronize(done[b]));  // buffer b drained
+        if (narrow) {
+          uint8_t* p8 = reinterpret_cast<uint8_t*>(pin[b]);
+          if (read_parallel_u8(f.fd, p8, cn * rows, kScnbHeader + (first + c0) * col_bytes, path,
+                               "truncated scenario payload", readers)) {
+            uint8_t* d8 = reinterpret_cast<uint8_t*>(dstage);
+            ctx->copy(d8, p8, cn * rows, cudaMemcpyHostToDevice);
+            launch_to_tiled_u8(ctx, d8, rows, cn, out + (c0 / 32) * rows * 32);
+            CUDA_CHECK(cudaEventRecord(done[b], ctx->stream));
+            used[b] = true;
+            continue;
+          }
+          narrow = false;
+        }
         read_parallel(f.fd, pin[b], cn * col_bytes, kScnbHeader + (first + c0) * col_bytes,
                       path, "truncated scenario payload", readers);
         if (layout == SCENDP_MEM_DEVICE) {
