@@ -48,3 +48,18 @@ def test_scnb_multichunk_and_evaluation(ctx, oracle, reference, tmp_path):
     np.testing.assert_array_equal(got["totals"][0], tot)
     assert got["agg"][0]["mean"] == mean
     buf.free()
+
+
+def test_scnb_narrow_then_wide_chunks(ctx, oracle, tmp_path):
+    """Tiled loads narrow byte-sized values while reading; a wider value in a
+    later chunk switches the rest of the load to u32 -- the tiled set is the
+    file's either way (values 0..9, then one 70000 in the last chunk)."""
+    n, m = 200, 200_000
+    dem = oracle.generate(UNIFORM, 0, 9, 5, n, m)
+    dem[m - 10, 17] = 70_000
+    path = tmp_path / "mixed.scnb"
+    ctx.scnb_write(path, dem)
+    til = ctx.scnb_load(path, tiled=True)
+    flat = til.download(np.uint32, ctx.tiled_bytes(n, m) // 4)
+    np.testing.assert_array_equal(tiled_to_reference(flat, n, m), dem)
+    til.free()
