@@ -152,6 +152,7 @@ struct scendp_ctx {
   cudaEvent_t tables_done = nullptr;
   void* pinned_tables(uint64_t bytes);
   std::vector<char> tours_blob;  // split tour tables resident at tours_dev
+  std::vector<double> valid_costs;  // last cost matrix that passed validation
   void* tours_dev = nullptr;
   void tables_uploaded();
 };

@@ -488,6 +488,13 @@ inline bool is_whole(double x) {
   return (x >= k52) | (((x + k52) - k52) == x);  // IEEE: not folded without -ffast-math
 }
 
+// The instance checks other than the cost matrix scan (split.cpp:128-138).
+void validate_instance_scalars(const scendp_routing* inst) {
+  if (inst->capacity <= 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "capacity Q must be > 0");
+  if (!inst->hard && !(inst->penalty_beta >= 0.0))
+    fail(SCENDP_ERR_INVALID_ARGUMENT, "penalty beta must be >= 0");
+}
+
 void validate_instance(const scendp_routing* inst) {
   if (!inst) fail(SCENDP_ERR_INVALID_ARGUMENT, "instance is null");
   const int n = inst->n;
@@ -799,7 +806,17 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
   return guard([&] {
     if (!ctx) fail(SCENDP_ERR_INVALID_ARGUMENT, "ctx is null");
     if (!sc || !out) fail(SCENDP_ERR_INVALID_ARGUMENT, "scenarios/out is null");
-    validate_instance(inst);
+    // the scan of the (n+2)^2 matrix is skipped when it equals the last one
+    // that passed (glibc's vectorized memcmp is several times faster than
+    // the checks); the rest of the instance is validated every call
+    const size_t cells = (static_cast<size_t>(inst ? inst->n : 0) + 2) * (static_cast<size_t>(inst ? inst->n : 0) + 2);
+    if (inst && inst->n >= 1 && inst->costs && ctx->valid_costs.size() == cells &&
+        std::memcmp(ctx->valid_costs.data(), inst->costs, cells * sizeof(double)) == 0) {
+      validate_instance_scalars(inst);
+    } else {
+      validate_instance(inst);
+      ctx->valid_costs.assign(inst->costs, inst->costs + cells);
+    }
     const int n = inst->n;
     if (!tours || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one tour");
     if (k_tours >= (1u << 23)) fail(SCENDP_ERR_UNSUPPORTED, "too many tours per call");
