@@ -146,18 +146,23 @@ void launch_long(scendp_ctx* ctx, const DsirpArgs& a, bool full, int max_u, int 
   const uint32_t max_states = static_cast<uint32_t>(max_u) + 1;
   const uint64_t per_thread = static_cast<uint64_t>(max_states) *
                               (2 * sizeof(double) + (full ? static_cast<uint64_t>(H) * 4 : 0));
-  // as many threads as 512 MB of scratch allows (>= one warp), 128 per CTA
+  // as many threads as 512 MB of scratch allows, at least one warp, in
+  // CTAs of 128 (or of one warp when fewer than 128 fit)
   constexpr uint64_t kBudget = 512ull << 20;
+  if (per_thread > (16ull << 30) / 32)
+    scendp_host::fail(SCENDP_ERR_UNSUPPORTED,
+                      "dsirp: capacity x horizon too large for the dense long-horizon path");
   uint64_t threads = std::max<uint64_t>(32, kBudget / per_thread);
-  threads = std::min<uint64_t>(threads, (items + 127) / 128 * 128);
+  threads = std::min<uint64_t>(threads, (items + 31) / 32 * 32);
   threads = std::min<uint64_t>(threads, static_cast<uint64_t>(ctx->sm_count) * 2048);
-  const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
-  const uint64_t grid_threads = static_cast<uint64_t>(blocks) * 128;
+  const unsigned block = threads >= 128 ? 128u : 32u;
+  const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(1, threads / block));
+  const uint64_t grid_threads = static_cast<uint64_t>(blocks) * block;
   char* scratch = static_cast<char*>(
       ctx->scratch_get(scendp_host::kScrLongHorizon, grid_threads * per_thread + 16));
   const int tok = ctx->timing_begin(0);
-  if (full) dsirp_dense_kernel<true><<<blocks, 128, 0, ctx->stream>>>(a, scratch, max_states);
-  else dsirp_dense_kernel<false><<<blocks, 128, 0, ctx->stream>>>(a, scratch, max_states);
+  if (full) dsirp_dense_kernel<true><<<blocks, block, 0, ctx->stream>>>(a, scratch, max_states);
+  else dsirp_dense_kernel<false><<<blocks, block, 0, ctx->stream>>>(a, scratch, max_states);
   scendp_host::cuda_check(cudaGetLastError(), "dsirp dense kernel launch");
   ctx->timing_end(tok);
   ctx->count_launch();
