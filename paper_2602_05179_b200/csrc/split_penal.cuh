@@ -152,16 +152,19 @@ split_penal_kernel(SplitArgs a) {
       // the window start advances past positions whose route (p, i]
       // overflows; d_i <= Q keeps p = i-1 inside, so no bound test is needed
       if (out_of_window(lo_c)) {
-        // two window tests per trip, their shared loads issued together (the
-        // loop is latency-bound).  The second one may look at lo+2: it is
-        // only used when lo+1 left the window, and then lo+2 <= i-1 (entry
+        // three window tests per trip, their shared loads issued together (the
+        // loop is latency-bound).  Test k (k = 2, 3) may look up to lo+k: it is
+        // only used when lo+k-1 left the window, and then lo+k <= i-1 (entry
         // i-1 never leaves when d_i <= Q), so it reads a written slot.
         for (;;) {
-          const bool o1 = out_of_window(lo_c + kH), o2 = out_of_window(lo_c + 2 * kH);
+          const bool o1 = out_of_window(lo_c + kH), o2 = out_of_window(lo_c + 2 * kH),
+                     o3 = out_of_window(lo_c + 3 * kH);
           lo_c += kH;
           if (!o1) break;
           lo_c += kH;
           if (!o2) break;
+          lo_c += kH;
+          if (!o3) break;
         }
         const int pc = lo_c - kH;  // lo - 1
         bmin = at32(ps_pm, pc, kPosMaskH);
