@@ -20,7 +20,7 @@ uniform:1:10 demands (the reference default), 10^6 scenarios per GPU
          compiled from /root/reference sources) running the same call with all
          host threads.
 
-Secondary lines (DSIRP C3/C4, SAA C5 candidate sweep, penalized and
+Secondary lines (DSIRP C3/C4 and the non-dyadic C3 twin, SAA C5 candidate sweep, penalized and
 float-cost split, full solutions, K5 min-plus, SCNB ingestion) ride in the
 same JSON object under "secondary"; at N = 1 each split/DSIRP line carries
 "cpu_reference", the reference's own evaluator (oracle/_ref) on a bounded
@@ -528,6 +528,25 @@ def secondary(ctx, d: Dist, args):
                      "scaling": "strong" if name == "dsirp_c4" else "weak"}
         sc.free()
         t3.free()
+    # non-dyadic twin of C3: h, rho, fixed and unit drawn as
+    # fractions, so the exact-integer kernel does not apply and K3's fp64
+    # path (the reference's association) runs
+    H, nc, m3 = 6, 50, 100_000
+    rng = np.random.default_rng(21)
+    fcusts = [Customer(U=100, I0=50, H=H, h=0.5 + rng.random(), rho=1.5 + rng.random(),
+                       fixed=30 + 20 * rng.random((H, 3)), unit=0.25 + rng.random((H, 3)))
+              for _ in range(nc)]
+    sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m3, w0=d.rank * m3)
+    t3 = ctx.alloc(nc * m3 * 8)
+    step_ms, k_ms = kernel_rate(lambda: ctx.dsirp_eval(
+        fcusts, (sc, A.MEM_DEVICE_TILED), count=m3, out_kind="device_tiled",
+        device_out={"totals": t3}, sync=False), 20)
+    out["dsirp_c3_float"] = {"value": d.world * nc * m3 / (step_ms / 1e3),
+                             "unit": "(customer, scenario)-evals/s", "kernel_ms": k_ms,
+                             "customers": nc, "scenarios": d.world * m3, "dtype": "f64",
+                             "scaling": "weak"}
+    sc.free()
+    t3.free()
     return out
 
 
@@ -584,6 +603,12 @@ def cpu_reference_secondary():
     r3 = rate(lambda: [R.expected_cost(cust, d3, threads) for _ in range(nc)], nc * m3)
     for name in ("dsirp_c3", "dsirp_c4"):
         out[name] = (r3, f"{nc} customers x batched_expected_cost (U=100, H=6, R=3, 10^5)")
+    rngf = np.random.default_rng(21)
+    fc = RefCust(U=100, I0=50, H=H, h=0.5 + rngf.random(), rho=1.5 + rngf.random(),
+                 fixed=30 + 20 * rngf.random((H, 3)), unit=0.25 + rngf.random((H, 3)))
+    out["dsirp_c3_float"] = (rate(lambda: [R.expected_cost(fc, d3, threads) for _ in range(nc)],
+                                  nc * m3),
+                             f"{nc} customers x batched_expected_cost, non-dyadic costs")
     return {k: {"value": v, "cores": threads, "kind": "reference", "sample": smp}
             for k, (v, smp) in out.items()}
 
