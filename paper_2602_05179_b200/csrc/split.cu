@@ -815,7 +815,8 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       validate_instance_scalars(inst);
     } else {
       validate_instance(inst);
-      ctx->valid_costs.assign(inst->costs, inst->costs + cells);
+      if (cells <= (size_t{1} << 20)) ctx->valid_costs.assign(inst->costs, inst->costs + cells);
+      else ctx->valid_costs.clear();  // very large matrices: no 8+ MB copy per change
     }
     const int n = inst->n;
     if (!tours || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one tour");
