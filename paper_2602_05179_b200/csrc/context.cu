@@ -8,6 +8,10 @@
 #include <limits>
 #include <mutex>
 
+#include <condition_variable>
+#include <exception>
+#include <thread>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -133,6 +137,112 @@ void* mapped_host_alias(void* host) {
   return at.devicePointer;
 }
 
+}  // namespace scendp_host
+
+// ---- host worker pool ----------------------------------------------------------
+namespace scendp_host {
+namespace {
+struct HostPool {
+  std::mutex use;  // one job at a time
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::vector<std::thread> workers;
+  const std::function<void(int)>* job = nullptr;
+  int parts = 0, next = 1, remaining = 0;
+  uint64_t gen = 0;
+  std::exception_ptr err;
+
+  explicit HostPool(int n) {
+    for (int w = 0; w < n; ++w) workers.emplace_back([this] { loop(); });
+  }
+  void take_parts() {  // with mu held on entry and exit
+    while (job && next < parts) {
+      const int p = next++;
+      const std::function<void(int)>* f = job;
+      mu.unlock();
+      std::exception_ptr e;
+      try {
+        (*f)(p);
+      } catch (...) {
+        e = std::current_exception();
+      }
+      mu.lock();
+      if (e && !err) err = e;
+      if (--remaining == 0) done_cv.notify_all();
+    }
+  }
+  void loop() {
+    std::unique_lock<std::mutex> lk(mu);
+    uint64_t seen = 0;
+    for (;;) {
+      cv.wait(lk, [&] { return gen != seen; });
+      seen = gen;
+      take_parts();
+    }
+  }
+};
+
+HostPool& host_pool() {
+  // leaked on purpose: workers must outlive every static destructor that
+  // could still stage data
+  static HostPool* pool = new HostPool(
+      static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency()))) - 1);
+  return *pool;
+}
+}  // namespace
+
+void parallel_parts(int parts, const std::function<void(int)>& fn) {
+  if (parts <= 1) {
+    if (parts == 1) fn(0);
+    return;
+  }
+  HostPool& pool = host_pool();
+  std::unique_lock<std::mutex> use(pool.use, std::try_to_lock);
+  if (!use.owns_lock() || pool.workers.empty()) {
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> errs(parts);
+    for (int p = 1; p < parts; ++p)
+      th.emplace_back([&, p] {
+        try {
+          fn(p);
+        } catch (...) {
+          errs[p] = std::current_exception();
+        }
+      });
+    try {
+      fn(0);
+    } catch (...) {
+      errs[0] = std::current_exception();
+    }
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    return;
+  }
+  std::exception_ptr first;
+  {
+    std::lock_guard<std::mutex> g(pool.mu);
+    pool.job = &fn;
+    pool.parts = parts;
+    pool.next = 1;
+    pool.remaining = parts - 1;
+    pool.err = nullptr;
+    ++pool.gen;
+  }
+  pool.cv.notify_all();
+  try {
+    fn(0);
+  } catch (...) {
+    first = std::current_exception();
+  }
+  std::unique_lock<std::mutex> lk(pool.mu);
+  pool.take_parts();  // help with whatever is left
+  pool.done_cv.wait(lk, [&] { return pool.remaining == 0; });
+  pool.job = nullptr;
+  if (!first) first = pool.err;
+  lk.unlock();
+  if (first) std::rethrow_exception(first);
+}
 }  // namespace scendp_host
 
 // ---- scendp_ctx members ------------------------------------------------------

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -44,6 +45,13 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CUDA_CHECK(x) ::scendp_host::cuda_check((x), #x)
 
 void set_last_error(const std::string& msg);
+
+// fn(part) for part in [0, parts) on a persistent process-wide pool of host
+// threads (the caller runs part 0 and waits for the rest).  Replaces a
+// thread spawn per staging chunk.  A call made while another call holds the
+// pool runs its parts on freshly spawned threads instead.  Exceptions from
+// parts are rethrown (the first one).
+void parallel_parts(int parts, const std::function<void(int)>& fn);
 
 // Named, growable device scratch buffers owned by a context.
 enum ScratchSlot {

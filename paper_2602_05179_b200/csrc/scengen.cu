@@ -249,8 +249,9 @@ void launch_to_tiled_u8(scendp_ctx* ctx, const uint8_t* src, uint64_t rows, uint
 // any value needs more than 8 bits (the chunk then goes as u32)
 static bool parallel_pack_u8(uint8_t* dst, const uint32_t* src, uint64_t n, int threads) {
   const uint64_t per = ((n + threads - 1) / threads + 4095) & ~uint64_t{4095};
-  std::vector<uint32_t> wide(threads, 0u);
-  auto pack = [&](int t) {
+  const int parts = static_cast<int>(std::max<uint64_t>(1, (n + per - 1) / per));
+  std::vector<uint32_t> wide(parts, 0u);
+  parallel_parts(parts, [&](int t) {
     const uint64_t lo = per * t, hi = std::min(n, per * (t + 1));
     uint32_t acc = 0u;
     for (uint64_t i = lo; i < hi; ++i) {
@@ -259,11 +260,7 @@ static bool parallel_pack_u8(uint8_t* dst, const uint32_t* src, uint64_t n, int 
       dst[i] = static_cast<uint8_t>(v);
     }
     wide[t] = acc >> 8;
-  };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads && per * t < n; ++t) pool.emplace_back(pack, t);
-  pack(0);
-  for (auto& th : pool) th.join();
+  });
   uint32_t any = 0u;
   for (uint32_t w : wide) any |= w;
   return any == 0u;
@@ -272,14 +269,11 @@ static bool parallel_pack_u8(uint8_t* dst, const uint32_t* src, uint64_t n, int 
 // memcpy of `bytes` split over up to `threads` host threads
 static void parallel_copy(char* dst, const char* src, uint64_t bytes, int threads) {
   const uint64_t per = ((bytes + threads - 1) / threads + 4095) & ~uint64_t{4095};
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads && per * t < bytes; ++t)
-    pool.emplace_back([=] {
-      const uint64_t lo = per * t, hi = std::min(bytes, per * (t + 1));
-      std::memcpy(dst + lo, src + lo, hi - lo);
-    });
-  std::memcpy(dst, src, std::min(bytes, per));
-  for (auto& th : pool) th.join();
+  const int parts = static_cast<int>(std::max<uint64_t>(1, (bytes + per - 1) / per));
+  parallel_parts(parts, [&](int t) {
+    const uint64_t lo = per * t, hi = std::min(bytes, per * (t + 1));
+    std::memcpy(dst + lo, src + lo, hi - lo);
+  });
 }
 
 // A pageable host scenario set (the reference's ScenarioBatch vector) into

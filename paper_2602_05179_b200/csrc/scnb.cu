@@ -85,22 +85,10 @@ void read_parallel(int fd, void* dst, uint64_t bytes, uint64_t off, const std::s
       1, std::min<uint64_t>(static_cast<uint64_t>(threads), bytes / kMinPart)));
   if (parts == 1) return read_full(fd, dst, bytes, off, name, what);
   const uint64_t per = ((bytes + parts - 1) / parts + 4095) & ~uint64_t{4095};
-  std::vector<std::thread> pool;
-  std::vector<std::string> errs(parts);
-  for (int p = 0; p < parts; ++p) {
+  parallel_parts(parts, [&](int p) {
     const uint64_t lo = std::min(bytes, per * p), hi = std::min(bytes, per * (p + 1));
-    if (lo >= hi) break;
-    pool.emplace_back([&, p, lo, hi] {
-      try {
-        read_full(fd, static_cast<char*>(dst) + lo, hi - lo, off + lo, name, what);
-      } catch (const Error& e) {
-        errs[p] = e.msg;
-      }
-    });
-  }
-  for (auto& t : pool) t.join();
-  for (const auto& e : errs)
-    if (!e.empty()) fail(SCENDP_ERR_RUNTIME, e);
+    if (lo < hi) read_full(fd, static_cast<char*>(dst) + lo, hi - lo, off + lo, name, what);
+  });
 }
 
 // Read `n` u32 values at file offset `off` and store them narrowed to bytes
@@ -114,33 +102,22 @@ bool read_parallel_u8(int fd, uint8_t* dst, uint64_t n, uint64_t off, const std:
   const int parts = static_cast<int>(std::max<uint64_t>(
       1, std::min<uint64_t>(static_cast<uint64_t>(threads), n / (2ull << 20))));
   const uint64_t per = (n + parts - 1) / parts;
-  std::vector<std::thread> pool;
-  std::vector<std::string> errs(parts);
   std::vector<uint32_t> wide(parts, 0u);
-  auto work = [&](int p) {
+  parallel_parts(parts, [&](int p) {
     const uint64_t lo = std::min(n, per * p), hi = std::min(n, per * (p + 1));
     std::vector<uint32_t> blk(kBlock);
     uint32_t acc = 0u;
-    try {
-      for (uint64_t a = lo; a < hi; a += kBlock) {
-        const uint64_t c = std::min(kBlock, hi - a);
-        read_full(fd, blk.data(), c * 4, off + a * 4, name, what);
-        for (uint64_t i = 0; i < c; ++i) {
-          acc |= blk[i];
-          dst[a + i] = static_cast<uint8_t>(blk[i]);
-        }
-        if (acc >> 8) break;  // wide: the chunk will be re-read as u32
+    for (uint64_t a = lo; a < hi; a += kBlock) {
+      const uint64_t c = std::min(kBlock, hi - a);
+      read_full(fd, blk.data(), c * 4, off + a * 4, name, what);
+      for (uint64_t i = 0; i < c; ++i) {
+        acc |= blk[i];
+        dst[a + i] = static_cast<uint8_t>(blk[i]);
       }
-    } catch (const Error& e) {
-      errs[p] = e.msg;
+      if (acc >> 8) break;  // wide: the chunk will be re-read as u32
     }
     wide[p] = acc >> 8;
-  };
-  for (int p = 1; p < parts; ++p) pool.emplace_back(work, p);
-  work(0);
-  for (auto& t : pool) t.join();
-  for (const auto& e : errs)
-    if (!e.empty()) fail(SCENDP_ERR_RUNTIME, e);
+  });
   for (uint32_t w : wide)
     if (w) return false;
   return true;

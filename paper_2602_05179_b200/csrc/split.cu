@@ -556,19 +556,13 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
   // tours are independent: large K (the SAA candidate sweeps) is split over
   // host threads, each with its own flags, combined after the join
   const unsigned parts = static_cast<unsigned>(std::min<uint64_t>(
-      std::max(1u, std::min(8u, std::thread::hardware_concurrency())),
-      std::max<uint64_t>(1, static_cast<uint64_t>(k) * n1 / 16384)));
+      std::max(1u, std::min(16u, std::thread::hardware_concurrency())),
+      std::max<uint64_t>(1, static_cast<uint64_t>(k) * n1 / 2048)));
   auto for_tours = [&](auto&& body) {
-    if (parts <= 1) {
-      body(0u, k, 0u);
-      return;
-    }
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < parts; ++t)
-      pool.emplace_back([&, t] { body(static_cast<uint32_t>(uint64_t{k} * t / parts),
-                                      static_cast<uint32_t>(uint64_t{k} * (t + 1) / parts), t); });
-    body(0u, static_cast<uint32_t>(k / parts), 0u);
-    for (auto& th : pool) th.join();
+    parallel_parts(static_cast<int>(parts), [&](int t) {
+      body(static_cast<uint32_t>(uint64_t{k} * t / parts),
+           static_cast<uint32_t>(uint64_t{k} * (t + 1) / parts), static_cast<unsigned>(t));
+    });
   };
   // an all-integer matrix makes every prefix integral (a rounded sum of
   // integers is an integer): for many tours one scan of the (n+2)^2 entries
