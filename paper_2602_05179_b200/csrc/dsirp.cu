@@ -28,6 +28,7 @@
 #include <unordered_map>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,9 @@ namespace scendp_dsirp {
 }  // namespace scendp_dsirp
 
 namespace {
+
+constexpr double kInfH = std::numeric_limits<double>::infinity();
+constexpr size_t kFastSmemMax = 48 * 1024;  // fast-form customer tables in shared memory
 
 // ---- host ----------------------------------------------------------------
 void validate_customer(const scendp_customer& s, int H) {
@@ -121,7 +125,9 @@ bool prepare_int(const scendp_customer& s, int H, CustDev& d, std::vector<int32_
   const double sc = std::ldexp(1.0, shift);
   // per (day, quantity): minimal scaled F and the first option attaining it
   const size_t base = ipool.size();
-  ipool.resize(base + static_cast<size_t>(H) * (U + 1), INT32_MAX);
+  // q = 0 (state U: no delivery possible) holds INT32_MIN, read as the
+  // unsigned key 0x80000000 by the fast kernel, above every real key
+  ipool.resize(base + static_cast<size_t>(H) * (U + 1), INT32_MIN);
   double maxF = 0.0;
   for (int t = 0; t < H; ++t)
     for (int q = 1; q <= U; ++q) {
@@ -218,10 +224,12 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     }
     key.push_back(want_int ? 1 : 0);
     bool int_path;
+    bool fast_fp64 = true;  // every customer admits the fast fp64 form
     int maxR = 1;
     if (!ctx->dsirp_key.empty() && ctx->dsirp_key == key) {
       int_path = ctx->dsirp_int_path;
       maxR = ctx->dsirp_maxR;
+      fast_fp64 = ctx->dsirp_fast_fp64;
     } else {
       std::vector<CustDev> cds(nc, CustDev{});
       std::vector<double> pool;
@@ -257,6 +265,25 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
           pool.insert(pool.end(), s.delivery_table, s.delivery_table + static_cast<size_t>(H) * (s.capacity + 1));
         d.off_htable = pool.size();
         if (s.holding_tabular) pool.insert(pool.end(), s.holding_table, s.holding_table + s.capacity + 1);
+        // fast fp64 form: min over r of the reference's rounded F(t, r, q)
+        // (DeliveryCostModel::cost, oudp.hpp:40-45), +inf at q = 0
+        d.off_fmin = pool.size();
+        for (int t = 0; t < H; ++t) {
+          pool.push_back(kInfH);
+          for (int q = 1; q <= s.capacity; ++q) {
+            double best = kInfH;
+            if (s.delivery_tabular) {
+              best = s.delivery_table[static_cast<size_t>(t) * (s.capacity + 1) + q];
+            } else {
+              for (int r = 0; r < s.options; ++r) {
+                const double F = s.fixed[t * s.options + r] + s.unit[t * s.options + r] * static_cast<double>(q);
+                if (F < best) best = F;
+              }
+            }
+            pool.push_back(best);
+          }
+        }
+        fast_fp64 &= std::isfinite(d.rh);
         // exact scaled-integer path when every customer admits it
         if (int_path) int_path = prepare_int(s, H, d, ipool);
       }
@@ -272,6 +299,7 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       ctx->dsirp_key = std::move(key);
       ctx->dsirp_int_path = int_path;
       ctx->dsirp_maxR = maxR;
+      ctx->dsirp_fast_fp64 = fast_fp64;
       ctx->dsirp_o_pool = o_pool;
       ctx->dsirp_o_ipool = o_ipool;
     }
@@ -351,7 +379,13 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       a.end_inventory = d_ei;
       a.route_option = d_ro;
       a.agg = d_agg;
-      if (H <= 8) launch_exact(ctx, a, smem, int_path, full);
+      // fast form (H <= 8) when the customer tables fit in shared memory:
+      // the exact-integer path (cost-only and schedules) and fp64 cost-only
+      const size_t vt = int_path ? 4 : 8;
+      const size_t fast_smem = (static_cast<size_t>(H) + (a.all_std_hold ? 0 : 1)) * (max_u + 1) * vt;
+      const bool fast = H <= 8 && fast_smem <= kFastSmemMax && (int_path || (!full && fast_fp64));
+      if (fast) launch_fast(ctx, a, fast_smem, int_path, full);
+      else if (H <= 8) launch_exact(ctx, a, smem, int_path, full);
       else if (H <= 16) launch_h16(ctx, a, smem, int_path, full);
       else if (H <= 32) launch_h32(ctx, a, smem, int_path, full);
       else launch_long(ctx, a, full, max_u, H);  // the reference's dense pass

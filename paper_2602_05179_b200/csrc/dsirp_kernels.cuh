@@ -26,8 +26,9 @@ struct CustDev {
   int32_t int_ok, shift;
   int32_t h_i, rh_i;       // scaled h and rho*h
   int32_t dlim;            // demands above this leave the exact int32 range
-  uint64_t off_gkey;       // int pool: [H][U+1] packed keys (minF << 8 | r)
+  uint64_t off_gkey;       // int pool: [H][U+1] packed keys (minF << 8 | r), q = 0: INT32_MIN
   uint64_t off_htab_i;     // int pool: [U+1] scaled holding table
+  uint64_t off_fmin;       // pool: [H][U+1] min over r of F(t, r, q), q = 0: +inf
 };
 
 struct DsirpArgs {
@@ -457,6 +458,204 @@ dsirp_int_kernel(DsirpArgs a) {
   agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
 }
 
+// ---------------------------------------------------------------------------
+// K3 fast form (horizons 1..8, launched with HMAX == H): the frontier without
+// liveness bookkeeping.  Slot e (created at the end of day e-1; slot 0 holds
+// I0) keeps one (state, value) pair; every slot is updated every day, so the
+// per-slot work is a fixed, branch-free sequence and all 32 lanes stay busy.
+//
+// Why no slot ever needs to be removed: states are non-decreasing in slot
+// order (a day maps i -> max(0, i-d) monotonically and appends the largest
+// state max(0, U-d)), and two slots reach the same state only by a merge at 0
+// or when the appended state equals a shifted one.  The reference keeps, per
+// state, the first strict minimum over its candidates in ascending predecessor
+// order, no-delivery before delivery (oudp.cpp:56-84).  Here the same
+// candidates sit in adjacent slots in exactly that order and identical states
+// receive identical increments afterwards, so "first minimum in slot order"
+// selects the reference's value (and, FULL, its backpointer path) wherever the
+// frontier is read: the delivery argmin, the terminal pick (oudp.cpp:94-106).
+// A slot the reference would have merged away only ever holds a larger or
+// equal value at an equal state, later in slot order.
+//
+// Per slot and day: delivery candidate = table[t][U - state] + value (one
+// shared-memory lookup; the route-option minimum is folded into the table on
+// the host), then the no-delivery shift.
+//  * INT (exact scaled-integer customers, see dsirp_int_kernel): the table
+//    holds (min_r F << 8 | argmin_r), so the packed key orders (value, option)
+//    and the cost-only minimum is one unsigned min; state U (no delivery
+//    possible) holds 0x80000000, a key no real candidate reaches.  A day
+//    without any delivery candidate, or a demand above dlim, sends the unit
+//    to dsirp_unit_fp64 (the reference's arithmetic), which also serves FULL.
+//  * fp64 (cost-only): table = min over r of the reference's rounded
+//    F(t, r, q) (+inf at q = 0).  Rounding is monotone, so
+//    min_r (v + (F_r + hold1)) = v + (min_r F_r + hold1) bit for bit; the
+//    hold term of the no-delivery step, h*J + (rho h)*s, is h*x for x = i-d
+//    >= 0 and (rho h)*(-x) otherwise (the other product is +0).
+template <int H, bool INT, bool FULL, bool STDHOLD, bool STAB>
+__global__ void __launch_bounds__(kDsirpThreads, 8)
+dsirp_fast_kernel(DsirpArgs a) {
+  static_assert(INT || !FULL, "fp64 schedules run dsirp_kernel");
+  using VT = typename std::conditional<INT, int32_t, double>::type;
+  constexpr int K = H + 1;
+  extern __shared__ __align__(16) char s_dyn[];
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t c = blockIdx.y;
+  const CustDev cd = a.cust[c];
+  const int U = cd.U, U1 = cd.U + 1;
+  const VT* g_del = INT ? reinterpret_cast<const VT*>(a.ipool + cd.off_gkey)
+                        : reinterpret_cast<const VT*>(a.pool + cd.off_fmin);
+  const VT* g_hold = INT ? reinterpret_cast<const VT*>(a.ipool + cd.off_htab_i)
+                         : reinterpret_cast<const VT*>(a.pool + cd.off_htable);
+  const VT* t_del = g_del;
+  const VT* t_hold = g_hold;
+  if constexpr (STAB) {
+    VT* s_del = reinterpret_cast<VT*>(s_dyn);
+    VT* s_hold = s_del + H * U1;
+    for (int x = threadIdx.x; x < H * U1; x += kDsirpThreads) s_del[x] = g_del[x];
+    if (!STDHOLD && cd.hold_tab)
+      for (int x = threadIdx.x; x < U1; x += kDsirpThreads) s_hold[x] = g_hold[x];
+    t_del = s_del;
+    t_hold = s_hold;
+  }
+  agg_cta_init(s_agg);
+  __syncthreads();
+  const int32_t rhI = cd.rh_i, hrI = cd.h_i + cd.rh_i;
+  const double h = cd.h, rh = cd.rh;
+  const double inv_scale = __longlong_as_double(static_cast<long long>(1023 - cd.shift) << 52);
+  // hold(J = j, s = j - x); !STDHOLD: the launch has tabular customers
+  const bool htabular = !STDHOLD && cd.hold_tab != 0;
+  auto hold_of = [&](int x, int j) -> VT {
+    if (htabular) return t_hold[j];
+    if constexpr (INT) return hrI * j - rhI * x;
+    else return __dmul_rn(x >= 0 ? h : rh, static_cast<double>(abs(x)));
+  };
+  for (int rep = 0; rep < kDsirpIntUnits; ++rep) {
+    const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(kDsirpIntUnits) + rep) * kDsirpThreads +
+                        threadIdx.x;
+    const bool active = wl < a.m_wave;
+    const uint64_t w = a.w_base + wl;
+    double total = kInfD;
+    bool ok = false;
+    if (active) {
+      int dem[H];
+      dsirp_load_demands<H>(a, c, wl, H, dem);
+      bool fb = false;  // run the reference-arithmetic unit instead
+      if constexpr (INT) {
+        uint32_t dmax = 0;
+#pragma unroll
+        for (int t = 0; t < H; ++t) dmax = max(dmax, static_cast<uint32_t>(dem[t]));
+        fb = dmax > static_cast<uint32_t>(cd.dlim);
+      }
+      if (!fb) {
+        int st[K];
+        VT vl[K];
+        uint32_t dm[K];
+        int opt[H];
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          st[e] = 0;
+          vl[e] = VT(0);
+          dm[e] = 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < H; ++t) opt[t] = 0;
+        st[0] = cd.I0;
+        uint32_t flag = 0u;
+#pragma unroll
+        for (int t = 0; t < H; ++t) {
+          const int d = dem[t];
+          const int j1 = max(0, U - d);
+          const VT hold1 = hold_of(U - d, j1);
+          const VT* row = t_del + t * U1 + U;  // row[-i]: quantity U - i
+          // (1) delivery: first minimum over (value, option, slot)
+          uint32_t bk = 0xffffffffu;
+          int be = 0;
+          double bv = kInfD;
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            if (e <= t) {
+              const VT g = row[-st[e]];
+              if constexpr (INT) {
+                const uint32_t key = static_cast<uint32_t>(g) + (static_cast<uint32_t>(vl[e]) << 8);
+                if constexpr (FULL) {
+                  if (key < bk) {
+                    bk = key;
+                    be = e;
+                  }
+                } else {
+                  bk = min(bk, key);
+                }
+              } else {
+                const double cand = __dadd_rn(vl[e], __dadd_rn(g, hold1));
+                bv = cand < bv ? cand : bv;
+              }
+            }
+          }
+          // (2) no delivery: every slot shifts by d
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            if (e <= t) {
+              const int x = st[e] - d;
+              const int j = max(x, 0);
+              if constexpr (INT) vl[e] += hold_of(x, j);
+              else vl[e] = __dadd_rn(vl[e], hold_of(x, j));
+              st[e] = j;
+            }
+          }
+          // (3) the delivery target: a new slot with the largest state
+          st[t + 1] = j1;
+          if constexpr (INT) {
+            flag |= bk;
+            vl[t + 1] = static_cast<int32_t>(bk >> 8) + hold1;
+            if constexpr (FULL) {
+              dm[t + 1] = sel_u<K>(dm, be) | (1u << t);
+              opt[t] = static_cast<int>(bk & 0xffu);
+            }
+          } else {
+            vl[t + 1] = bv;
+          }
+        }
+        if (INT && (flag & 0x80000000u)) {
+          fb = true;  // some day offered no delivery candidate at all
+        } else {
+          // pick_terminal: first minimum in slot (= state) order
+          VT tv = vl[0];
+          int ts = 0;
+#pragma unroll
+          for (int e = 1; e < K; ++e) {
+            if constexpr (FULL) {
+              if (vl[e] < tv) {
+                tv = vl[e];
+                ts = e;
+              }
+            } else {
+              tv = vl[e] < tv ? vl[e] : tv;
+            }
+          }
+          if constexpr (INT) {
+            ok = true;
+            total = static_cast<double>(tv) * inv_scale;
+          } else {
+            ok = tv < kInfD;  // all-infinite: the reference's logic_error slot
+            total = ok ? tv : kInfD;
+          }
+          if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
+          if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+          if constexpr (FULL)
+            dsirp_write_schedule<H>(a, c, w, U, cd.I0, H, ok, sel_u<K>(dm, ts), opt, dem);
+        }
+      }
+      if (fb)
+        total = dsirp_unit_fp64<H, FULL>(a, cd, a.pool + cd.off_fixed, a.pool + cd.off_unit, c, w,
+                                         dem, ok);
+    }
+    __syncwarp();
+    agg_warp_add(s_agg, agg_pieces(total, ok), active);
+  }
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
+}
+
 // Launch one HMAX instantiation (fp64 or exact-integer kernel).
 template <typename Kern>
 void launch_kernel(scendp_ctx* ctx, Kern kernel, const DsirpArgs& a, size_t smem, int units = 1) {
@@ -477,6 +676,26 @@ void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, b
 
 // Horizons 1..8: instantiations with HMAX == H (dsirp_exact.cu).
 void launch_exact(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full);
+
+// Fast form for horizons 1..8 (dsirp_fast_a.cu / dsirp_fast_b.cu): INT with
+// or without schedules, fp64 cost-only.  smem = the customer tables.
+template <int H>
+void launch_fast_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
+  auto go = [&](auto kernel) { launch_kernel(ctx, kernel, a, smem, kDsirpIntUnits); };
+  if (int_path) {
+    if (a.all_std_hold) {
+      if (full) go(dsirp_fast_kernel<H, true, true, true, true>);
+      else go(dsirp_fast_kernel<H, true, false, true, true>);
+    } else {
+      if (full) go(dsirp_fast_kernel<H, true, true, false, true>);
+      else go(dsirp_fast_kernel<H, true, false, false, true>);
+    }
+  } else {
+    if (a.all_std_hold) go(dsirp_fast_kernel<H, false, false, true, true>);
+    else go(dsirp_fast_kernel<H, false, false, false, true>);
+  }
+}
+bool launch_fast(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full);
 
 template <int HMAX>
 void launch_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {

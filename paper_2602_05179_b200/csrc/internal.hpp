@@ -148,6 +148,7 @@ struct scendp_ctx {
   std::vector<char> dsirp_key;
   bool dsirp_int_path = false;
   int dsirp_maxR = 1;
+  bool dsirp_fast_fp64 = false;
   size_t dsirp_o_pool = 0, dsirp_o_ipool = 0;  // offsets inside kScrCustomers
   // page-locked staging buffers (SCNB ingestion double buffering)
   void* stage_pinned[2] = {nullptr, nullptr};

@@ -1,13 +1,17 @@
 """Short, fixed workloads for ncu captures (run under gpurun; never a bench).
 
-    python profiles/cases.py <case> [--reps R]
+    python profiles/cases.py <case>[,<case>...] [--reps R]
 
 Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
   c2        split hard n=200, 10^6 scenarios, tiled HBM input, cost-only (K1 int32)
   c2float   the same with non-integral costs (K1 fp64)
   c2full    C2 with full solutions (V, cuts)
   c2gen     C2 with in-kernel generation (the e2e call, batched_split_costs_generated)
+  c2rand    C2 with a random giant tour (the SAA case), integer costs
+  c2randf   the same with non-integral costs (K1 fp64, column gather)
   c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
+  c3float   the non-dyadic C3 twin (K3 fp64 path)
+  c4        DSIRP 200 customers x 10^6 scenarios (one GPU)
   c5        1000 tours x 10^5 scenarios, n=50, penalized beta=10
   k5        dense (min,+) sweep: 6 stages x 3 options x 101x101, 10^5 frontiers
 
@@ -23,22 +27,22 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main():
-    p = argparse.ArgumentParser()
-    p.add_argument("case")
-    p.add_argument("--reps", type=int, default=2)
-    args = p.parse_args()
-    from paper_2602_05179_b200 import (Context, Customer, Distribution, RoutingInstance,
+HBM = 6553.6  # MEASURED_PEAKS.json hbm_gbs (GB/s)
+
+
+def build(ctx, c):
+    """-> (fn, algorithmic bytes per launch or None)"""
+    from paper_2602_05179_b200 import (Customer, Distribution, RoutingInstance,
                                        derive_stream, make_random_instance, pinned_empty)
     from paper_2602_05179_b200 import _capi as A
-
-    ctx = Context(0, timing=True)
-    c = args.case
     if c.startswith("c2"):
         n, m = 200, 1_000_000
         tour = np.arange(1, n + 1, dtype=np.int32)
+        if c.startswith("c2rand"):
+            tour = (np.random.default_rng(7).permutation(n) + 1).astype(np.int32)
         dist = Distribution("uniform", 1, 10, seed=derive_stream(1, 0x5343454E, 0))
-        if c == "c2float":
+        nbytes = m * (4 * n + 8) + (m * 12 * (n + 1) if c == "c2full" else 0)
+        if c in ("c2float", "c2randf"):
             rng = np.random.default_rng(1)
             cc = np.triu(rng.random((n + 2, n + 2)) * 20.0, 1)
             inst = RoutingInstance(n, 100, True, 0.0, cc + cc.T)
@@ -59,16 +63,24 @@ def main():
             fn = lambda: ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m,
                                         full=full, out_kind="device_tiled", device_out=outs,
                                         sync=False)
-    elif c == "c3":
-        nc, m, H = 50, 100_000, 6
-        custs = [Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
-                          fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
-                          unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
+        return fn, nbytes
+    elif c in ("c3", "c4", "c3float"):
+        nc, m, H = (200, 1_000_000, 6) if c == "c4" else (50, 100_000, 6)
+        if c == "c3float":
+            rng = np.random.default_rng(21)
+            custs = [Customer(U=100, I0=50, H=H, h=0.5 + rng.random(), rho=1.5 + rng.random(),
+                              fixed=30 + 20 * rng.random((H, 3)), unit=0.25 + rng.random((H, 3)))
+                     for _ in range(nc)]
+        else:
+            custs = [Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
+                              fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                              unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
         sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m)
         t3 = ctx.alloc(nc * m * 8)
         fn = lambda: ctx.dsirp_eval(custs, (sc, A.MEM_DEVICE_TILED), count=m,
                                     out_kind="device_tiled", device_out={"totals": t3},
                                     sync=False)
+        return fn, nc * m * (4 * H + 8)
     elif c == "c5":
         n5, m5, K5 = 50, 100_000, 1000
         inst5 = make_random_instance(n5, 5, 100, False, 10.0)
@@ -77,6 +89,7 @@ def main():
         scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, m5)
         fn = lambda: ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=m5,
                                     totals=False)
+        return fn, None
     elif c == "k5":
         rng = np.random.default_rng(11)
         stages = []
@@ -87,16 +100,30 @@ def main():
         init = np.full((100_000, 101), np.inf)
         init[np.arange(100_000), rng.integers(0, 101, 100_000)] = 0.0
         fn = lambda: ctx.minplus_sweep(stages, init)
-    else:
-        raise SystemExit(f"unknown case {c}")
-    fn()
-    ctx.sync()
-    ctx.kernel_stats(reset=True)
-    for _ in range(args.reps):
+        return fn, None
+    raise SystemExit(f"unknown case {c}")
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("case")
+    p.add_argument("--reps", type=int, default=2)
+    args = p.parse_args()
+    from paper_2602_05179_b200 import Context
+
+    ctx = Context(0, timing=True)
+    for c in args.case.split(","):
+        fn, nbytes = build(ctx, c)
         fn()
-    ctx.sync()
-    st = ctx.kernel_stats(reset=True)
-    print(f"{c}: {st}")
+        ctx.sync()
+        ctx.kernel_stats(reset=True)
+        for _ in range(args.reps):
+            fn()
+        ctx.sync()
+        st = ctx.kernel_stats(reset=True)
+        k_ms = st["dp_ms"] / max(1, st["dp_launches"])
+        frac = f" frac={nbytes / (k_ms / 1e3) / 1e9 / HBM:.3f}" if nbytes else ""
+        print(f"{c}: kernel_ms={k_ms:.4f}{frac} {st}", flush=True)
     ctx.close()
 
 

@@ -58,6 +58,11 @@ def compare_one(ctx, reference, g, o, dem):
     assert a["finite_count"] == fc
     if mean is not None:
         assert abs(a["mean"] - mean) <= 1e-9 * abs(mean) + 1e-300
+    # cost-only call (the fast form's fp64 table path for non-dyadic models)
+    co = ctx.dsirp_eval([g], dem)
+    np.testing.assert_array_equal(co["totals"][0], tot)
+    np.testing.assert_array_equal(co["evaluated"][0], ev)
+    assert co["agg"] == got["agg"]
     return got
 
 

@@ -34,6 +34,11 @@ def check(ctx, reference, custs, dem, H):
     f64 = ctx.dsirp_eval([c[0] for c in custs], dem, full=True, fp64=True)
     for k in ("totals", "deliver", "quantity", "end_inventory", "route_option"):
         np.testing.assert_array_equal(got[k], f64[k])
+    # cost-only: exact-integer and fp64-table fast forms
+    for fp64 in (False, True):
+        co = ctx.dsirp_eval([c[0] for c in custs], dem, fp64=fp64)
+        np.testing.assert_array_equal(co["totals"], got["totals"])
+        assert co["agg"] == got["agg"]
     for ci, (g, o) in enumerate(custs):
         sl = np.ascontiguousarray(dem[:, ci * H:(ci + 1) * H])
         tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, sl)
