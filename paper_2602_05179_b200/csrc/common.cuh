@@ -172,6 +172,55 @@ __device__ __forceinline__ void agg_warp_add(unsigned long long* cta_acc,
   }
 }
 
+// Per-warp register accumulator for kernels that add many warps of values
+// per CTA: lane L (< kAggSlots) holds word L of the CTA accumulator layout.
+// The common warp -- every lane finite, all digit indices equal -- costs the
+// six reductions and three selects, with no atomics; anything else takes
+// agg_warp_add into the shared accumulator.  Converged warp, all 32 lanes.
+__device__ __forceinline__ void agg_warp_acc(unsigned long long& acc, unsigned long long* cta_acc,
+                                             AggPieces a, bool valid) {
+  const unsigned full = 0xffffffffu;
+  if (!valid) a.kind = 4;
+  int same = 0;
+  __match_all_sync(full, a.kind == 0 ? a.li : -1 - a.kind, &same);
+  if (!same || a.kind != 0) {
+    agg_warp_add(cta_acc, a, valid);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned long long s0 = __reduce_add_sync(full, a.p0 & 0xffffu) +
+                                (static_cast<unsigned long long>(__reduce_add_sync(full, a.p0 >> 16)) << 16);
+  const unsigned long long s1 = __reduce_add_sync(full, a.p1 & 0xffffu) +
+                                (static_cast<unsigned long long>(__reduce_add_sync(full, a.p1 >> 16)) << 16);
+  const unsigned long long s2 = __reduce_add_sync(full, a.p2 & 0xffffu) +
+                                (static_cast<unsigned long long>(__reduce_add_sync(full, a.p2 >> 16)) << 16);
+  const int o = lane - a.li;
+  acc += o == 0 ? s0 : o == 1 ? s1 : o == 2 ? s2 : 0ull;
+  acc += lane == kDigitFinite ? 32ull : 0ull;
+}
+
+// Flush a per-warp register accumulator into the CTA accumulator.
+__device__ __forceinline__ void agg_warp_acc_flush(unsigned long long acc,
+                                                   unsigned long long* cta_acc) {
+  const int lane = threadIdx.x & 31;
+  if (lane < kAggSlots && acc) atomicAdd(cta_acc + lane, acc);
+}
+
+// Add an exact integer sum S * 2^-shift (S < 2^53, 0 <= shift <= 64) and a
+// finite count into the CTA accumulator (one lane).
+__device__ __forceinline__ void agg_cta_add_scaled(unsigned long long* cta_acc, uint64_t S,
+                                                   int shift, uint32_t count) {
+  if (count) atomicAdd(cta_acc + kDigitFinite, static_cast<unsigned long long>(count));
+  if (!S) return;
+  const int pos = 192 - shift;
+  const int li = pos >> 5, sub = pos & 31;
+  const uint32_t lo = static_cast<uint32_t>(S), hi = static_cast<uint32_t>(S >> 32);
+  atomicAdd(cta_acc + li, static_cast<unsigned long long>(lo << sub));
+  atomicAdd(cta_acc + li + 1, static_cast<unsigned long long>(__funnelshift_l(lo, hi, sub)));
+  const uint32_t p2 = sub ? (hi >> (32 - sub)) : 0u;
+  if (p2) atomicAdd(cta_acc + li + 2, static_cast<unsigned long long>(p2));
+}
+
 // CTA epilogue: add the CTA accumulator into the global raw aggregate of one
 // candidate (scendp_agg_raw layout: 12 digits, finite, infeasible, error,
 // range).  Integer atomics: associative, hence deterministic.

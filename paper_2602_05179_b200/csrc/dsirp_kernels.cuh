@@ -519,16 +519,21 @@ dsirp_fast_kernel(DsirpArgs a) {
   }
   agg_cta_init(s_agg);
   __syncthreads();
-  const int32_t rhI = cd.rh_i, hrI = cd.h_i + cd.rh_i;
+  const int32_t nrhI = -cd.rh_i, hrI = cd.h_i + cd.rh_i;
   const double h = cd.h, rh = cd.rh;
   const double inv_scale = __longlong_as_double(static_cast<long long>(1023 - cd.shift) << 52);
   // hold(J = j, s = j - x); !STDHOLD: the launch has tabular customers
   const bool htabular = !STDHOLD && cd.hold_tab != 0;
   auto hold_of = [&](int x, int j) -> VT {
     if (htabular) return t_hold[j];
-    if constexpr (INT) return hrI * j - rhI * x;
+    if constexpr (INT) return hrI * j + nrhI * x;
     else return __dmul_rn(x >= 0 ? h : rh, static_cast<double>(abs(x)));
   };
+  // aggregates: INT sums the scaled integer totals per thread (one exact
+  // add per CTA and warp at the end); fp64 keeps a per-warp register
+  // accumulator.  Units run by dsirp_unit_fp64 go through agg_warp_add.
+  uint32_t isum = 0u, icnt = 0u;  // < 4 units x 2^22 per thread
+  unsigned long long wacc = 0ull;
   for (int rep = 0; rep < kDsirpIntUnits; ++rep) {
     const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(kDsirpIntUnits) + rep) * kDsirpThreads +
                         threadIdx.x;
@@ -536,10 +541,10 @@ dsirp_fast_kernel(DsirpArgs a) {
     const uint64_t w = a.w_base + wl;
     double total = kInfD;
     bool ok = false;
+    bool fb = false;  // run the reference-arithmetic unit instead
     if (active) {
       int dem[H];
       dsirp_load_demands<H>(a, c, wl, H, dem);
-      bool fb = false;  // run the reference-arithmetic unit instead
       if constexpr (INT) {
         uint32_t dmax = 0;
 #pragma unroll
@@ -635,6 +640,8 @@ dsirp_fast_kernel(DsirpArgs a) {
           if constexpr (INT) {
             ok = true;
             total = static_cast<double>(tv) * inv_scale;
+            isum += static_cast<uint32_t>(tv);
+            icnt += 1u;
           } else {
             ok = tv < kInfD;  // all-infinite: the reference's logic_error slot
             total = ok ? tv : kInfD;
@@ -650,7 +657,18 @@ dsirp_fast_kernel(DsirpArgs a) {
                                          dem, ok);
     }
     __syncwarp();
-    agg_warp_add(s_agg, agg_pieces(total, ok), active);
+    if constexpr (INT) {
+      if (__any_sync(0xffffffffu, fb)) agg_warp_add(s_agg, agg_pieces(total, ok), fb);
+    } else {
+      agg_warp_acc(wacc, s_agg, agg_pieces(total, ok), active);
+    }
+  }
+  if constexpr (INT) {
+    const uint32_t S = __reduce_add_sync(0xffffffffu, isum);  // < 2^29
+    const uint32_t n = __reduce_add_sync(0xffffffffu, icnt);
+    if ((threadIdx.x & 31) == 0) agg_cta_add_scaled(s_agg, S, cd.shift, n);
+  } else {
+    agg_warp_acc_flush(wacc, s_agg);
   }
   __syncthreads();
   agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(c) * kAggWords);
