@@ -260,6 +260,7 @@ void* scendp_ctx::scratch_get(int slot, uint64_t bytes) {
   const uint64_t want = (bytes + (bytes >> 3) + 4095) & ~uint64_t{4095};
   CUDA_CHECK(cudaMalloc(&scratch[slot], want));
   scratch_bytes[slot] = want;
+  ++scratch_gen[slot];
   return scratch[slot];
 }
 

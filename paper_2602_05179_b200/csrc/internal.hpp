@@ -79,13 +79,16 @@ struct NcclApi;
 struct scendp_ctx {
   int device = 0;
   int sm_count = 0;
-  // split overflow bitmap: scratch base it lives at, bytes known all-zero
-  void* ovf_base = nullptr;
+  // split overflow bitmap: allocation generation it lives in, bytes known
+  // all-zero (reset on reallocation -- a new block may reuse the address --
+  // and while a call that may set bits is in flight)
+  uint64_t ovf_gen = ~uint64_t{0};
   uint64_t ovf_clean = 0;
   cudaStream_t stream = nullptr;
   scendp_opts opts{};
   void* scratch[scendp_host::kScrCount] = {};
   uint64_t scratch_bytes[scendp_host::kScrCount] = {};
+  uint64_t scratch_gen[scendp_host::kScrCount] = {};  // bumped on every (re)allocation
   void* agg_pinned = nullptr;       // pinned staging for raw aggregates
   uint64_t agg_pinned_bytes = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;

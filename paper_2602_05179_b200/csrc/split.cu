@@ -927,13 +927,16 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
         std::min<uint64_t>(std::max<uint64_t>(wave_items / 128, 1u << 16), 1u << 26));
     const uint64_t bits_bytes = (((wave_items + 31) / 32) * 4 + 15) & ~uint64_t{15};
     char* ovf = static_cast<char*>(ctx->scratch_get(kScrHandoff, bits_bytes + ovf_cap * 8ull));
-    if (ovf != ctx->ovf_base) {
-      ctx->ovf_base = ovf;
+    if (ctx->scratch_gen[kScrHandoff] != ctx->ovf_gen) {
+      ctx->ovf_gen = ctx->scratch_gen[kScrHandoff];
       ctx->ovf_clean = 0;
     }
     if (ctx->ovf_clean < bits_bytes)
       CUDA_CHECK(cudaMemsetAsync(ovf + ctx->ovf_clean, 0, bits_bytes - ctx->ovf_clean, ctx->stream));
-    ctx->ovf_clean = bits_bytes;
+    // dirty until this call's hand-off passes are enqueued: an error exit in
+    // between leaves the bitmap to be cleared by the next call
+    ctx->ovf_clean = 0;
+    const uint64_t ovf_clean_after = bits_bytes;
     auto* d_ovf_bits = reinterpret_cast<uint32_t*>(ovf);
     auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + bits_bytes);
     // generic path: latency-bound (dependent global-scratch accesses), so as
@@ -1049,6 +1052,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
         h_aggc = nullptr;  // aggregates changed: read them again below
       }
     }
+    ctx->ovf_clean = ovf_clean_after;  // every hand-off pass is enqueued
     // the single collective: per-candidate raw aggregates, K x 16 u64
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(k) * kAggWords);
 

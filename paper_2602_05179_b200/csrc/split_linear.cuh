@@ -94,6 +94,21 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
   // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96); the
   // evicted slot becomes the -inf sentinel below the new head
   if constexpr (SAFE) {
+    if (d > Qc) {
+      // every route into i carries d_i > Q: the window empties.  Decided on
+      // d itself -- the u32 difference load - front_l wraps once d_i >=
+      // 2^32 - Q (loads are int64 in the reference, split.cpp:93); with
+      // d_i <= Q every window difference is < 2Q < 2^32 and exact mod 2^32
+      ring_at(rf, s.tail - kStep) = k1_neg_inf<VT>();
+      s.head = s.tail;
+      s.back_f = k1_neg_inf<VT>();
+      s.front_f = k1_inf<VT>();
+      s.front_l = s.load;
+      if (FULL) {
+        s.front_i = -1;
+        s.front_rc = -1;
+      }
+    }
     while (s.load - s.front_l > Qc) {
       ring_at(rf, s.head) = k1_neg_inf<VT>();
       s.head += kStep;

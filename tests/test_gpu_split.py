@@ -361,3 +361,32 @@ def test_pageable_upload_narrow_and_wide_chunks(ctx, oracle):
         got = ctx.split_eval(inst, tour, dem)
         want = oracle.split_batch(n, Q, 1, 0.0, inst.costs, tour, dem)
         np.testing.assert_array_equal(got["totals"][0], want)
+
+
+@pytest.mark.parametrize("Q", [100, 1 << 30, (1 << 31) - 1])
+@pytest.mark.parametrize("costs", ["int", "float"])
+def test_hard_demands_near_u32_max(ctx, oracle, reference, Q, costs):
+    """Demands up to 2^32-1 are legal (u32 batches, DistributionSpec lo >= 0).
+    A demand d_i >= 2^32 - Q must empty the window even though the u32 load
+    difference wraps (the reference's loads are int64, split.cpp:93), and
+    loads that wrap u32 with d_i <= Q keep exact window differences."""
+    n, m = 40, 640
+    rng = np.random.default_rng(Q % 1000 + (costs == "int"))
+    dem = rng.integers(0, min(Q, 12) + 1, size=(m, n)).astype(np.uint32)
+    big = rng.random((m, n)) < 0.05
+    dem[big] = np.uint32(0xFFFFFFF0)
+    dem[::9, 5] = np.uint32(0xFFFFFFFF)
+    if Q >= (1 << 30):
+        dem[1::3] = rng.integers(Q // 2, Q + 1, size=(len(dem[1::3]), n)).astype(np.uint32)
+    inst = (RoutingInstance(n, Q, True, 0.0, oracle.make_random_instance(n, 4)) if costs == "int"
+            else float_instance(n, Q, 9))
+    for tour in (np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 5)):
+        got = ctx.split_eval(inst, tour, dem, full=True)
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+            n, Q, 1, 0.0, inst.costs, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        co = ctx.split_eval(inst, tour, dem)
+        np.testing.assert_array_equal(co["totals"][0], tot)
+        assert co["agg"][0]["finite_count"] == fc and co["agg"][0]["infeasible_count"] == ic
