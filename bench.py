@@ -3,34 +3,48 @@
 
 Headline (BASELINE.json configs[1], "C2"): CVRPSD split, n=200, Q=100, hard
 capacities, identity giant tour, make_random_instance(200, seed=1) costs,
-uniform:1:10 demands (the reference default), 10^6 scenarios per GPU
-(weak scaling: rank r owns scenario indices [r*10^6, (r+1)*10^6)).
+uniform:1:10 demands (the reference default), 10^6 scenarios in total,
+STRONG-sharded over the N GPUs: rank g owns the contiguous scenario range
+[g*m/N, (g+1)*m/N), generated on its own device with the
+reference's streams, so every shard is bit-identical to the 1-GPU run.
 
-  value  one step = one scendp_split_eval over the HBM-resident (tiled)
-         scenario set: K1 DP kernel + overflow pass (+ the NCCL all-reduce of
-         the aggregate when N > 1); device-timed with CUDA events, max over
-         ranks.  Inputs (800 MB) exceed the 126 MB L2, so no flush.
+  value  one step = one scendp_split_eval per rank over its HBM-resident
+         (tiled) shard: K1 DP kernel (+ hand-off pass) + the NCCL all-reduce
+         of the 128-byte exact aggregate when N > 1 (overlapped with the next
+         step's kernel; the timer ends after the last one); device-timed with
+         CUDA events, max over ranks.  Inputs (800 MB) exceed the 126 MB L2,
+         so no flush.
   e2e    the reference's own benchmark call, batched_split_costs_generated
-         (saa.cpp:366-375), through the C-ABI: per step the host->device copy
-         of the step's inputs (instance/tour tables; the scenarios are the
-         distribution spec) and the device->host read of all 10^6 per-scenario
-         totals into pinned memory.  `e2e_host_batch` is the same metric with a
-         materialized host ScenarioBatch (800 MB pinned H2D per step).
+         (saa.cpp:366-375), through the C-ABI with host buffers, as an SAA
+         caller makes it: every step evaluates a DIFFERENT (instance, giant
+         tour) pair -- 4 cost matrices x 8 random tours, cycled -- so each step
+         validates its cost matrix, builds its tour tables in pinned memory and
+         copies them host->device (nothing is cached across steps), generates
+         its shard's demands in-kernel, and reads all per-scenario totals and
+         the aggregate back to host memory.  `e2e_host_batch` is the same
+         metric with a materialized host ScenarioBatch (800 MB of pinned
+         demands H2D per step, batched_split_costs).
   --impl reference  the reference's own CPU implementation (oracle/_ref,
          compiled from /root/reference sources) running the same call with all
-         host threads.
+         host threads (rank 0 only under torchrun).
 
-Secondary lines (DSIRP C3/C4 and the non-dyadic C3 twin, SAA C5 candidate sweep, penalized and
-float-cost split, full solutions, K5 min-plus, SCNB ingestion) ride in the
-same JSON object under "secondary"; at N = 1 each split/DSIRP line carries
-"cpu_reference", the reference's own evaluator (oracle/_ref) on a bounded
-sample of that workload with all host threads.
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (one process per GPU; fails loudly when fewer than N GPUs are
+visible).  NCCL's INIT lines (nRanks) go to stderr.
+
+Secondary lines (weak-scaled C2, random-tour C2 int/fp64, float-cost and
+full-solution C2, penalized C2, SAA C5 candidate sweep, DSIRP C3/C4 and the
+non-dyadic C3 twin, K5 min-plus, SCNB ingestion) ride in the same JSON object
+under "secondary"; at N = 1 each split/DSIRP line carries "cpu_reference",
+the reference's own evaluator (oracle/_ref) on a bounded sample of that
+workload with all host threads.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,6 +59,7 @@ METRIC = "scenario DP evals/sec (split & DSIRP, 10^6 scen) at 1/2/4/8 B200 vs ho
 UNIT = "scenario-evals/s"
 N_C2, Q_C2, M_C2 = 200, 100, 1_000_000
 TAG_SCENARIO = 0x5343454E
+DRY = os.environ.get("SCENDP_BENCH_DRY_RUN") == "1"  # launcher test without a GPU
 
 
 def parse():
@@ -53,10 +68,41 @@ def parse():
     p.add_argument("--steps", type=int, default=4000)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--scenarios", type=int, default=M_C2, help="scenarios per GPU")
+    p.add_argument("--scenarios", type=int, default=M_C2, help="scenarios in total (C2)")
     p.add_argument("--no-secondary", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
+
+
+def shard(m: int, rank: int, world: int):
+    """[g*m/G, (g+1)*m/G): contiguous scenario range of rank g."""
+    return m * rank // world, m * (rank + 1) // world
+
+
+# ---- launcher ------------------------------------------------------------------
+def visible_gpus() -> int:
+    import torch
+    return torch.cuda.device_count()
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args) -> int:
+    """Re-run this script under torch.distributed.run with args.gpus ranks."""
+    if not DRY and args.impl == "ours":  # the reference arm uses no GPU
+        n = visible_gpus()
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}",
+                  file=sys.stderr, flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 # ---- distributed plumbing (gloo: barrier, id broadcast, max over ranks) -------
@@ -171,6 +217,24 @@ def ncu_traffic(name: str):
         return None
 
 
+def workload_config(args, world):
+    return {"workload": "C2: CVRPSD split n=200 Q=100 hard, identity giant tour, "
+                        "make_random_instance(200, seed=1), uniform:1:10 demands, "
+                        f"{args.scenarios} scenarios in total",
+            "n": N_C2, "Q": Q_C2, "scenarios": args.scenarios, "tours": 1,
+            "mode": "hard (linear deque)",
+            "parallelism": f"scenario shards x{world}: rank g owns [g*m/{world}, (g+1)*m/{world})",
+            "l2": "inputs (4n B/scenario = 800 MB) exceed the 126 MB L2; no flush"}
+
+
+def base_line(args, world, value, ms_step, scaling, dtype):
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic (seeded generator, bit-identical to the reference's)",
+            "config": workload_config(args, world)}
+
+
 # ---- reference (CPU) arm -------------------------------------------------------
 def reference_rate(m: int, threads: int, reps: int, warmup: int, budget_s: float = 60.0):
     from oracle import UNIFORM, Reference
@@ -207,155 +271,163 @@ def run_reference(args, d: Dist):
     if args.steps * m / probe > 60.0:
         m = max(10_000, int(60.0 * probe / max(1, args.steps)))
     rate, done = reference_rate(m, threads, args.steps, min(args.warmup, 3))
-    line = {
-        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
-        "warmup": args.warmup, "ms_per_step": m / rate * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": workload_config(args),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"batched_split_costs_generated, {m} scenarios per step, "
-                                   f"{threads} threads (BackendConfig::multi_thread)"},
-        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    line = base_line(args, d.world, rate, m / rate * 1e3, "strong", "f64")
+    line["steps"] = done
+    line["impl"] = "reference"
+    line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"batched_split_costs_generated, {m} scenarios per step, "
+                                      f"{threads} threads (BackendConfig::multi_thread)"}
+    line["e2e"] = {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
-
-
-def workload_config(args):
-    return {"workload": "C2: CVRPSD split n=200 Q=100 hard, identity giant tour, "
-                        "make_random_instance(200, seed=1), uniform:1:10 demands, "
-                        f"{args.scenarios} scenarios per GPU",
-            "n": N_C2, "Q": Q_C2, "scenarios_per_gpu": args.scenarios, "tours": 1,
-            "mode": "hard (linear deque)", "parallelism": f"scenario shards x{args.gpus}",
-            "l2": "inputs (4n B/scenario = 800 MB) exceed the 126 MB L2; no flush"}
 
 
 # ---- our arm -------------------------------------------------------------------
 def timed(ctx, d: Dist, fn, steps: int, warmup: int):
-    for _ in range(warmup):
-        fn()
+    """W untimed steps, then K steps between barrier + device sync on both
+    sides, CUDA events on the library stream; returns (max over ranks, local,
+    kernel stats of the timed region)."""
+    for i in range(warmup):
+        fn(i)
     ctx.sync()
     ctx.kernel_stats(reset=True)
     d.barrier()
     ctx.sync()
     ctx.timer_start()
-    for _ in range(steps):
-        fn()
-    ms = ctx.timer_stop()  # synchronizes
+    for i in range(steps):
+        fn(warmup + i)
+    ms = ctx.timer_stop()  # synchronizes (and waits for the last all-reduce)
     st = ctx.kernel_stats(reset=True)
     d.barrier()
     return d.max(ms), ms, st
 
 
+def run_dry(args, d: Dist):
+    """SCENDP_BENCH_DRY_RUN=1: the launcher / rank plumbing without a GPU
+    (tests/test_bench_launcher.py): barrier, max over ranks, one line."""
+    lo, hi = shard(args.scenarios, d.rank, d.world)
+    d.barrier()
+    ms = d.max(1.0 + 0.5 * d.rank)
+    total = d.max(float(hi - lo)) * d.world  # equal shards in the test
+    line = base_line(args, d.world, args.scenarios / (ms / 1e3), ms, "strong", "f64")
+    line["dry_run"] = {"shard": [lo, hi], "sum_of_shards_le": total}
+    if d.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args, d: Dist):
-    from paper_2602_05179_b200 import (Context, Customer, Distribution, RoutingInstance,
-                                       derive_stream, make_random_instance, pinned_empty)
+    from paper_2602_05179_b200 import (Context, Distribution, derive_stream,
+                                       make_random_instance, pinned_empty)
     from paper_2602_05179_b200 import _capi as A
+    import ctypes
     ctx = Context(d.local_rank, timing=True)
     if d.world > 1:
         uid = d.bcast_bytes(Context.nccl_unique_id() if d.rank == 0 else b"")
         ctx.comm_init_rank(uid, d.world, d.rank)
     hbm_peak, peak_src = peaks()
-    m = args.scenarios
     n = N_C2
-    w0 = d.rank * m
+    lo, hi = shard(args.scenarios, d.rank, d.world)
+    m = hi - lo
     inst = make_random_instance(n, 1, Q_C2, True)
     tour = np.arange(1, n + 1, dtype=np.int32)
     dist = Distribution("uniform", 1, 10, seed=derive_stream(1, TAG_SCENARIO, 0))
-    scen = ctx.gen_scenarios(dist, n, m, w0=w0)          # HBM-resident, tiled
+    scen = ctx.gen_scenarios(dist, n, m, w0=lo)          # HBM-resident, tiled
     tot = ctx.alloc(m * 8)
 
-    def step():
-        ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m,
-                       out_kind="device_tiled", device_out={"totals": tot}, sync=False)
+    call = ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m, first_index=lo,
+                          out_kind="device_tiled", device_out={"totals": tot}, sync=False,
+                          prepare=True)  # the C-ABI call, argument structs built once
+
+    def step(_):
+        call()
 
     clocks = Clocks(d.local_rank)
     clocks.start()
     ms_max, ms_local, st = timed(ctx, d, step, args.steps, args.warmup)
     clk = clocks.stop()
     ms_step = ms_max / args.steps
-    value = d.world * m / (ms_step / 1e3)
+    value = args.scenarios / (ms_step / 1e3)
     k_ms = st["dp_ms"] / max(1, st["dp_launches"])
     bytes_per_launch = m * (4 * n + 8)
     achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
-    # correctness spot check of the timed path against the exact aggregate
-    chk = ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m, totals=False)
+    # the timed path's aggregate, all-reduced over the ranks (exact)
+    chk = ctx.split_eval(inst, tour, (scen, A.MEM_DEVICE_TILED), count=m, first_index=lo,
+                         totals=False)
 
-    # ---- e2e: reference-facing call with host buffers ------------------------
-    host_tot = pinned_empty(m, np.float64)
-    # the C-ABI call as a C/C++ caller makes it: argument structs built once,
-    # generated scenarios, per-scenario totals into host (pinned) memory and
-    # the aggregate read back -- synchronous, like batched_split_costs_generated
-    import ctypes
-    c_inst, c_dist = inst.as_c(), dist.as_c()
-    c_sc = A.Scenarios(A.MEM_GENERATED, None, n, m, w0, ctypes.pointer(c_dist))
+    # ---- e2e: reference-facing call with host buffers, new inputs each step --
+    host_tot = pinned_empty(max(1, m), np.float64)
+    insts = [make_random_instance(n, s, Q_C2, True) for s in (1, 2, 3, 4)]
+    rng = np.random.default_rng(17)
+    tours = [(rng.permutation(n) + 1).astype(np.int32) for _ in range(8)]
+    c_insts = [x.as_c() for x in insts]
+    c_dist = dist.as_c()
+    c_sc = A.Scenarios(A.MEM_GENERATED, None, n, m, lo, ctypes.pointer(c_dist))
     c_agg = (A.Agg * 1)()
     c_out = A.SplitOut(A.MEM_HOST, host_tot.ctypes.data, None, None, None, None, c_agg, None)
 
-    def e2e_step():
-        A.check(ctx.lib.scendp_split_eval(ctx.handle, ctypes.byref(c_inst), tour.ctypes.data, 1,
-                                          ctypes.byref(c_sc), 0, ctypes.byref(c_out)))
+    def e2e_step(i):
+        A.check(ctx.lib.scendp_split_eval(ctx.handle, ctypes.byref(c_insts[i % 4]),
+                                          tours[i % 8].ctypes.data, 1, ctypes.byref(c_sc), 0,
+                                          ctypes.byref(c_out)))
 
-    e2e_steps = max(3, min(args.steps, 200))
-    e_ms_max, _, est = timed(ctx, d, e2e_step, e2e_steps, 2)
-    e2e_value = d.world * m / (e_ms_max / e2e_steps / 1e3)
-    e2e = {"value": e2e_value, "unit": UNIT,
+    e2e_steps = max(8, min(args.steps, 400))
+    e_ms_max, _, est = timed(ctx, d, e2e_step, e2e_steps, max(3, args.warmup))
+    e2e = {"value": args.scenarios / (e_ms_max / e2e_steps / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": est["h2d_bytes"] // e2e_steps,
            "d2h_bytes_per_step": est["d2h_bytes"] // e2e_steps,
-           "call": "scendp_split_eval(GENERATED uniform:1:10, host totals) == "
-                   "batched_split_costs_generated"}
-    # materialized host ScenarioBatch (reference layout, pinned)
-    ref_layout = ctx.gen_scenarios(dist, n, m, w0=w0, tiled=False)
+           "steps": e2e_steps,
+           "call": "scendp_split_eval(GENERATED uniform:1:10 shard, host totals) == "
+                   "batched_split_costs_generated; a different (instance, random giant tour) "
+                   "each step: validation, tour tables built and copied H2D every step",
+           "gpu_launches": est["launches"]}
+    # materialized host ScenarioBatch (reference layout, pinned) of this shard
+    ref_layout = ctx.gen_scenarios(dist, n, m, w0=lo, tiled=False)
     host_batch = pinned_empty(m * n, np.uint32)
     A.check(ctx.lib.scendp_memcpy(ctx.handle, host_batch.ctypes.data, ref_layout.ptr,
                                   m * n * 4, 1, 0))
     ref_layout.free()
     hb = host_batch.reshape(m, n)
 
-    def host_step():
-        ctx.split_eval(inst, tour, hb, host_totals=host_tot)
+    def host_step(i):
+        ctx.split_eval(insts[i % 4], tours[i % 8], hb, host_totals=host_tot, first_index=lo)
 
     h_steps = max(3, min(args.steps, 20))
     h_ms_max, _, hst = timed(ctx, d, host_step, h_steps, 1)
-    e2e_host = {"value": d.world * m / (h_ms_max / h_steps / 1e3), "unit": UNIT,
+    e2e_host = {"value": args.scenarios / (h_ms_max / h_steps / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": hst["h2d_bytes"] // h_steps,
                 "d2h_bytes_per_step": hst["d2h_bytes"] // h_steps,
-                "call": "scendp_split_eval(HOST ScenarioBatch) == batched_split_costs"}
-    # the same from pageable memory (what a std::vector ScenarioBatch is):
-    # chunked multi-threaded staging into pinned buffers, overlapped with H2D
+                "call": "scendp_split_eval(HOST pinned ScenarioBatch shard) == batched_split_costs"}
     pageable = np.array(hb, copy=True)
-    p_ms_max, _, pst = timed(ctx, d, lambda: ctx.split_eval(inst, tour, pageable,
-                                                            host_totals=host_tot), h_steps, 1)
-    e2e_host_pageable = {"value": d.world * m / (p_ms_max / h_steps / 1e3), "unit": UNIT,
+    p_ms_max, _, pst = timed(ctx, d, lambda i: ctx.split_eval(
+        insts[i % 4], tours[i % 8], pageable, host_totals=host_tot, first_index=lo), h_steps, 1)
+    e2e_host_pageable = {"value": args.scenarios / (p_ms_max / h_steps / 1e3), "unit": UNIT,
                          "h2d_bytes_per_step": pst["h2d_bytes"] // h_steps,
                          "d2h_bytes_per_step": pst["d2h_bytes"] // h_steps,
-                         "call": "scendp_split_eval(HOST pageable ScenarioBatch)"}
+                         "call": "scendp_split_eval(HOST pageable ScenarioBatch shard)"}
     del pageable
-    scen_tot_check = float(np.sum(host_tot))  # keep the D2H result live
+    scen_tot_check = float(np.sum(host_tot[:m]))  # keep the D2H result live
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64 (exact int32 path: integral costs, bit-identical to fp64)",
-        "data": "synthetic (seeded generator, bit-identical to the reference's)",
-        "config": workload_config(args),
+    line = base_line(args, d.world, value, ms_step, "strong",
+                     "f64 (exact int32 path: integral costs, bit-identical to fp64)")
+    line.update({
         "gpu_launches": st["launches"],
         "kernel_ms": k_ms,
         "bellman_state_updates_per_s": value * n,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic("split_linear_c2"),
-                     "kernel": "split_linear_kernel<cost-only, tiled, int32>",
+                     "kernel": "split_linear_kernel<cost-only, tiled, int32, identity tour>",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "unit_bytes": "4n+8 per scenario (demand column read once, total written once)",
                      "peak_source": peak_src},
         "clocks": clk,
         "e2e": e2e,
         "e2e_host_batch": e2e_host,
         "e2e_host_batch_pageable": e2e_host_pageable,
         "check": {"mean_cost": chk["agg"][0]["mean"], "finite": chk["agg"][0]["finite_count"],
-                  "host_totals_sum": scen_tot_check},
-    }
-    if d.world == 1 and not args.no_cpu_baseline:
+                  "host_totals_sum_rank0": scen_tot_check},
+    })
+    scen.free()
+    tot.free()
+    if d.world == 1 and not args.no_cpu_baseline and d.rank == 0:
         line["cpu_baseline"] = cpu_baseline()
     if not args.no_secondary:
         line["secondary"] = secondary(ctx, d, args)
@@ -367,12 +439,11 @@ def run_ours(args, d: Dist):
                         line["secondary"][k]["cpu_reference"] = v
             except Exception as e:  # reference library missing on this box
                 line["secondary_cpu_reference"] = f"unavailable: {e}"
-
+    if d.world > 1:
+        ctx.comm_destroy()
+    ctx.close()
     if d.rank == 0:
         print(json.dumps(line), flush=True)
-    scen.free()
-    tot.free()
-    ctx.close()
 
 
 def cpu_baseline():
@@ -394,76 +465,139 @@ def secondary(ctx, d: Dist, args):
     from paper_2602_05179_b200 import _capi as A
     out = {}
     hbm_peak, _ = peaks()
-    n = N_C2
+    n, G, g = N_C2, d.world, d.rank
 
     def kernel_rate(fn, steps, warm=2):
-        ms_max, ms, st = timed(ctx, d, fn, steps, warm)
+        """fn: a prepared C-ABI call (argument structs built once) or any callable"""
+        ms_max, ms, st = timed(ctx, d, lambda i: fn(), steps, warm)
         return ms_max / steps, st["dp_ms"] / max(1, st["dp_launches"])
 
-    # float-cost twin of C2 (pure fp64 path) and full solutions
-    m = min(args.scenarios, 1_000_000)
+    def frac(nbytes, k_ms):
+        return nbytes / (k_ms / 1e3) / 1e9 / hbm_peak
+
+    # C2 weak-scaled: 10^6 scenarios per GPU (rank g owns [g*10^6, (g+1)*10^6))
+    mw = M_C2
+    distw = Distribution("uniform", 1, 10, seed=0x5eed)
+    scen = ctx.gen_scenarios(distw, n, mw, w0=g * mw)
+    tot = ctx.alloc(mw * 8)
+    iinst = make_random_instance(n, 1, Q_C2, True)
+    ident = np.arange(1, n + 1, dtype=np.int32)
+    step_ms, k_ms = kernel_rate(ctx.split_eval(
+        iinst, ident, (scen, A.MEM_DEVICE_TILED), count=mw, first_index=g * mw,
+        out_kind="device_tiled", device_out={"totals": tot}, sync=False, prepare=True), 50)
+    out["split_c2_weak"] = {"value": G * mw / (step_ms / 1e3), "unit": UNIT, "kernel_ms": k_ms,
+                            "scaling": "weak", "scenarios_per_gpu": mw,
+                            "roofline_frac": frac(mw * (4 * n + 8), k_ms)}
+
+    # strong shards of the 10^6-scenario sets below
+    lo, hi = shard(M_C2, g, G)
+    m = hi - lo
     dist = Distribution("uniform", 1, 10, seed=77)
-    scen = ctx.gen_scenarios(dist, n, m, w0=d.rank * m)
-    tot = ctx.alloc(m * 8)
+    scen2 = ctx.gen_scenarios(dist, n, m, w0=lo)
     rng = np.random.default_rng(1)
     c = rng.random((n + 2, n + 2)) * 20.0
     c = np.triu(c, 1)
     c = c + c.T
     finst = RoutingInstance(n, Q_C2, True, 0.0, c)
-    tour = np.arange(1, n + 1, dtype=np.int32)
-    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
-        finst, tour, (scen, A.MEM_DEVICE_TILED), count=m, out_kind="device_tiled",
-        device_out={"totals": tot}, sync=False), 50)
-    out["split_c2_float_costs"] = {"value": d.world * m / (step_ms / 1e3), "unit": UNIT,
-                                   "kernel_ms": k_ms, "dtype": "f64",
-                                   "roofline_frac": m * (4 * n + 8) / (k_ms / 1e3) / 1e9 / hbm_peak}
-    iinst = make_random_instance(n, 1, Q_C2, True)
+    rtour = (np.random.default_rng(7).permutation(n) + 1).astype(np.int32)
+    for name, inst_, tour_ in (("split_c2_float_costs", finst, ident),
+                               ("split_c2_random_tour", iinst, rtour),
+                               ("split_c2_random_tour_float", finst, rtour)):
+        step_ms, k_ms = kernel_rate(ctx.split_eval(
+            inst_, tour_, (scen2, A.MEM_DEVICE_TILED), count=m, first_index=lo,
+            out_kind="device_tiled", device_out={"totals": tot}, sync=False, prepare=True), 50)
+        out[name] = {"value": M_C2 / (step_ms / 1e3), "unit": UNIT, "kernel_ms": k_ms,
+                     "dtype": "f64" if inst_ is finst else "int32-exact",
+                     "tour": "identity" if tour_ is ident else "random permutation (SAA case)",
+                     "roofline_frac": frac(m * (4 * n + 8), k_ms), "scaling": "strong"}
     V = ctx.alloc(ctx.tiled_bytes(n + 1, m) * 2)
     cuts = ctx.alloc(ctx.tiled_bytes(n + 1, m))
     rc = ctx.alloc(m * 4)
     fe = ctx.alloc(m)
-    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
-        iinst, tour, (scen, A.MEM_DEVICE_TILED), count=m, full=True, out_kind="device_tiled",
+    step_ms, k_ms = kernel_rate(ctx.split_eval(
+        iinst, ident, (scen2, A.MEM_DEVICE_TILED), count=m, first_index=lo, full=True,
+        out_kind="device_tiled",
         device_out={"totals": tot, "values": V, "cuts": cuts, "route_count": rc, "feasible": fe},
-        sync=False), 10)
+        sync=False, prepare=True), 10)
     out["split_c2_full_solution"] = {
-        "value": d.world * m / (step_ms / 1e3), "unit": UNIT, "kernel_ms": k_ms,
-        "roofline_frac": m * (4 * n + 8 + 12 * (n + 1)) / (k_ms / 1e3) / 1e9 / hbm_peak}
+        "value": M_C2 / (step_ms / 1e3), "unit": UNIT, "kernel_ms": k_ms, "scaling": "strong",
+        "roofline_frac": frac(m * (4 * n + 8 + 12 * (n + 1)), k_ms)}
     for b in (V, cuts, rc, fe):
         b.free()
-    # penalized split (quadratic, FP64-bound), n = 200 and the SAA shape n = 50
+    # penalized split (K2-int, O(n) exact form), n = 200
     pinst = make_random_instance(n, 1, Q_C2, False, 10.0)
     mp = min(m, 200_000)
-    step_ms, k_ms = kernel_rate(lambda: ctx.split_eval(
-        pinst, tour, (scen, A.MEM_DEVICE_TILED), count=mp, out_kind="device_tiled",
-        device_out={"totals": tot}, sync=False), 2, 1)
-    out["split_c2_penalized"] = {"value": d.world * mp / (step_ms / 1e3), "unit": UNIT,
-                                 "kernel_ms": k_ms, "scenarios": mp,
-                                 "dense_candidates_per_s": d.world * mp * n * (n + 1) / 2 / (step_ms / 1e3)}
+    step_ms, k_ms = kernel_rate(ctx.split_eval(
+        pinst, ident, (scen2, A.MEM_DEVICE_TILED), count=mp, first_index=lo,
+        out_kind="device_tiled", device_out={"totals": tot}, sync=False, prepare=True), 5, 1)
+    out["split_c2_penalized"] = {"value": G * mp / (step_ms / 1e3), "unit": UNIT,
+                                 "kernel_ms": k_ms, "scenarios_per_gpu": mp, "scaling": "weak",
+                                 "dense_candidates_per_s": G * mp * n * (n + 1) / 2 / (step_ms / 1e3)}
     scen.free()
+    scen2.free()
     tot.free()
 
-    # C5: 1000 giant tours x 10^5 scenarios, n = 50, penalized beta = 10, one launch
+    # C5: 1000 giant tours x 10^5 scenarios, n = 50, penalized beta = 10, one
+    # launch per rank over its scenario shard; the K x 16-word exact aggregate
+    # is all-reduced, so the argmin is over the whole 10^5
     n5, m5, K5 = 50, 100_000, 1000
     inst5 = make_random_instance(n5, 5, Q_C2, False, 10.0)
     rng = np.random.default_rng(5)
     tours5 = np.stack([rng.permutation(n5) + 1 for _ in range(K5)]).astype(np.int32)
-    scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, m5, w0=d.rank * m5)
+    lo5, hi5 = shard(m5, g, G)
+    scen5 = ctx.gen_scenarios(Distribution("uniform", 1, 10, seed=55), n5, hi5 - lo5, w0=lo5)
     res = {}
 
     def c5():
-        res["r"] = ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=m5,
-                                  totals=False)
+        res["r"] = ctx.split_eval(inst5, tours5, (scen5, A.MEM_DEVICE_TILED), count=hi5 - lo5,
+                                  first_index=lo5, totals=False)
 
-    step_ms, k_ms = kernel_rate(c5, 2, 1)
+    step_ms, k_ms = kernel_rate(c5, 3, 1)
     out["saa_c5_candidates"] = {
-        "value": d.world * K5 * m5 / (step_ms / 1e3), "unit": "(tour, scenario)-evals/s",
+        "value": K5 * m5 / (step_ms / 1e3), "unit": "(tour, scenario)-evals/s",
         "candidates_per_s": K5 / (step_ms / 1e3), "ms_per_launch": step_ms, "kernel_ms": k_ms,
-        "best_tour": res["r"]["best"], "config": "K=1000 tours x 1e5 scenarios, n=50, beta=10"}
+        "best_tour": res["r"]["best"], "scaling": "strong",
+        "config": "K=1000 tours x 1e5 scenarios, n=50, beta=10"}
     scen5.free()
 
+    # DSIRP C3 (50 customers, H=6, 1e5; weak), C4 (200 customers, H=6, 1e6
+    # sharded over the ranks) and the non-dyadic C3 twin (K3 fp64 path)
+    H = 6
+    rngf = np.random.default_rng(21)
+    fcusts = [Customer(U=100, I0=50, H=H, h=0.5 + rngf.random(), rho=1.5 + rngf.random(),
+                       fixed=30 + 20 * rngf.random((H, 3)), unit=0.25 + rngf.random((H, 3)))
+              for _ in range(50)]
+    for name, nc, mtot, steps, scaling in (("dsirp_c3", 50, 100_000, 20, "weak"),
+                                           ("dsirp_c4", 200, 1_000_000, 5, "strong"),
+                                           ("dsirp_c3_float", 50, 100_000, 20, "weak")):
+        if scaling == "strong":
+            l3, h3 = shard(mtot, g, G)
+        else:
+            l3, h3 = g * mtot, (g + 1) * mtot
+        m3 = h3 - l3
+        custs = fcusts if name == "dsirp_c3_float" else [
+            Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
+                     fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
+                     unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
+        sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m3, w0=l3)
+        t3 = ctx.alloc(nc * m3 * 8)
+        step_ms, k_ms = kernel_rate(ctx.dsirp_eval(
+            custs, (sc, A.MEM_DEVICE_TILED), count=m3, first_index=l3, out_kind="device_tiled",
+            device_out={"totals": t3}, sync=False, prepare=True), steps)
+        units = nc * (mtot if scaling == "strong" else G * mtot)
+        out[name] = {"value": units / (step_ms / 1e3), "unit": "(customer, scenario)-evals/s",
+                     "kernel_ms": k_ms, "customers": nc, "scenarios": units // nc,
+                     "bellman_state_updates_per_s": units * H * 101 / (step_ms / 1e3),
+                     "roofline_frac": frac(nc * m3 * (4 * H + 8), k_ms),
+                     "unit_bytes": "4H+8 per (customer, scenario)", "scaling": scaling,
+                     "dtype": "f64" if name == "dsirp_c3_float" else "int32-exact (dyadic pins)"}
+        sc.free()
+        t3.free()
+    if G > 1:
+        return out
+
     # K5: generic dense (min,+) sweep -- the DSIRP dense chain shape (H = 6
-    # stages of 101 x 101, option depth 3) for 10^5 frontiers per GPU
+    # stages of 101 x 101, option depth 3) for 10^5 frontiers
     rng = np.random.default_rng(11)
     stages = []
     for _ in range(6):
@@ -474,7 +608,7 @@ def secondary(ctx, d: Dist, args):
     init = np.full((B, 101), np.inf)
     init[np.arange(B), rng.integers(0, 101, B)] = 0.0
     ctx.minplus_sweep(stages, init[:1000])
-    st0 = ctx.kernel_stats(reset=True)
+    ctx.kernel_stats(reset=True)
     t0 = time.perf_counter()
     ctx.minplus_sweep(stages, init)
     wall = time.perf_counter() - t0
@@ -506,47 +640,6 @@ def secondary(ctx, d: Dist, args):
     out["scnb_ingest"] = {"value": arr.nbytes / wall / 1e9, "unit": "GB/s (file -> tiled HBM)",
                           "bytes": arr.nbytes, "wall_ms": wall * 1e3,
                           "note": "page-cached 800 MB file (C2 set), best of 3"}
-
-    # DSIRP C3 (50 customers, H=6, 1e5) and C4 (200 customers, H=6, 1e6)
-    for name, nc, m3, steps in (("dsirp_c3", 50, 100_000, 20), ("dsirp_c4", 200, 1_000_000, 3)):
-        m3 = m3 // d.world if name == "dsirp_c4" else m3
-        H = 6
-        custs = [Customer(U=100, I0=50, H=H, h=1.0, rho=2.0,
-                          fixed=np.tile(40 + 5 * np.arange(3.0), (H, 1)),
-                          unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
-        sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m3,
-                               w0=d.rank * m3)
-        t3 = ctx.alloc(nc * m3 * 8)
-        step_ms, k_ms = kernel_rate(lambda: ctx.dsirp_eval(
-            custs, (sc, A.MEM_DEVICE_TILED), count=m3, out_kind="device_tiled",
-            device_out={"totals": t3}, sync=False), steps)
-        units = d.world * nc * m3
-        out[name] = {"value": units / (step_ms / 1e3), "unit": "(customer, scenario)-evals/s",
-                     "kernel_ms": k_ms, "customers": nc, "scenarios": d.world * m3,
-                     "bellman_state_updates_per_s": units * H * 101 / (step_ms / 1e3),
-                     "roofline_frac": nc * m3 * 32 / (k_ms / 1e3) / 1e9 / hbm_peak,
-                     "scaling": "strong" if name == "dsirp_c4" else "weak"}
-        sc.free()
-        t3.free()
-    # non-dyadic twin of C3: h, rho, fixed and unit drawn as
-    # fractions, so the exact-integer kernel does not apply and K3's fp64
-    # path (the reference's association) runs
-    H, nc, m3 = 6, 50, 100_000
-    rng = np.random.default_rng(21)
-    fcusts = [Customer(U=100, I0=50, H=H, h=0.5 + rng.random(), rho=1.5 + rng.random(),
-                       fixed=30 + 20 * rng.random((H, 3)), unit=0.25 + rng.random((H, 3)))
-              for _ in range(nc)]
-    sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m3, w0=d.rank * m3)
-    t3 = ctx.alloc(nc * m3 * 8)
-    step_ms, k_ms = kernel_rate(lambda: ctx.dsirp_eval(
-        fcusts, (sc, A.MEM_DEVICE_TILED), count=m3, out_kind="device_tiled",
-        device_out={"totals": t3}, sync=False), 20)
-    out["dsirp_c3_float"] = {"value": d.world * nc * m3 / (step_ms / 1e3),
-                             "unit": "(customer, scenario)-evals/s", "kernel_ms": k_ms,
-                             "customers": nc, "scenarios": d.world * m3, "dtype": "f64",
-                             "scaling": "weak"}
-    sc.free()
-    t3.free()
     return out
 
 
@@ -567,16 +660,27 @@ def cpu_reference_secondary():
 
     n = N_C2
     tour = np.arange(1, n + 1, dtype=np.int32)
+    rtour = (np.random.default_rng(7).permutation(n) + 1).astype(np.int32)
     ms = 20_000
     dem = R.generate(UNIFORM, 1, 10, 77, n, 1, ms)
     rng = np.random.default_rng(1)
     c = rng.random((n + 2, n + 2)) * 20.0
     c = np.triu(c, 1)
     c = c + c.T
+    icost = R.make_random_instance(n, 1)
+    out["split_c2_weak"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, icost, tour, dem,
+                                                        threads), ms),
+                            f"batched_split_costs, {ms} scenarios")
     out["split_c2_float_costs"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, c, tour, dem,
                                                                threads), ms),
                                    f"batched_split_costs, float-cost twin, {ms} scenarios")
-    icost = R.make_random_instance(n, 1)
+    out["split_c2_random_tour"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, icost, rtour, dem,
+                                                               threads), ms),
+                                   f"batched_split_costs, random tour, {ms} scenarios")
+    out["split_c2_random_tour_float"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, c, rtour,
+                                                                     dem, threads), ms),
+                                         f"batched_split_costs, random tour, float costs, "
+                                         f"{ms} scenarios")
     out["split_c2_full_solution"] = (rate(lambda: R.expected_split(n, Q_C2, 1, 0.0, icost, tour,
                                                                     dem, threads), ms),
                                      f"batched_expected_split, {ms} scenarios")
@@ -615,10 +719,24 @@ def cpu_reference_secondary():
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args))
+    if args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # NCCL's communicator lines (nRanks, rings, NVLS) on stderr; stdout
+        # keeps the single JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     d = Dist()
+    if d.world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={d.world}", file=sys.stderr, flush=True)
+        d.close()
+        sys.exit(2)
     try:
         if args.impl == "reference":
             run_reference(args, d)
+        elif DRY:
+            run_dry(args, d)
         else:
             run_ours(args, d)
     finally:

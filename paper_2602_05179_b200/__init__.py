@@ -319,12 +319,14 @@ class Context:
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    quadratic: bool = False, out_kind: str = "host",
                    device_out: Optional[dict] = None, sync: bool = True,
-                   host_totals: Optional[np.ndarray] = None, raw: bool = False) -> dict:
+                   host_totals: Optional[np.ndarray] = None, raw: bool = False,
+                   prepare: bool = False):
         """Evaluate tours (k x n, 1-based ids) on a scenario set.
 
         Returns totals [k][m] (host), V/cuts [m][n+1], route_count, feasible
         (full mode) and per-tour aggregates.  out_kind 'device_tiled' writes
         into caller DeviceBuffers (device_out) and returns only aggregates.
+        prepare=True returns a callable that issues this exact call again.
         """
         tours = np.ascontiguousarray(np.atleast_2d(np.asarray(tours, np.int32)))
         k, n = tours.shape
@@ -361,6 +363,13 @@ class Context:
             raws = (A.AggRaw * k)()
             o.agg_raw = raws
             res["agg_raw"] = raws
+        if prepare:
+            # the same C call, argument structs built once (bench loops: the
+            # Python marshalling would otherwise dominate short device calls)
+            lib, h, held = self.lib, self.handle, (rinst, tours, sc, keep, o, agg, inst)
+            return lambda: A.check(lib.scendp_split_eval(
+                h, C.byref(held[0]), held[1].ctypes.data, k, C.byref(held[2]), flags,
+                C.byref(held[4])))
         A.check(self.lib.scendp_split_eval(self.handle, C.byref(rinst), tours.ctypes.data, k,
                                            C.byref(sc), flags, C.byref(o)))
         if sync or out_kind == "host":
@@ -373,7 +382,8 @@ class Context:
                    first_index: int = 0, full: bool = False, totals: bool = True,
                    out_kind: str = "host", device_out: Optional[dict] = None,
                    sync: bool = True, fp64: bool = False,
-                   host_totals: Optional[np.ndarray] = None, raw: bool = False) -> dict:
+                   host_totals: Optional[np.ndarray] = None, raw: bool = False,
+                   prepare: bool = False):
         nc = len(customers)
         H = customers[0].H
         carr = (A.Customer * nc)(*[c.as_c() for c in customers])
@@ -406,6 +416,10 @@ class Context:
             raws = (A.AggRaw * nc)()
             o.agg_raw = raws
             res["agg_raw"] = raws
+        if prepare:
+            lib, h, held = self.lib, self.handle, (carr, sc, keep, o, agg, list(customers))
+            return lambda: A.check(lib.scendp_dsirp_eval(h, held[0], nc, C.byref(held[1]), flags,
+                                                         C.byref(held[3])))
         A.check(self.lib.scendp_dsirp_eval(self.handle, carr, nc, C.byref(sc), flags,
                                            C.byref(o)))
         if sync or out_kind == "host":
