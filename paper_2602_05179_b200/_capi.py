@@ -11,6 +11,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libscendp_b200.so")
+# A/B measurements of another in-tree build (profiles/ scripts only)
+LIB_PATH = os.environ.get("SCENDP_LIB", LIB_PATH)
 
 OK = 0
 ERR_INVALID_ARGUMENT = 1

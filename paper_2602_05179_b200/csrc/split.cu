@@ -79,7 +79,7 @@ struct SplitArgs {
   uint32_t pen_lmax;     // K2-int: loads above this leave the exact int32 range
   const uint32_t* ccol;  // customer row of position s+1
   const int32_t* itab;   // [k][2][npad]: A = dist+ret, B = c0 - dist_next (int path)
-  const double* dtab;    // [k][4][npad]: dist, ret, c0, dist_next
+  const double* dtab;    // [k][npad][4]: dist, ret, c0, dist_next (interleaved)
   const double* f0d;     // [k] f(0) = (0.0 + c(0,s_1)) - dist[1]
   const int32_t* f0i;    // [k] same, integer path
   // scenarios
@@ -446,7 +446,7 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
 // sections 16-byte aligned.  Per tour q, positions i = 0..n:
 //   dist/ret/c0/col [k][n+1]   (generic / quadratic kernels)
 //   ccol [k][npad]             (K1 / K2-int column table, slot s = position s+1)
-//   itab [k][2][npad] int32    (exact integer path) | dtab [k][4][npad] fp64
+//   itab [k][2][npad] int32    (exact integer path) | dtab [k][npad][4] fp64
 //   f0d [k], f0i [k]           (f(0))
 struct TableLayout {
   int npad = 0;
@@ -639,15 +639,17 @@ void build_tables(const scendp_routing* inst, const int32_t* tours, uint32_t k,
         for (int i = n; i < npad; ++i) it[i] = it[npad + i] = 0;
       } else {
         f0i[q] = 0;
+        // interleaved per position: (dist, ret, c0, dist_next) of slot s at
+        // dt[4 s .. 4 s + 3] (two 128-bit shared loads per K1 step)
         double* dt = D(L.o_tab) + static_cast<size_t>(q) * 4 * npad;
         for (int i = 1; i <= n; ++i) {
-          const size_t sidx = static_cast<size_t>(i - 1);
-          dt[0 * npad + sidx] = dist[i];
-          dt[1 * npad + sidx] = ret[i];
-          dt[2 * npad + sidx] = c0[i];
-          dt[3 * npad + sidx] = i < n ? dist[i + 1] : 0.0;
+          double* e = dt + 4 * static_cast<size_t>(i - 1);
+          e[0] = dist[i];
+          e[1] = ret[i];
+          e[2] = c0[i];
+          e[3] = i < n ? dist[i + 1] : 0.0;
         }
-        for (int i = n; i < npad; ++i) dt[i] = dt[npad + i] = dt[2 * npad + i] = dt[3 * npad + i] = 0.0;
+        for (int i = n; i < npad; ++i) dt[4 * i] = dt[4 * i + 1] = dt[4 * i + 2] = dt[4 * i + 3] = 0.0;
       }
     }
   });
@@ -736,6 +738,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     const int T = kK1Threads;
     const bool intv = a.itab != nullptr;
     const size_t vt = intv ? 4 : 8;
+    // column table (non-identity tours), position tables, per-thread rings
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + (intv ? 2 : 4) * vt) +
                         static_cast<size_t>(kRing) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
