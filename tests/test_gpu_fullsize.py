@@ -5,13 +5,17 @@ reference (oracle/_ref) on the same box.
   generate_scenarios + batched_split_costs over all 10^6 columns; every total
   bit-exact, for the materialized (tiled) and the in-kernel-generated paths;
   the aggregate equals the exact mean of the totals.
-* C3 (DSIRP 50 customers x 10^5, H=6): every customer's totals against the
-  reference's per-customer batched_expected_cost on a sample of customers
-  (first, last, and a mixed fp64 one), all 10^5 scenarios each.
-* C4 (200 customers x 10^6): prefix stability -- the first 20,000 scenarios
-  of sampled customers equal the reference's.
+* C3 (DSIRP 50 customers x 10^5, H=6): all 50 customers x all 10^5
+  scenarios against the reference's per-customer batched_expected_cost,
+  totals bit-exact and means within 1e-9, on the exact-integer and the fp64
+  launch.
+* C4 (200 customers x 10^6): all 200 customers on the first 20,000
+  scenarios (prefix of the full launch; means of a 20,000-scenario call),
+  three customers over all 10^6 (totals and means).
 * C5 (1000 tours x 10^5, n=50, penalized beta=10): sampled tours' totals
-  bit-exact and the first-minimum argmin consistent with the per-tour means.
+  bit-exact over 10^5 and the first-minimum argmin consistent with the
+  per-tour means; all 1000 tours on a 10,000-scenario prefix against the
+  reference (totals, means, argmin).
 * C2 float-cost twin over 10^6 (one launch and 300,000-scenario waves), C2
   full solutions and penalized totals on 200,000 scenarios, C3 full
   schedules, and K5 at the bench shape against forward_sweep.
@@ -53,16 +57,17 @@ def test_c2_full_size_bit_exact(ctx, reference):
     scen.free()
 
 
-def _c3_customers(nc, H):
+def _c3_customers(nc, H, dyadic_only=False):
     """C3 pins (U=100, I0=50, h=1, rho=2, R=3, fixed 40+5r, unit 0.5+0.25r),
-    perturbed per customer by dyadic offsets; customer 1 gets non-dyadic
-    costs, which moves the launch onto the fp64 kernel path for it."""
+    perturbed per customer by dyadic offsets; unless dyadic_only, customer 1
+    gets non-dyadic costs, which moves the whole launch onto the K3 fp64
+    path (the exact-integer path needs every customer of a launch)."""
     ours, refs = [], []
     for c in range(nc):
         fixed = np.tile(40 + 5 * np.arange(3.0), (H, 1)) + (c % 7)
         unit = np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1)) + 0.25 * (c % 3)
         h = 1.0
-        if c == 1:
+        if c == 1 and not dyadic_only:
             fixed = fixed + 0.1
             h = 0.7
         kw = dict(U=100, I0=50, H=H, h=h, rho=2.0, fixed=fixed, unit=unit)
@@ -71,27 +76,60 @@ def _c3_customers(nc, H):
     return ours, refs
 
 
-@pytest.mark.parametrize("nc,m,sample,prefix", [(50, 100_000, (0, 1, 27, 49), None),
-                                                (200, 1_000_000, (0, 1, 199), 20_000)])
-def test_dsirp_c3_c4_bit_exact(ctx, reference, nc, m, sample, prefix):
-    H = 6
-    ours, refs = _c3_customers(nc, H)
+def _check_customer(got, c, ref_out, mean_check=True):
+    tot, _, _, _, _, ev, (mean, fc, ic) = ref_out
+    assert ev.all()
+    np.testing.assert_array_equal(got["totals"][c], tot)
+    if mean_check:
+        a = got["agg"][c]
+        assert a["finite_count"] == fc and a["infeasible_count"] == ic
+        assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
+
+
+@pytest.mark.parametrize("dyadic_only", [True, False])
+def test_dsirp_c3_all_customers_bit_exact(ctx, reference, dyadic_only):
+    """C3 in full: all 50 customers x all 10^5 scenarios against the
+    reference's per-customer batched_expected_cost (oudp.cpp:398-438, the
+    composition oracle of SURVEY 8c): every total bit-exact, every mean within
+    1e-9; the exact-integer launch (dyadic pins) and the fp64 launch."""
+    nc, m, H = 50, 100_000, 6
+    ours, refs = _c3_customers(nc, H, dyadic_only)
     dist = Distribution("uniform", 0, 33, seed=7)
     scen = ctx.gen_scenarios(dist, nc * H, m)
     got = ctx.dsirp_eval(ours, (scen, A.MEM_DEVICE_TILED), count=m)
     scen.free()
     assert got["evaluated"].all()
-    mref = prefix or m
-    dem = reference.generate(UNIFORM, 0, 33, 7, nc, H, mref)  # rows c*H + t
-    for c in sample:
-        cols = dem[:, c * H:(c + 1) * H]
-        tot, _, _, _, _, ev, (mean, fc, ic) = reference.expected_cost(refs[c], cols, THREADS)
-        assert ev.all()
-        np.testing.assert_array_equal(got["totals"][c][:mref], tot)
-        if prefix is None:
-            a = got["agg"][c]
-            assert a["finite_count"] == fc and a["infeasible_count"] == ic
-            assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
+    dem = reference.generate(UNIFORM, 0, 33, 7, nc, H, m)  # rows c*H + t
+    for c in range(nc):
+        _check_customer(got, c, reference.expected_cost(
+            refs[c], np.ascontiguousarray(dem[:, c * H:(c + 1) * H]), THREADS))
+
+
+@pytest.mark.parametrize("dyadic_only", [True, False])
+def test_dsirp_c4_all_customers(ctx, reference, dyadic_only):
+    """C4 (200 customers x 10^6 scenarios, one GPU): all 200 customers on the
+    first 20,000 scenarios -- the prefix of the full 10^6 launch, and a
+    20,000-scenario call whose per-customer means must match the reference's
+    within 1e-9 -- plus three customers over all 10^6 scenarios (totals and
+    means)."""
+    nc, m, H, pre = 200, 1_000_000, 6, 20_000
+    ours, refs = _c3_customers(nc, H, dyadic_only)
+    dist = Distribution("uniform", 0, 33, seed=7)
+    scen = ctx.gen_scenarios(dist, nc * H, m)
+    full = ctx.dsirp_eval(ours, (scen, A.MEM_DEVICE_TILED), count=m)
+    part = ctx.dsirp_eval(ours, (scen, A.MEM_DEVICE_TILED), count=pre)
+    scen.free()
+    assert full["evaluated"].all()
+    dem = reference.generate(UNIFORM, 0, 33, 7, nc, H, pre)
+    for c in range(nc):
+        r = reference.expected_cost(refs[c], np.ascontiguousarray(dem[:, c * H:(c + 1) * H]),
+                                    THREADS)
+        np.testing.assert_array_equal(full["totals"][c][:pre], r[0])
+        _check_customer(part, c, r)
+    big = reference.generate(UNIFORM, 0, 33, 7, nc, H, m)
+    for c in (0, 1, nc - 1):
+        _check_customer(full, c, reference.expected_cost(
+            refs[c], np.ascontiguousarray(big[:, c * H:(c + 1) * H]), THREADS))
 
 
 def test_c5_saa_sweep_bit_exact(ctx, reference):
@@ -113,6 +151,28 @@ def test_c5_saa_sweep_bit_exact(ctx, reference):
         tot, (mean, fc, ic) = reference.split_costs(n, Q, 0, beta, costs, tours[t], dem, THREADS)
         np.testing.assert_array_equal(got["totals"][t], tot)
         assert got["agg"][t]["mean"] == mean
+
+
+def test_c5_all_tours_prefix_bit_exact(ctx, reference):
+    """C5's 1000 candidate tours, every one of them, on the first 10,000
+    scenarios: totals bit-exact, means equal, and the selected candidate is
+    the first minimum of the reference's per-tour means (SAA scorer,
+    saa.cpp:127-134)."""
+    n, m, K, Q, beta = 50, 10_000, 1000, 100, 10.0
+    costs = reference.make_random_instance(n, 5)
+    inst = RoutingInstance(n, Q, False, beta, costs)
+    rng = np.random.default_rng(5)
+    tours = np.stack([rng.permutation(n) + 1 for _ in range(K)]).astype(np.int32)
+    seed = reference.derive_stream(5, TAG_SCENARIO, 0)
+    got = ctx.split_eval(inst, tours, Distribution("uniform", 1, 10, seed=seed), count=m)
+    dem = reference.generate(UNIFORM, 1, 10, seed, n, 1, m)
+    ref_means = np.empty(K)
+    for t in range(K):
+        tot, (mean, fc, ic) = reference.split_costs(n, Q, 0, beta, costs, tours[t], dem, THREADS)
+        np.testing.assert_array_equal(got["totals"][t], tot)
+        assert got["agg"][t]["mean"] == mean and got["agg"][t]["finite_count"] == fc
+        ref_means[t] = mean
+    assert got["best"] == int(np.argmin(ref_means))
 
 
 def _float_costs(n, seed):
