@@ -61,12 +61,16 @@ typedef struct scendp_ctx scendp_ctx;
 /* ---- context ------------------------------------------------------------
  * One context = one CUDA device + one stream + cached scratch.  The
  * reference's BackendConfig (engine.hpp:24-51) maps onto it: memory_budget
- * -> scratch_limit (bytes a single call may stage; 0 = no limit), batch_size
- * -> max_batch (scenarios per launch wave; 0 = whole call). */
+ * -> scratch_limit (device bytes a single call's scratch may use; 0 = the
+ * free device memory), batch_size -> max_batch (scenarios per launch wave;
+ * 0 = whole call).  A call runs in waves sized by its device footprint
+ * model (scendp_split_footprint / scendp_dsirp_footprint) under that budget;
+ * an allocation failure halves the wave and retries (never below one
+ * 32-scenario tile), so results never depend on the budget. */
 typedef struct {
   int32_t device;          /* CUDA ordinal; -1 = current device */
-  uint64_t scratch_limit;  /* bytes of staged (tiled) scenario copy per wave:
-                              caps the wave size; 0 = unlimited */
+  uint64_t scratch_limit;  /* device scratch budget of a call (bytes): caps
+                              the wave size; 0 = free device memory */
   uint64_t max_batch;      /* scenarios per launch wave; 0 = unlimited */
   uint32_t flags;          /* SCENDP_CTX_* */
 } scendp_opts;
@@ -293,6 +297,44 @@ scendp_status scendp_dsirp_eval(scendp_ctx* ctx,
                                 uint32_t n_customers,
                                 const scendp_scenarios* sc, uint32_t flags,
                                 const scendp_dsirp_out* out);
+
+/* ---- device footprint model ----------------------------------------------
+ * The device analogue of the reference's per-scenario footprint and batch
+ * sizing (split_per_scenario_bytes, split.cpp:287-301; oudp.cpp:383-396;
+ * adjust_batch_size / memory_footprint, engine.cpp:7-30): the scratch bytes a
+ * call with these arguments allocates, split into a part independent of the
+ * wave (tour / customer tables, aggregates, hand-off list floor, fallback
+ * scratch, a pageable upload's staging chunk) and a part per scenario of a
+ * wave (staged tiled input and its staging copy, outputs bound for pageable
+ * host memory or the reference layout, hand-off bitmap), and the wave the
+ * context's budget allows.  Caller-provided device outputs are not scratch
+ * and are not counted. */
+typedef struct {
+  uint64_t fixed_bytes;
+  uint64_t per_scenario_bytes;
+  uint64_t wave;     /* scenarios per wave the call would use */
+  uint64_t budget;   /* scratch_limit, else held scratch + free memory - 1/16 */
+} scendp_footprint;
+
+scendp_status scendp_split_footprint(scendp_ctx* ctx, const scendp_routing* inst,
+                                     uint32_t k_tours, const scendp_scenarios* sc,
+                                     uint32_t flags, const scendp_split_out* out,
+                                     scendp_footprint* fp);
+scendp_status scendp_dsirp_footprint(scendp_ctx* ctx, const scendp_customer* customers,
+                                     uint32_t n_customers, const scendp_scenarios* sc,
+                                     uint32_t flags, const scendp_dsirp_out* out,
+                                     scendp_footprint* fp);
+
+typedef struct {
+  uint64_t scratch_bytes;  /* device bytes the context holds in scratch */
+  uint64_t scratch_peak;   /* high-water mark of scratch_bytes */
+  uint64_t device_free;    /* cudaMemGetInfo */
+  uint64_t device_total;
+  uint64_t oom_retries;    /* waves halved after an allocation failure */
+  uint64_t last_wave;      /* wave size of the last split / DSIRP call */
+} scendp_memory_info;
+
+scendp_status scendp_ctx_memory(scendp_ctx* ctx, scendp_memory_info* info);
 
 /* ---- K5: generic dense (min,+) stage sweep (minplus.hpp / minplus.cpp) ---
  * forward_sweep (minplus.cpp:94-102) of `batch` initial frontiers through one

@@ -185,6 +185,11 @@ def tiled_to_reference(flat: np.ndarray, rows: int, count: int) -> np.ndarray:
     return np.ascontiguousarray(t.reshape(tiles * 32, rows)[:count])
 
 
+def _fp_dict(f: A.Footprint) -> dict:
+    return {"fixed": f.fixed_bytes, "per_scenario": f.per_scenario_bytes, "wave": f.wave,
+            "budget": f.budget}
+
+
 def _agg_dict(a: A.Agg) -> dict:
     return {"sum": a.sum, "mean": a.mean if a.finite_count else None,
             "finite_count": a.finite_count, "infeasible_count": a.infeasible_count,
@@ -320,13 +325,14 @@ class Context:
                    quadratic: bool = False, out_kind: str = "host",
                    device_out: Optional[dict] = None, sync: bool = True,
                    host_totals: Optional[np.ndarray] = None, raw: bool = False,
-                   prepare: bool = False):
+                   prepare: bool = False, footprint: bool = False):
         """Evaluate tours (k x n, 1-based ids) on a scenario set.
 
         Returns totals [k][m] (host), V/cuts [m][n+1], route_count, feasible
         (full mode) and per-tour aggregates.  out_kind 'device_tiled' writes
         into caller DeviceBuffers (device_out) and returns only aggregates.
-        prepare=True returns a callable that issues this exact call again.
+        prepare=True returns a callable that issues this exact call again;
+        footprint=True returns the call's device footprint model instead.
         """
         tours = np.ascontiguousarray(np.atleast_2d(np.asarray(tours, np.int32)))
         k, n = tours.shape
@@ -363,6 +369,11 @@ class Context:
             raws = (A.AggRaw * k)()
             o.agg_raw = raws
             res["agg_raw"] = raws
+        if footprint:
+            fp = A.Footprint()
+            A.check(self.lib.scendp_split_footprint(self.handle, C.byref(rinst), k, C.byref(sc),
+                                                    flags, C.byref(o), C.byref(fp)))
+            return _fp_dict(fp)
         if prepare:
             # the same C call, argument structs built once (bench loops: the
             # Python marshalling would otherwise dominate short device calls)
@@ -383,7 +394,7 @@ class Context:
                    out_kind: str = "host", device_out: Optional[dict] = None,
                    sync: bool = True, fp64: bool = False,
                    host_totals: Optional[np.ndarray] = None, raw: bool = False,
-                   prepare: bool = False):
+                   prepare: bool = False, footprint: bool = False):
         nc = len(customers)
         H = customers[0].H
         carr = (A.Customer * nc)(*[c.as_c() for c in customers])
@@ -416,6 +427,11 @@ class Context:
             raws = (A.AggRaw * nc)()
             o.agg_raw = raws
             res["agg_raw"] = raws
+        if footprint:
+            fp = A.Footprint()
+            A.check(self.lib.scendp_dsirp_footprint(self.handle, carr, nc, C.byref(sc), flags,
+                                                    C.byref(o), C.byref(fp)))
+            return _fp_dict(fp)
         if prepare:
             lib, h, held = self.lib, self.handle, (carr, sc, keep, o, agg, list(customers))
             return lambda: A.check(lib.scendp_dsirp_eval(h, held[0], nc, C.byref(held[1]), flags,
@@ -434,6 +450,12 @@ class Context:
         ms = C.c_double()
         A.check(self.lib.scendp_timer_stop(self.handle, C.byref(ms)))
         return ms.value
+
+    def memory_info(self) -> dict:
+        """Scratch held / high-water mark, cudaMemGetInfo, wave retries."""
+        mi = A.MemoryInfo()
+        A.check(self.lib.scendp_ctx_memory(self.handle, C.byref(mi)))
+        return {k: getattr(mi, k) for k, _ in A.MemoryInfo._fields_}
 
     def kernel_stats(self, reset: bool = False) -> dict:
         s = A.KernelStats()

@@ -110,6 +110,17 @@ class ScnbHeader(C.Structure):
     _fields_ = [("rows", C.c_uint64), ("count", C.c_uint64)]
 
 
+class Footprint(C.Structure):
+    _fields_ = [("fixed_bytes", C.c_uint64), ("per_scenario_bytes", C.c_uint64),
+                ("wave", C.c_uint64), ("budget", C.c_uint64)]
+
+
+class MemoryInfo(C.Structure):
+    _fields_ = [("scratch_bytes", C.c_uint64), ("scratch_peak", C.c_uint64),
+                ("device_free", C.c_uint64), ("device_total", C.c_uint64),
+                ("oom_retries", C.c_uint64), ("last_wave", C.c_uint64)]
+
+
 # Every symbol include/scendp_cuda.h declares, with its ctypes signature.
 SIGNATURES = {
     "scendp_ctx_create": (C.c_int, [C.POINTER(Opts), C.POINTER(C.c_void_p)]),
@@ -154,6 +165,13 @@ SIGNATURES = {
     "scendp_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "scendp_kernel_stats_get": (C.c_int, [C.c_void_p, C.POINTER(KernelStats), C.c_int32]),
     "scendp_flush_l2": (C.c_int, [C.c_void_p]),
+    "scendp_split_footprint": (C.c_int, [C.c_void_p, C.POINTER(Routing), C.c_uint32,
+                                         C.POINTER(Scenarios), C.c_uint32, C.POINTER(SplitOut),
+                                         C.POINTER(Footprint)]),
+    "scendp_dsirp_footprint": (C.c_int, [C.c_void_p, C.POINTER(Customer), C.c_uint32,
+                                         C.POINTER(Scenarios), C.c_uint32, C.POINTER(DsirpOut),
+                                         C.POINTER(Footprint)]),
+    "scendp_ctx_memory": (C.c_int, [C.c_void_p, C.POINTER(MemoryInfo)]),
 }
 
 _lib = None

@@ -249,19 +249,52 @@ void parallel_parts(int parts, const std::function<void(int)>& fn) {
 void* scendp_ctx::scratch_get(int slot, uint64_t bytes) {
   if (bytes == 0) bytes = 256;
   if (scratch_bytes[slot] >= bytes) return scratch[slot];
-  if (slot == scendp_host::kScrCustomers) dsirp_key.clear();  // tables move
-  if (slot == scendp_host::kScrTours) tours_dev = nullptr;
-  if (scratch[slot]) {
-    CUDA_CHECK(cudaStreamSynchronize(stream));
-    CUDA_CHECK(cudaFree(scratch[slot]));
-    scratch[slot] = nullptr;
-    scratch_bytes[slot] = 0;
-  }
+  scratch_free(slot);
   const uint64_t want = (bytes + (bytes >> 3) + 4095) & ~uint64_t{4095};
-  CUDA_CHECK(cudaMalloc(&scratch[slot], want));
+  const cudaError_t e = cudaMalloc(&scratch[slot], want);
+  if (e != cudaSuccess) {
+    scratch[slot] = nullptr;
+    (void)cudaGetLastError();  // not sticky: clear it for the caller's retry
+    CUDA_CHECK(e);
+  }
   scratch_bytes[slot] = want;
   ++scratch_gen[slot];
+  scratch_total += want;
+  scratch_peak = std::max(scratch_peak, scratch_total);
   return scratch[slot];
+}
+
+void scendp_ctx::scratch_free(int slot) {
+  if (slot == scendp_host::kScrCustomers) dsirp_key.clear();  // tables move
+  if (slot == scendp_host::kScrTours) tours_dev = nullptr;
+  if (!scratch[slot]) return;
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  CUDA_CHECK(cudaFree(scratch[slot]));
+  scratch[slot] = nullptr;
+  scratch_total -= scratch_bytes[slot];
+  scratch_bytes[slot] = 0;
+}
+
+uint64_t scendp_ctx::wave_for_model(uint64_t m, uint64_t fixed, uint64_t per_scenario,
+                                    uint64_t* budget_out) {
+  uint64_t w = ((std::max<uint64_t>(m, 1) + 31) / 32) * 32;
+  if (opts.max_batch) w = std::min(w, (opts.max_batch + 31) & ~uint64_t{31});
+  uint64_t budget = opts.scratch_limit;
+  if (!budget) {
+    if (fixed + per_scenario * w <= scratch_total) {
+      budget = scratch_total;  // fits what is already held: no driver query
+    } else {
+      size_t fr = 0, tot = 0;
+      CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+      budget = scratch_total + fr - fr / 16;
+    }
+  }
+  if (budget_out) *budget_out = budget;
+  if (per_scenario) {
+    const uint64_t room = budget > fixed ? budget - fixed : 0;
+    w = std::min(w, std::max<uint64_t>(32, (room / per_scenario) & ~uint64_t{31}));
+  }
+  return w;
 }
 
 void* scendp_ctx::pinned_agg(uint64_t bytes) {
@@ -535,6 +568,21 @@ scendp_status scendp_memset(scendp_ctx* ctx, void* dst, int32_t value, uint64_t 
   return guard([&] {
     CUDA_CHECK(cudaSetDevice(ctx->device));
     CUDA_CHECK(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  });
+}
+
+scendp_status scendp_ctx_memory(scendp_ctx* ctx, scendp_memory_info* info) {
+  return guard([&] {
+    if (!ctx || !info) fail(SCENDP_ERR_INVALID_ARGUMENT, "null argument");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    size_t fr = 0, tot = 0;
+    CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+    info->scratch_bytes = ctx->scratch_total;
+    info->scratch_peak = ctx->scratch_peak;
+    info->device_free = fr;
+    info->device_total = tot;
+    info->oom_retries = ctx->oom_retries;
+    info->last_wave = ctx->last_wave;
   });
 }
 

@@ -190,6 +190,80 @@ void append_customer_key(const scendp_customer& s, int H, std::vector<char>& key
   if (s.holding_tabular) put(s.holding_table, static_cast<size_t>(s.capacity + 1) * 8);
 }
 
+// Device footprint model of one scendp_dsirp_eval call (device analogue of
+// the reference's oudp footprint, oudp.cpp:383-396): fixed bytes (customer
+// tables, aggregates, dense long-horizon scratch), bytes per scenario of a
+// wave (staged input, host-bound outputs), and the wave under the budget.
+struct DsirpFootprint {
+  uint64_t fixed = 0, per_scenario = 0, wave = 0, budget = 0;
+};
+
+DsirpFootprint dsirp_footprint(scendp_ctx* ctx, uint32_t nc, int H, const scendp_scenarios* sc,
+                               uint32_t flags, const scendp_dsirp_out* out, uint64_t table_bytes) {
+  const bool full = (flags & SCENDP_DSIRP_FULL) != 0;
+  const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+  const uint64_t NC = nc, Hh = static_cast<uint64_t>(H);
+  DsirpFootprint f;
+  f.fixed = table_bytes + NC * sizeof(scendp_agg_raw) + (H > 32 ? (512ull << 20) : 0);
+  uint64_t in_fixed = 0;
+  f.per_scenario = stage_footprint(sc, &in_fixed);
+  f.fixed += in_fixed;
+  if (host_out && out->totals && !mapped_host_alias(out->totals)) f.per_scenario += NC * 8;
+  if (host_out && out->evaluated) f.per_scenario += NC;
+  if (full && out->mem_kind != SCENDP_MEM_DEVICE_TILED) f.per_scenario += 13 * NC * Hh;  // tiled
+  if (full && host_out) f.per_scenario += 13 * NC * Hh;  // reference layout
+  f.wave = ctx->wave_for_model(sc->count, f.fixed, f.per_scenario, &f.budget);
+  return f;
+}
+
+struct DsirpWaveBufs {
+  double* totals = nullptr;
+  uint8_t* evaluated = nullptr;
+  uint8_t *dl = nullptr, *r_dl = nullptr;
+  int32_t *q = nullptr, *ei = nullptr, *ro = nullptr, *r_q = nullptr, *r_ei = nullptr,
+          *r_ro = nullptr;
+};
+
+DsirpWaveBufs reserve_dsirp_wave(scendp_ctx* ctx, uint32_t nc, int H, const scendp_scenarios* sc,
+                                 bool full, const scendp_dsirp_out* out, bool call_totals,
+                                 uint64_t mw) {
+  const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+  const uint64_t NC = nc, Hh = static_cast<uint64_t>(H), fcount = NC * ((mw + 31) / 32) * 32 * Hh;
+  DsirpWaveBufs b;
+  reserve_stage(ctx, sc, mw);
+  if (host_out && out->totals && !call_totals)
+    b.totals = static_cast<double*>(ctx->scratch_get(kScrTotals, NC * mw * 8));
+  if (host_out && out->evaluated) b.evaluated = static_cast<uint8_t*>(ctx->scratch_get(kScrOut5, NC * mw));
+  if (full && out->mem_kind != SCENDP_MEM_DEVICE_TILED) {
+    b.dl = static_cast<uint8_t*>(ctx->scratch_get(kScrOut1, fcount));
+    b.q = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, fcount * 4));
+    b.ei = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, fcount * 4));
+    b.ro = static_cast<int32_t*>(ctx->scratch_get(kScrOut4, fcount * 4));
+  }
+  if (full && host_out) {
+    b.r_dl = static_cast<uint8_t*>(ctx->scratch_get(kScrOut7, NC * mw * Hh));
+    b.r_q = static_cast<int32_t*>(ctx->scratch_get(kScrOut6, NC * mw * Hh * 4));
+    b.r_ei = static_cast<int32_t*>(ctx->scratch_get(kScrOut8, NC * mw * Hh * 4));
+    b.r_ro = static_cast<int32_t*>(ctx->scratch_get(kScrOut9, NC * mw * Hh * 4));
+  }
+  return b;
+}
+
+// rows x wave_pitch bytes of per-wave scratch -> host rows of host_pitch
+// bytes at byte offset `off` (one contiguous copy for a single-wave call).
+template <typename T>
+void copy_rows_back(scendp_ctx* ctx, T* host, const T* dev, uint64_t rows, uint64_t host_pitch,
+                    uint64_t wave_pitch, uint64_t off) {
+  char* h = reinterpret_cast<char*>(host) + off;
+  if (host_pitch == wave_pitch || rows == 1) {
+    download(ctx, h, dev, rows * wave_pitch);
+  } else {
+    CUDA_CHECK(cudaMemcpy2DAsync(h, host_pitch, dev, wave_pitch, wave_pitch, rows,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->stats.d2h_bytes += rows * wave_pitch;
+  }
+}
+
 }  // namespace
 
 extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_customer* customers,
@@ -313,42 +387,36 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
     auto* d_agg = static_cast<unsigned long long*>(ctx->agg_buffer(nc * sizeof(scendp_agg_raw)));
     CUDA_CHECK(cudaMemsetAsync(d_agg, 0, nc * sizeof(scendp_agg_raw), ctx->stream));
 
+    // outputs: the caller's device buffers and page-locked host totals are
+    // written in place at each wave's offset; whatever is bound for pageable
+    // host memory goes through per-wave scratch, copied back after its wave
     const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
     const bool out_dev_ref = out->mem_kind == SCENDP_MEM_DEVICE;
     const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
-    const bool dev_out = out_dev_tiled || out_dev_ref;
-    double* d_totals = nullptr;
-    uint8_t* d_eval = nullptr;
     double* zc_totals = host_out ? static_cast<double*>(mapped_host_alias(out->totals)) : nullptr;
-    if (out->totals)
-      d_totals = dev_out    ? out->totals
-                 : zc_totals ? zc_totals
-                             : static_cast<double*>(ctx->scratch_get(kScrTotals, nc * m * 8));
-    if (out->evaluated)
-      d_eval = dev_out ? out->evaluated : static_cast<uint8_t*>(ctx->scratch_get(kScrOut5, nc * m));
-    const uint64_t tiles = (m + 31) / 32;
-    const uint64_t fcount = static_cast<uint64_t>(nc) * tiles * 32 * H;
-    uint8_t* d_dl = nullptr;
-    int32_t *d_q = nullptr, *d_ei = nullptr, *d_ro = nullptr;
-    if (full) {
-      if (out_dev_tiled) {
-        d_dl = out->deliver;
-        d_q = out->quantity;
-        d_ei = out->end_inventory;
-        d_ro = out->route_option;
-      } else {
-        d_dl = static_cast<uint8_t*>(ctx->scratch_get(kScrOut1, fcount));
-        d_q = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, fcount * 4));
-        d_ei = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, fcount * 4));
-        d_ro = static_cast<int32_t*>(ctx->scratch_get(kScrOut4, fcount * 4));
-      }
-    }
+    double* call_totals = !out->totals ? nullptr : host_out ? zc_totals : out->totals;
 
     int max_u = 0;
     for (uint32_t c = 0; c < nc; ++c) max_u = std::max(max_u, customers[c].capacity);
-    uint64_t wave = ctx->wave_for(m, sc->mem_kind == SCENDP_MEM_DEVICE_TILED ? 0 : 4ull * sc->rows);
-    for (uint64_t w0 = 0; w0 < m; w0 += wave) {
+    // device footprint model -> wave size
+    const DsirpFootprint fpm = dsirp_footprint(ctx, nc, H, sc, flags, out,
+                                               ctx->scratch_bytes[kScrCustomers]);
+    uint64_t wave = fpm.wave;
+    const uint64_t Hh = static_cast<uint64_t>(H);
+    for (uint64_t w0 = 0; w0 < m;) {
       const uint64_t mw = std::min(wave, m - w0);
+      const uint64_t wtiles = (mw + 31) / 32;
+      DsirpWaveBufs wb;
+      try {
+        wb = reserve_dsirp_wave(ctx, nc, H, sc, full, out, call_totals != nullptr, mw);
+      } catch (const Error& e) {
+        if (e.status != SCENDP_ERR_OUT_OF_MEMORY || wave <= 32) throw;
+        wave = std::max<uint64_t>(32, (wave / 2) & ~uint64_t{31});
+        release_wave_scratch(ctx);
+        ++ctx->oom_retries;
+        continue;
+      }
+      ctx->last_wave = wave;
       scendp_scenarios sw = *sc;
       sw.count = mw;
       sw.first_index = sc->first_index + w0;
@@ -368,16 +436,22 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       for (uint32_t c = 0; c < nc; ++c) a.all_std_hold &= customers[c].holding_tabular ? 0 : 1;
       a.rows = sc->rows;
       a.m_wave = mw;
-      a.w_base = w0;
-      a.m_total = m;
+      // wave-local addressing: call-level destinations at the wave's offset
+      a.w_base = 0;
       a.tiled = fused ? nullptr : tiled;
       a.gen = gp;
-      a.totals = d_totals;
-      a.evaluated = d_eval;
-      a.deliver = d_dl;
-      a.quantity = d_q;
-      a.end_inventory = d_ei;
-      a.route_option = d_ro;
+      a.totals = !out->totals ? nullptr : call_totals ? call_totals + w0 : wb.totals;
+      a.tot_stride = call_totals ? m : mw;
+      a.evaluated = !out->evaluated ? nullptr : host_out ? wb.evaluated : out->evaluated + w0;
+      a.ev_stride = host_out ? mw : m;
+      if (full) {
+        const uint64_t toff = (w0 / 32) * Hh * 32;
+        a.deliver = out_dev_tiled ? out->deliver + toff : wb.dl;
+        a.quantity = out_dev_tiled ? out->quantity + toff : wb.q;
+        a.end_inventory = out_dev_tiled ? out->end_inventory + toff : wb.ei;
+        a.route_option = out_dev_tiled ? out->route_option + toff : wb.ro;
+        a.sched_tiles = out_dev_tiled ? (m + 31) / 32 : wtiles;
+      }
       a.agg = d_agg;
       // fast form (H <= 8) when the customer tables fit in shared memory:
       // the exact-integer path (cost-only and schedules) and fp64 cost-only
@@ -389,44 +463,37 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       else if (H <= 16) launch_h16(ctx, a, smem, int_path, full);
       else if (H <= 32) launch_h32(ctx, a, smem, int_path, full);
       else launch_long(ctx, a, full, max_u, H);  // the reference's dense pass
+
+      // per-wave copies back
+      if (host_out) {
+        if (out->totals && !call_totals)
+          copy_rows_back(ctx, out->totals, wb.totals, nc, m * 8, mw * 8, w0 * 8);
+        if (out->evaluated) copy_rows_back(ctx, out->evaluated, wb.evaluated, nc, m, mw, w0);
+      }
+      if (full && !out_dev_tiled) {
+        // tiled [c][mw/32][H][32] -> [c][mw][H], into the caller's device
+        // buffers at the wave's rows or through scratch to host memory
+        for (uint32_t c = 0; c < nc; ++c) {
+          const uint64_t src = static_cast<uint64_t>(c) * wtiles * 32 * Hh;
+          const uint64_t dst = out_dev_ref ? (static_cast<uint64_t>(c) * m + w0) * Hh
+                                           : static_cast<uint64_t>(c) * mw * Hh;
+          launch_from_tiled<uint8_t>(ctx, wb.dl + src, Hh, mw, (out_dev_ref ? out->deliver : wb.r_dl) + dst);
+          launch_from_tiled<int32_t>(ctx, wb.q + src, Hh, mw, (out_dev_ref ? out->quantity : wb.r_q) + dst);
+          launch_from_tiled<int32_t>(ctx, wb.ei + src, Hh, mw, (out_dev_ref ? out->end_inventory : wb.r_ei) + dst);
+          launch_from_tiled<int32_t>(ctx, wb.ro + src, Hh, mw, (out_dev_ref ? out->route_option : wb.r_ro) + dst);
+        }
+        if (host_out) {
+          copy_rows_back(ctx, out->deliver, wb.r_dl, nc, m * Hh, mw * Hh, w0 * Hh);
+          copy_rows_back(ctx, out->quantity, wb.r_q, nc, m * Hh * 4, mw * Hh * 4, w0 * Hh * 4);
+          copy_rows_back(ctx, out->end_inventory, wb.r_ei, nc, m * Hh * 4, mw * Hh * 4, w0 * Hh * 4);
+          copy_rows_back(ctx, out->route_option, wb.r_ro, nc, m * Hh * 4, mw * Hh * 4, w0 * Hh * 4);
+        }
+      }
+      w0 += mw;
     }
 
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(nc) * kAggWords);
-
-    if (host_out) {
-      if (out->totals) {
-        if (zc_totals) ctx->stats.d2h_bytes += nc * m * 8;  // stored by the kernels
-        else download(ctx, out->totals, d_totals, nc * m * 8);
-      }
-      if (out->evaluated)
-        ctx->copy(out->evaluated, d_eval, nc * m, cudaMemcpyDeviceToHost);
-    }
-    if (full && !out_dev_tiled) {
-      // tiled [c][m/32][H][32] -> [c][m][H]
-      uint8_t* r_dl = out_dev_ref ? out->deliver : static_cast<uint8_t*>(ctx->scratch_get(kScrStaging, nc * m * H));
-      int32_t* r_q = out_dev_ref ? out->quantity : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, nc * m * H * 4));
-      int32_t* r_ei = out_dev_ref ? out->end_inventory : static_cast<int32_t*>(ctx->scratch_get(kScrFallback, nc * m * H * 4));
-      int32_t* r_ro = out_dev_ref ? out->route_option : static_cast<int32_t*>(ctx->scratch_get(kScrOverflow, nc * m * H * 4));
-      for (uint32_t c = 0; c < nc; ++c) {
-        const uint64_t src = static_cast<uint64_t>(c) * tiles * 32 * H;
-        const uint64_t dst = static_cast<uint64_t>(c) * m * H;
-        launch_from_tiled<uint8_t>(ctx, d_dl + src, H, m, r_dl + dst);
-        launch_from_tiled<int32_t>(ctx, d_q + src, H, m, r_q + dst);
-        launch_from_tiled<int32_t>(ctx, d_ei + src, H, m, r_ei + dst);
-        launch_from_tiled<int32_t>(ctx, d_ro + src, H, m, r_ro + dst);
-        if (m % 32 == 0) {
-          // [c][m/32][H][32] is [(c*m)/32][H][32]: one launch covered all
-          // customers only if we had passed count = nc*m; keep per-customer
-          // launches for clarity when m is ragged
-        }
-      }
-      if (host_out) {
-        download(ctx, out->deliver, r_dl, nc * m * H);
-        download(ctx, out->quantity, r_q, nc * m * H * 4);
-        download(ctx, out->end_inventory, r_ei, nc * m * H * 4);
-        download(ctx, out->route_option, r_ro, nc * m * H * 4);
-      }
-    }
+    if (host_out && out->totals && zc_totals) ctx->stats.d2h_bytes += nc * m * 8;  // stored by the kernels
     const bool want_agg = out->agg || out->agg_raw;
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
@@ -438,5 +505,32 @@ extern "C" scendp_status scendp_dsirp_eval(scendp_ctx* ctx, const scendp_custome
       if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, nc * sizeof(scendp_agg_raw));
       if (out->agg) finalize_agg(h_raw, 1, nc, out->agg);
     }
+  });
+}
+
+extern "C" scendp_status scendp_dsirp_footprint(scendp_ctx* ctx, const scendp_customer* customers,
+                                                uint32_t n_customers, const scendp_scenarios* sc,
+                                                uint32_t flags, const scendp_dsirp_out* out,
+                                                scendp_footprint* fp) {
+  return guard([&] {
+    if (!ctx || !customers || !n_customers || !sc || !out || !fp)
+      fail(SCENDP_ERR_INVALID_ARGUMENT, "null argument");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    const int H = customers[0].horizon;
+    // customer tables without deduplication (an upper bound of the cached
+    // record | pool | ipool block)
+    uint64_t tb = 0;
+    for (uint32_t c = 0; c < n_customers; ++c) {
+      const scendp_customer& s = customers[c];
+      const uint64_t U1 = static_cast<uint64_t>(s.capacity) + 1, Hh = static_cast<uint64_t>(H);
+      tb += sizeof(CustDev) + 8 * (2 * Hh * s.options + Hh * U1 + (s.delivery_tabular ? Hh * U1 : 0) +
+                                   (s.holding_tabular ? U1 : 0)) +
+            4 * (Hh * U1 + (s.holding_tabular ? U1 : 0)) + 48;
+    }
+    const DsirpFootprint f = dsirp_footprint(ctx, n_customers, H, sc, flags, out, tb);
+    fp->fixed_bytes = f.fixed;
+    fp->per_scenario_bytes = f.per_scenario;
+    fp->wave = f.wave;
+    fp->budget = f.budget;
   });
 }

@@ -39,12 +39,17 @@ struct DsirpArgs {
   int32_t H;
   int32_t all_std_hold;  // every customer uses the standard holding model
   uint64_t rows;         // nc * H
-  uint64_t m_wave, w_base, m_total;
+  uint64_t m_wave, w_base;
+  // outputs are addressed by w = w_base + wl (the host passes them at the
+  // wave's offset with w_base = 0); row strides per customer:
+  uint64_t tot_stride;   // totals [nc][tot_stride]
+  uint64_t ev_stride;    // evaluated [nc][ev_stride]
+  uint64_t sched_tiles;  // schedules [nc][sched_tiles][H][32]
   const uint32_t* tiled; // wave-local tiled demands
   GenParams gen;
-  double* totals;        // [nc][m_total] or null
-  uint8_t* evaluated;    // [nc][m_total] or null
-  uint8_t* deliver;      // FULL tiled [nc][m/32][H][32]
+  double* totals;        // or null
+  uint8_t* evaluated;    // or null
+  uint8_t* deliver;      // FULL tiled
   int32_t* quantity;
   int32_t* end_inventory;
   int32_t* route_option;
@@ -88,7 +93,7 @@ __device__ __forceinline__ void dsirp_write_schedule(const DsirpArgs& a, uint32_
                                                      int U, int I0, int H, bool ok,
                                                      uint32_t mask, const int (&opt)[HMAX],
                                                      const int (&dem)[HMAX]) {
-  const uint64_t tiles = (a.m_total + 31) / 32;
+  const uint64_t tiles = a.sched_tiles;
   const uint64_t ob = ((static_cast<uint64_t>(c) * tiles + (w >> 5)) * H) * kTile + (w & 31);
   int inv = I0;
 #pragma unroll
@@ -240,8 +245,8 @@ __device__ __forceinline__ double dsirp_unit_fp64(const DsirpArgs& a, const Cust
   }
   ok = ts >= 0;
   if (!ok) total = kInfD;  // logic_error slot: evaluated = 0
-  if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-  if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+  if (a.totals) a.totals[static_cast<uint64_t>(c) * a.tot_stride + w] = total;
+  if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.ev_stride + w] = ok ? 1 : 0;
   if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
   return total;
 }
@@ -446,8 +451,8 @@ dsirp_int_kernel(DsirpArgs a) {
         }
         ok = ts >= 0;  // always: the no-delivery chain keeps a state alive
         total = ok ? static_cast<double>(tv) * inv_scale : kInfD;
-        if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-        if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+        if (a.totals) a.totals[static_cast<uint64_t>(c) * a.tot_stride + w] = total;
+        if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.ev_stride + w] = ok ? 1 : 0;
         if (FULL) dsirp_write_schedule<HMAX>(a, c, w, U, cd.I0, H, ok, ok ? sel_u<K>(dm, ts) : 0u, opt, dem);
       }
     }
@@ -646,8 +651,8 @@ dsirp_fast_kernel(DsirpArgs a) {
             ok = tv < kInfD;  // all-infinite: the reference's logic_error slot
             total = ok ? tv : kInfD;
           }
-          if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-          if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+          if (a.totals) a.totals[static_cast<uint64_t>(c) * a.tot_stride + w] = total;
+          if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.ev_stride + w] = ok ? 1 : 0;
           if constexpr (FULL)
             dsirp_write_schedule<H>(a, c, w, U, cd.I0, H, ok, sel_u<K>(dm, ts), opt, dem);
         }

@@ -112,11 +112,11 @@ dsirp_dense_kernel(DsirpArgs a, char* scratch, uint32_t max_states) {
       }
     }
     const bool ok = ts >= 0;  // else the reference's logic_error: evaluated = 0
-    if (a.totals) a.totals[static_cast<uint64_t>(c) * a.m_total + w] = total;
-    if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.m_total + w] = ok ? 1 : 0;
+    if (a.totals) a.totals[static_cast<uint64_t>(c) * a.tot_stride + w] = total;
+    if (a.evaluated) a.evaluated[static_cast<uint64_t>(c) * a.ev_stride + w] = ok ? 1 : 0;
     if (FULL) {
       // assemble_schedule: backtrack, then quantities forward (tiled outputs)
-      const uint64_t tiles = (a.m_total + 31) / 32;
+      const uint64_t tiles = a.sched_tiles;
       const uint64_t ob = ((static_cast<uint64_t>(c) * tiles + (w >> 5)) * H) * kTile + (w & 31);
       int j = ts;
       for (int t = H - 1; t >= 0; --t) {

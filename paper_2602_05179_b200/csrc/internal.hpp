@@ -61,6 +61,7 @@ enum ScratchSlot {
   kScrAgg,             // raw aggregates [k]
   kScrTotals,          // per-scenario totals when the caller wants host copies
   kScrOut1, kScrOut2, kScrOut3, kScrOut4, kScrOut5, kScrOut6,
+  kScrOut7, kScrOut8, kScrOut9,
   kScrOverflow,        // general staging (DSIRP reference-layout outputs)
   kScrHandoff,         // split hand-off bitmap + list: owned by split_eval
                        // only (the bitmap must stay all-zero at rest)
@@ -102,6 +103,17 @@ struct scendp_ctx {
   int nranks = 1, rank = 0;
 
   void* scratch_get(int slot, uint64_t bytes);
+  void scratch_free(int slot);
+  uint64_t scratch_total = 0;  // device bytes held in scratch blocks
+  uint64_t scratch_peak = 0;   // high-water mark of scratch_total
+  uint64_t oom_retries = 0;    // waves halved after cudaErrorMemoryAllocation
+  uint64_t last_wave = 0;      // wave size of the last split / DSIRP call
+  // Scenarios per wave from the device footprint model: fixed + per_scenario
+  // x wave must fit the budget -- scratch_limit if set, else the scratch
+  // already held plus the free device memory (less 1/16 headroom); also
+  // capped by max_batch.  Tile-aligned, at least one tile.
+  uint64_t wave_for_model(uint64_t m, uint64_t fixed, uint64_t per_scenario,
+                          uint64_t* budget_out);
   // kernel timing helpers (no-ops unless SCENDP_CTX_KERNEL_TIMING)
   int timing_begin(int kind);
   void timing_end(int token);
@@ -210,5 +222,13 @@ struct GenParamsHost;
 const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
                                 bool allow_fused, void* gen_params_out,
                                 bool* fused);
+
+// Device bytes stage_scenarios needs for `sc` (allow_fused = true): per
+// scenario of a wave (returned) and independent of the wave (*fixed).
+uint64_t stage_footprint(const scendp_scenarios* sc, uint64_t* fixed);
+// Reserve stage_scenarios' scratch for a wave of `mw` scenarios of `sc`.
+void reserve_stage(scendp_ctx* ctx, const scendp_scenarios* sc, uint64_t mw);
+// Free the per-wave scratch blocks (out-of-memory retry with a smaller wave).
+void release_wave_scratch(scendp_ctx* ctx);
 
 }  // namespace scendp_host

@@ -283,12 +283,22 @@ static void parallel_copy(char* dst, const char* src, uint64_t bytes, int thread
 // driver-staged copy from pageable memory runs at ~11 GB/s).  Demands below
 // 256 are narrowed to one byte while staging (1/4 of the PCIe bytes, widened
 // by the tiling kernel); a chunk with a wider value is copied as is.
-void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, uint64_t count,
-                           uint32_t* dst) {
+// Scenarios per staging chunk of a pageable upload (whole tiles, ~64 MB).
+uint64_t pageable_chunk(uint64_t rows, uint64_t count) {
   constexpr uint64_t kChunkBytes = 64ull << 20;
   const uint64_t col_bytes = rows * 4;
-  uint64_t chunk = std::max<uint64_t>(32, (kChunkBytes / col_bytes) & ~uint64_t{31});
-  chunk = std::min(chunk, (count + 31) & ~uint64_t{31});
+  const uint64_t chunk = std::max<uint64_t>(32, (kChunkBytes / col_bytes) & ~uint64_t{31});
+  return std::min(chunk, (count + 31) & ~uint64_t{31});
+}
+
+uint64_t pageable_chunk_bytes(uint64_t rows, uint64_t count) {
+  return pageable_chunk(rows, count) * rows * 4;
+}
+
+void upload_pageable_tiled(scendp_ctx* ctx, const uint32_t* src, uint64_t rows, uint64_t count,
+                           uint32_t* dst) {
+  const uint64_t col_bytes = rows * 4;
+  const uint64_t chunk = pageable_chunk(rows, count);
   const uint64_t stage_bytes = chunk * col_bytes;
   char* pin[2] = {static_cast<char*>(ctx->pinned_stage(0, stage_bytes)),
                   static_cast<char*>(ctx->pinned_stage(1, stage_bytes))};
@@ -404,6 +414,56 @@ const uint32_t* stage_scenarios(scendp_ctx* ctx, const scendp_scenarios* sc,
     default:
       fail(SCENDP_ERR_INVALID_ARGUMENT, "unknown scenario mem_kind");
   }
+}
+
+uint64_t stage_footprint(const scendp_scenarios* sc, uint64_t* fixed) {
+  const uint64_t rows = sc->rows;
+  *fixed = 0;
+  switch (sc->mem_kind) {
+    case SCENDP_MEM_GENERATED:
+      if (sc->dist && sc->dist->kind == SCENDP_DIST_TNORMAL) return 4 * rows;  // tiled set
+      if (sc->dist && sc->dist->kind == SCENDP_DIST_POISSON) *fixed = 64 << 10;  // CDF table
+      return 0;  // generated inside the DP kernels
+    case SCENDP_MEM_HOST:
+      // page-locked or small (<= 16 MB): one staging copy + the tiled set;
+      // larger pageable sets: the tiled set + one ~64 MB staging chunk
+      if ((sc->data && mapped_host_alias(const_cast<uint32_t*>(sc->data))) ||
+          rows * sc->count * 4 <= (16ull << 20))
+        return 8 * rows;
+      *fixed = pageable_chunk_bytes(rows, sc->count);
+      return 4 * rows;
+    case SCENDP_MEM_DEVICE:
+      return 4 * rows;
+    default:
+      return 0;
+  }
+}
+
+void reserve_stage(scendp_ctx* ctx, const scendp_scenarios* sc, uint64_t mw) {
+  const uint64_t rows = sc->rows, tiled = scendp_tiled_bytes(rows, mw);
+  switch (sc->mem_kind) {
+    case SCENDP_MEM_GENERATED:
+      if (sc->dist && sc->dist->kind == SCENDP_DIST_TNORMAL) ctx->scratch_get(kScrScenarios, tiled);
+      return;
+    case SCENDP_MEM_HOST: {
+      ctx->scratch_get(kScrScenarios, tiled);
+      const bool direct = (sc->data && mapped_host_alias(const_cast<uint32_t*>(sc->data))) ||
+                          rows * mw * 4 <= (16ull << 20);
+      ctx->scratch_get(kScrStaging, direct ? rows * mw * 4 : pageable_chunk_bytes(rows, mw));
+      return;
+    }
+    case SCENDP_MEM_DEVICE:
+      ctx->scratch_get(kScrScenarios, tiled);
+      return;
+    default:
+      return;
+  }
+}
+
+void release_wave_scratch(scendp_ctx* ctx) {
+  for (int s : {kScrScenarios, kScrStaging, kScrTotals, kScrOut1, kScrOut2, kScrOut3, kScrOut4,
+                kScrOut5, kScrOut6, kScrOut7, kScrOut8, kScrOut9, kScrOverflow, kScrHandoff})
+    ctx->scratch_free(s);
 }
 
 }  // namespace scendp_host

@@ -769,6 +769,116 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     launch_overflow_pass<FULL, KSRC>(ctx, a, generic_scratch, generic_stride, generic_blocks);
 }
 
+// Generic (hand-off) kernel scratch: latency-bound (dependent global-scratch
+// accesses), so as many threads as ~64 MB of scratch allows, 2..8 CTAs/SM.
+struct GenericLayout {
+  uint64_t stride;
+  int blocks;
+  uint64_t bytes() const { return stride * static_cast<uint64_t>(blocks) * kGenericThreads; }
+};
+
+GenericLayout generic_layout(const scendp_ctx* ctx, int n) {
+  const uint64_t n1 = static_cast<uint64_t>(n) + 1;
+  GenericLayout g;
+  g.stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
+  const uint64_t per_sm = static_cast<uint64_t>(ctx->sm_count) * kGenericThreads * g.stride;
+  g.blocks = ctx->sm_count *
+             static_cast<int>(std::clamp<uint64_t>((64ull << 20) / per_sm, kGenericBlocksPerSm, 8));
+  return g;
+}
+
+// Hand-off list capacity and bitmap bytes of a wave of `items` items.
+inline uint32_t handoff_cap(uint64_t items) {
+  return static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(items / 128, 1u << 16), 1u << 26));
+}
+inline uint64_t handoff_bits_bytes(uint64_t items) {
+  return (((items + 31) / 32) * 4 + 15) & ~uint64_t{15};
+}
+
+// Device footprint model of one scendp_split_eval call (the device analogue
+// of split_per_scenario_bytes / adjust_batch_size, split.cpp:287-301,
+// engine.cpp:7-20): bytes that do not depend on the wave, bytes per
+// scenario of a wave, and the wave the context's budget allows.  The terms
+// are exactly the scratch blocks reserve_split_wave requests.
+struct SplitFootprint {
+  uint64_t fixed = 0, per_scenario = 0, wave = 0, budget = 0;
+};
+
+SplitFootprint split_footprint(scendp_ctx* ctx, int n, uint32_t k, const scendp_scenarios* sc,
+                               uint32_t flags, const scendp_split_out* out, uint64_t table_bytes,
+                               const GenericLayout& gl) {
+  const uint64_t n1 = static_cast<uint64_t>(n) + 1, K = k;
+  const bool full = (flags & SCENDP_SPLIT_FULL) != 0;
+  const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+  SplitFootprint f;
+  f.fixed = table_bytes + K * sizeof(scendp_agg_raw) + 16 + gl.bytes() + (uint64_t{1} << 16) * 8;
+  uint64_t in_fixed = 0;
+  f.per_scenario = stage_footprint(sc, &in_fixed);
+  f.fixed += in_fixed;
+  f.per_scenario += K / 8 + 1 + K / 16 + 1;  // hand-off bitmap + list above its floor
+  if (out->totals && host_out && !mapped_host_alias(out->totals)) f.per_scenario += K * 8;
+  if (full && out->mem_kind != SCENDP_MEM_DEVICE_TILED) f.per_scenario += 12 * n1;  // tiled V, cuts
+  if (full && host_out) f.per_scenario += 12 * n1 + 5;  // reference-layout V, cuts; rc, feasible
+  f.wave = ctx->wave_for_model(sc->count, f.fixed, f.per_scenario, &f.budget);
+  return f;
+}
+
+// Scratch blocks of one split wave (reserved before its kernels run).
+struct SplitWaveBufs {
+  char* handoff = nullptr;
+  uint64_t bits_bytes = 0;
+  uint32_t ovf_cap = 0;
+  char* generic = nullptr;
+  double* totals = nullptr;
+  double* V = nullptr;
+  int32_t* cuts = nullptr;
+  double* V_ref = nullptr;
+  int32_t* C_ref = nullptr;
+  int32_t* rc = nullptr;
+  uint8_t* feas = nullptr;
+};
+
+SplitWaveBufs reserve_split_wave(scendp_ctx* ctx, int n, uint32_t k, const scendp_scenarios* sc,
+                                 bool full, const scendp_split_out* out, bool call_totals,
+                                 uint64_t table_bytes, const GenericLayout& gl, uint64_t mw,
+                                 uint64_t wave) {
+  (void)table_bytes;
+  const uint64_t n1 = static_cast<uint64_t>(n) + 1, tiles = (mw + 31) / 32;
+  const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
+  SplitWaveBufs b;
+  reserve_stage(ctx, sc, mw);
+  const uint64_t items = static_cast<uint64_t>(k) * std::max(mw, wave);
+  b.ovf_cap = handoff_cap(items);
+  b.bits_bytes = handoff_bits_bytes(items);
+  b.handoff = static_cast<char*>(ctx->scratch_get(kScrHandoff, b.bits_bytes + b.ovf_cap * 8ull));
+  b.generic = static_cast<char*>(ctx->scratch_get(kScrFallback, gl.bytes()));
+  if (out->totals && !call_totals)
+    b.totals = static_cast<double*>(ctx->scratch_get(kScrTotals, static_cast<uint64_t>(k) * mw * 8));
+  if (full && out->mem_kind != SCENDP_MEM_DEVICE_TILED) {
+    b.V = static_cast<double*>(ctx->scratch_get(kScrOut1, tiles * 32 * n1 * 8));
+    b.cuts = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, tiles * 32 * n1 * 4));
+  }
+  if (full && host_out) {
+    b.V_ref = static_cast<double*>(ctx->scratch_get(kScrOut5, mw * n1 * 8));
+    b.C_ref = static_cast<int32_t*>(ctx->scratch_get(kScrOut6, mw * n1 * 4));
+    b.rc = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, mw * 4));
+    b.feas = static_cast<uint8_t*>(ctx->scratch_get(kScrOut4, mw));
+  }
+  return b;
+}
+
+// Per-wave totals [k][mw] -> host [k][m] at column w0.
+void copy_totals_back(scendp_ctx* ctx, double* host, const double* wave_totals, uint32_t k,
+                      uint64_t m, uint64_t w0, uint64_t mw) {
+  if (k == 1 || mw == m) {
+    download(ctx, host + w0, wave_totals, static_cast<uint64_t>(k) * mw * 8);
+  } else {
+    CUDA_CHECK(cudaMemcpy2DAsync(host + w0, m * 8, wave_totals, mw * 8, mw * 8, k,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->stats.d2h_bytes += static_cast<uint64_t>(k) * mw * 8;
+  }
+}
+
 }  // namespace
 
 // SCENDP_HOST_TRACE=1: per-call host-side phase times (microseconds) on
@@ -880,90 +990,74 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     unsigned int* d_ovf_count = reinterpret_cast<unsigned int*>(aggbuf + k * sizeof(scendp_agg_raw));
     CUDA_CHECK(cudaMemsetAsync(aggbuf, 0, k * sizeof(scendp_agg_raw) + 16, ctx->stream));
 
-    // outputs: device destinations (caller's device buffers when tiled/device
-    // layout matches, else scratch)
+    // outputs: the caller's device buffers (tiled or reference layout) and
+    // page-locked host totals (stored by the kernels over PCIe) are written in
+    // place at each wave's offset; whatever is bound for pageable host memory
+    // goes through per-wave scratch and is copied back after its wave
     const bool out_dev_tiled = out->mem_kind == SCENDP_MEM_DEVICE_TILED;
     const bool out_dev_ref = out->mem_kind == SCENDP_MEM_DEVICE;
-    double* d_totals = nullptr;
-    // host totals in pinned memory: the kernels write them over PCIe directly
+    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
     double* zc_totals = nullptr;
-    if (out->totals && out->mem_kind == SCENDP_MEM_HOST)
-      zc_totals = static_cast<double*>(mapped_host_alias(out->totals));
-    if (out->totals) {
-      d_totals = (out_dev_tiled || out_dev_ref) ? out->totals
-                 : zc_totals                    ? zc_totals
-                                                : static_cast<double*>(ctx->scratch_get(kScrTotals, k * m * 8));
-    }
-    double* d_V = nullptr;
-    int32_t* d_cuts = nullptr;
-    int32_t* d_rc = nullptr;
-    uint8_t* d_feas = nullptr;
-    const uint64_t tiles = (m + 31) / 32;
-    if (full) {
-      if (out_dev_tiled) {
-        d_V = out->values;
-        d_cuts = out->cuts;
-      } else {
-        d_V = static_cast<double*>(ctx->scratch_get(kScrOut1, tiles * 32 * n1 * 8));
-        d_cuts = static_cast<int32_t*>(ctx->scratch_get(kScrOut2, tiles * 32 * n1 * 4));
-      }
-      if (out_dev_tiled || out_dev_ref) {
-        d_rc = out->route_count;
-        d_feas = out->feasible;
-      } else {
-        d_rc = static_cast<int32_t*>(ctx->scratch_get(kScrOut3, m * 4));
-        d_feas = static_cast<uint8_t*>(ctx->scratch_get(kScrOut4, m));
-      }
-    }
+    if (out->totals && host_out) zc_totals = static_cast<double*>(mapped_host_alias(out->totals));
+    double* call_totals = !out->totals ? nullptr : host_out ? zc_totals : out->totals;
 
-    // waves (BackendConfig::batch_size / memory_budget analogue)
-    uint64_t wave = ctx->wave_for(m, sc->mem_kind == SCENDP_MEM_DEVICE_TILED ? 0 : 4ull * n);
-    if (wave == 0) wave = 32;
-
-    // overflow items for the generic kernel: a list sized for ~1% of the
-    // wave's items (the rates seen at the BASELINE shapes are <= 0.3%), and a
-    // bitmap of every item for the rest -- kept all-zero at rest (the generic
-    // kernel clears what it processes; the bytes after it hold the list, so
-    // only the part known clean is skipped when it grows)
-    const uint64_t wave_items = static_cast<uint64_t>(k) * std::min(wave, std::max<uint64_t>(m, 1));
-    const uint32_t ovf_cap = static_cast<uint32_t>(
-        std::min<uint64_t>(std::max<uint64_t>(wave_items / 128, 1u << 16), 1u << 26));
-    const uint64_t bits_bytes = (((wave_items + 31) / 32) * 4 + 15) & ~uint64_t{15};
-    char* ovf = static_cast<char*>(ctx->scratch_get(kScrHandoff, bits_bytes + ovf_cap * 8ull));
-    if (ctx->scratch_gen[kScrHandoff] != ctx->ovf_gen) {
-      ctx->ovf_gen = ctx->scratch_gen[kScrHandoff];
-      ctx->ovf_clean = 0;
-    }
-    if (ctx->ovf_clean < bits_bytes)
-      CUDA_CHECK(cudaMemsetAsync(ovf + ctx->ovf_clean, 0, bits_bytes - ctx->ovf_clean, ctx->stream));
-    // dirty until this call's hand-off passes are enqueued: an error exit in
-    // between leaves the bitmap to be cleared by the next call
-    ctx->ovf_clean = 0;
-    const uint64_t ovf_clean_after = bits_bytes;
-    auto* d_ovf_bits = reinterpret_cast<uint32_t*>(ovf);
-    auto* d_ovf_items = reinterpret_cast<unsigned long long*>(ovf + bits_bytes);
-    // generic path: latency-bound (dependent global-scratch accesses), so as
-    // many threads as ~64 MB of scratch allows, 2..8 CTAs per SM
-    const uint64_t generic_stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
-    const uint64_t per_sm = static_cast<uint64_t>(ctx->sm_count) * kGenericThreads * generic_stride;
-    const int generic_blocks =
-        ctx->sm_count * static_cast<int>(std::clamp<uint64_t>((64ull << 20) / per_sm,
-                                                              kGenericBlocksPerSm, 8));
-    char* gen_scratch = static_cast<char*>(
-        ctx->scratch_get(kScrFallback, generic_stride * generic_blocks * kGenericThreads));
+    // device footprint model (fixed + per-scenario bytes) -> wave size under
+    // the context's budget (scratch_limit, else the free device memory)
+    const GenericLayout gl = generic_layout(ctx, n);
+    const SplitFootprint fpm = split_footprint(ctx, n, k, sc, flags, out, L.bytes, gl);
+    uint64_t wave = fpm.wave;
 
     // a call that syncs anyway, in one wave, cost-only, on one GPU reads the
     // hand-off counter back with the aggregates and skips the (almost
     // always empty) overflow pass -- one launch less per call
-    const bool host_out = out->mem_kind == SCENDP_MEM_HOST;
     const bool want_agg = out->agg || out->agg_raw;
     const bool syncs = !(flags & SCENDP_ASYNC) || (host_out && out->totals) || want_agg;
-    const bool defer_ovf = syncs && !full && wave >= m && !ctx->nccl_comm;
+    bool defer_ovf = false;
     SplitArgs last_a{};
     int last_src = kSrcTiled;
-    for (uint64_t w0 = 0; w0 < m || (m == 0 && w0 == 0); w0 += wave) {
-      if (m == 0) break;
+    char* gen_scratch = nullptr;
+    // hand-off bitmap bytes known all-zero (in stream order); the context's
+    // record stays "dirty" until every hand-off pass of the call is enqueued,
+    // so an error exit in between leaves the bitmap to the next call's memset
+    uint64_t known_clean = ctx->scratch_gen[kScrHandoff] == ctx->ovf_gen ? ctx->ovf_clean : 0;
+    ctx->ovf_clean = 0;
+    double* w_tot = nullptr;  // per-wave scratch totals [k][mw] (pageable host totals)
+    for (uint64_t w0 = 0; w0 < m;) {
       const uint64_t mw = std::min(wave, m - w0);
+      // every scratch block of this wave is reserved before its kernels are
+      // enqueued: out of device memory halves the wave and retries
+      SplitWaveBufs wb;
+      try {
+        // (hand-off bitmap and list sized for the full wave, so every wave
+        // of the call places its list at the same offset)
+        wb = reserve_split_wave(ctx, n, k, sc, full, out, call_totals != nullptr, L.bytes, gl, mw,
+                                wave);
+      } catch (const Error& e) {
+        if (e.status != SCENDP_ERR_OUT_OF_MEMORY || wave <= 32) throw;
+        wave = std::max<uint64_t>(32, (wave / 2) & ~uint64_t{31});
+        release_wave_scratch(ctx);
+        ++ctx->oom_retries;
+        continue;
+      }
+      ctx->last_wave = wave;
+      gen_scratch = wb.generic;
+      w_tot = wb.totals;
+      // overflow items for the generic kernel: a list sized for ~1% of the
+      // wave's items (the rates seen at the BASELINE shapes are <= 0.3%), and
+      // a bitmap of every item for the rest -- kept all-zero at rest (the
+      // generic kernel clears what it processes; the bytes after it hold the
+      // list, so only the part known clean is skipped when it grows)
+      if (ctx->scratch_gen[kScrHandoff] != ctx->ovf_gen) {  // a new block
+        ctx->ovf_gen = ctx->scratch_gen[kScrHandoff];
+        known_clean = 0;
+      }
+      if (known_clean < wb.bits_bytes)
+        CUDA_CHECK(cudaMemsetAsync(wb.handoff + known_clean, 0, wb.bits_bytes - known_clean,
+                                   ctx->stream));
+      // after this wave's pass: its bits are clear, its list (right after
+      // the bitmap) is not
+      known_clean = wb.bits_bytes;
+
       scendp_scenarios sw = *sc;
       sw.count = mw;
       sw.first_index = sc->first_index + w0;
@@ -981,8 +1075,10 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.beta = inst->penalty_beta;
       a.k = k;
       a.m_wave = mw;
-      a.w_base = w0;
-      a.m_total = m;
+      // outputs are addressed wave-locally: call-level destinations are
+      // passed at the wave's offset (waves start on 32-scenario tiles)
+      a.w_base = 0;
+      a.m_total = call_totals ? m : mw;
       a.dist = d_dist;
       a.ret = d_ret;
       a.c0 = d_c0;
@@ -1010,29 +1106,53 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.f0i = reinterpret_cast<const int32_t*>(dtab + o_f0i);
       a.tiled = tiled;
       a.gen = gp;
-      a.totals = d_totals;
-      a.V = d_V;
-      a.cuts = d_cuts;
-      a.route_count = d_rc;
-      a.feasible = d_feas;
+      a.totals = !out->totals ? nullptr : call_totals ? call_totals + w0 : wb.totals;
+      if (full) {
+        const uint64_t toff = (w0 / 32) * n1 * 32;
+        a.V = out_dev_tiled ? out->values + toff : wb.V;
+        a.cuts = out_dev_tiled ? out->cuts + toff : wb.cuts;
+        a.route_count = host_out ? wb.rc : out->route_count + w0;
+        a.feasible = host_out ? wb.feas : out->feasible + w0;
+      }
       a.agg = d_agg;
       a.ovf_count = d_ovf_count;
-      a.ovf_items = d_ovf_items;
-      a.ovf_cap = ovf_cap;
-      a.ovf_bits = d_ovf_bits;
+      a.ovf_items = reinterpret_cast<unsigned long long*>(wb.handoff + wb.bits_bytes);
+      a.ovf_cap = wb.ovf_cap;
+      a.ovf_bits = reinterpret_cast<uint32_t*>(wb.handoff);
       if (w0 > 0) CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
       const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
       last_a = a;
       last_src = u32 ? kSrcGenU32 : fused ? kSrcGen : kSrcTiled;
+      defer_ovf = syncs && !full && w0 == 0 && mw == m && !ctx->nccl_comm;
+      const uint64_t gstride = gl.stride;
+      const int gblocks = gl.blocks;
       if (full) {
-        if (u32) launch_wave<true, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
-        else if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
-        else launch_wave<true, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks);
+        if (u32) launch_wave<true, kSrcGenU32>(ctx, a, linear, gen_scratch, gstride, gblocks);
+        else if (fused) launch_wave<true, kSrcGen>(ctx, a, linear, gen_scratch, gstride, gblocks);
+        else launch_wave<true, kSrcTiled>(ctx, a, linear, gen_scratch, gstride, gblocks);
       } else {
-        if (u32) launch_wave<false, kSrcGenU32>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
-        else if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
-        else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, generic_stride, generic_blocks, defer_ovf);
+        if (u32) launch_wave<false, kSrcGenU32>(ctx, a, linear, gen_scratch, gstride, gblocks, defer_ovf);
+        else if (fused) launch_wave<false, kSrcGen>(ctx, a, linear, gen_scratch, gstride, gblocks, defer_ovf);
+        else launch_wave<false, kSrcTiled>(ctx, a, linear, gen_scratch, gstride, gblocks, defer_ovf);
       }
+      // per-wave copies back (a deferred hand-off pass -- single wave only --
+      // still writes totals: that wave's copy follows it below)
+      if (!defer_ovf && out->totals && !call_totals) copy_totals_back(ctx, out->totals, wb.totals, k, m, w0, mw);
+      if (full && !out_dev_tiled) {
+        // tiled -> reference layout [mw][n+1], into the caller's device
+        // buffer at the wave's rows or through scratch to host memory
+        double* V_ref = out_dev_ref ? out->values + w0 * n1 : wb.V_ref;
+        int32_t* C_ref = out_dev_ref ? out->cuts + w0 * n1 : wb.C_ref;
+        launch_from_tiled<double>(ctx, wb.V, n1, mw, V_ref);
+        launch_from_tiled<int32_t>(ctx, wb.cuts, n1, mw, C_ref);
+        if (host_out) {
+          download(ctx, out->values + w0 * n1, V_ref, mw * n1 * 8);
+          download(ctx, out->cuts + w0 * n1, C_ref, mw * n1 * 4);
+          ctx->copy(out->route_count + w0, wb.rc, mw * 4, cudaMemcpyDeviceToHost);
+          ctx->copy(out->feasible + w0, wb.feas, mw, cudaMemcpyDeviceToHost);
+        }
+      }
+      w0 += mw;
     }
 
     trace.mark("launch");
@@ -1046,37 +1166,22 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       uint32_t handed_off = 0;
       std::memcpy(&handed_off, h_aggc + agg_bytes, 4);
       if (handed_off > 0) {
+        const uint64_t gstride = gl.stride;
+        const int gblocks = gl.blocks;
         if (last_src == kSrcGenU32)
-          launch_overflow_pass<false, kSrcGenU32>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+          launch_overflow_pass<false, kSrcGenU32>(ctx, last_a, gen_scratch, gstride, gblocks);
         else if (last_src == kSrcGen)
-          launch_overflow_pass<false, kSrcGen>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+          launch_overflow_pass<false, kSrcGen>(ctx, last_a, gen_scratch, gstride, gblocks);
         else
-          launch_overflow_pass<false, kSrcTiled>(ctx, last_a, gen_scratch, generic_stride, generic_blocks);
+          launch_overflow_pass<false, kSrcTiled>(ctx, last_a, gen_scratch, gstride, gblocks);
         h_aggc = nullptr;  // aggregates changed: read them again below
       }
+      if (out->totals && !call_totals) copy_totals_back(ctx, out->totals, w_tot, k, m, 0, m);
     }
-    ctx->ovf_clean = ovf_clean_after;  // every hand-off pass is enqueued
+    ctx->ovf_clean = known_clean;  // every hand-off pass is enqueued
     // the single collective: per-candidate raw aggregates, K x 16 u64
     ctx->allreduce_agg(d_agg, static_cast<uint64_t>(k) * kAggWords);
-
-    // copies back
-    if (out->totals && host_out) {
-      if (zc_totals) ctx->stats.d2h_bytes += k * m * 8;  // stored by the kernels
-      else download(ctx, out->totals, d_totals, k * m * 8);
-    }
-    if (full && !out_dev_tiled) {
-      // tiled -> reference layout [m][n+1]
-      double* V_ref = out_dev_ref ? out->values : static_cast<double*>(ctx->scratch_get(kScrOut5, m * n1 * 8));
-      launch_from_tiled<double>(ctx, d_V, n1, m, V_ref);
-      if (host_out) download(ctx, out->values, V_ref, m * n1 * 8);
-      int32_t* C_ref = out_dev_ref ? out->cuts : static_cast<int32_t*>(ctx->scratch_get(kScrOut6, m * n1 * 4));
-      launch_from_tiled<int32_t>(ctx, d_cuts, n1, m, C_ref);
-      if (host_out) {
-        download(ctx, out->cuts, C_ref, m * n1 * 4);
-        ctx->copy(out->route_count, d_rc, m * 4, cudaMemcpyDeviceToHost);
-        ctx->copy(out->feasible, d_feas, m, cudaMemcpyDeviceToHost);
-      }
-    }
+    if (out->totals && zc_totals) ctx->stats.d2h_bytes += k * m * 8;  // stored by the kernels
     scendp_agg_raw* h_raw = nullptr;
     if (want_agg) {
       h_raw = static_cast<scendp_agg_raw*>(ctx->pinned_agg(agg_bytes + 16));
@@ -1088,5 +1193,23 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       if (out->agg_raw) std::memcpy(out->agg_raw, h_raw, k * sizeof(scendp_agg_raw));
       if (out->agg) finalize_agg(h_raw, 1, k, out->agg);
     }
+  });
+}
+
+extern "C" scendp_status scendp_split_footprint(scendp_ctx* ctx, const scendp_routing* inst,
+                                                uint32_t k_tours, const scendp_scenarios* sc,
+                                                uint32_t flags, const scendp_split_out* out,
+                                                scendp_footprint* fp) {
+  return guard([&] {
+    if (!ctx || !inst || !sc || !out || !fp) fail(SCENDP_ERR_INVALID_ARGUMENT, "null argument");
+    if (inst->n < 1 || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need n >= 1 and a tour");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    const TableLayout L(inst->n, k_tours);
+    const SplitFootprint f = split_footprint(ctx, inst->n, k_tours, sc, flags, out, L.bytes,
+                                             generic_layout(ctx, inst->n));
+    fp->fixed_bytes = f.fixed;
+    fp->per_scenario_bytes = f.per_scenario;
+    fp->wave = f.wave;
+    fp->budget = f.budget;
   });
 }
