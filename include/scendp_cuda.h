@@ -332,6 +332,8 @@ typedef struct {
   uint64_t device_total;
   uint64_t oom_retries;    /* waves halved after an allocation failure */
   uint64_t last_wave;      /* wave size of the last split / DSIRP call */
+  uint64_t tnormal_host_columns; /* tnormal columns the device could not
+                              certify, regenerated with the host's libm */
 } scendp_memory_info;
 
 scendp_status scendp_ctx_memory(scendp_ctx* ctx, scendp_memory_info* info);

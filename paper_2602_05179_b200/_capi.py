@@ -118,7 +118,8 @@ class Footprint(C.Structure):
 class MemoryInfo(C.Structure):
     _fields_ = [("scratch_bytes", C.c_uint64), ("scratch_peak", C.c_uint64),
                 ("device_free", C.c_uint64), ("device_total", C.c_uint64),
-                ("oom_retries", C.c_uint64), ("last_wave", C.c_uint64)]
+                ("oom_retries", C.c_uint64), ("last_wave", C.c_uint64),
+                ("tnormal_host_columns", C.c_uint64)]
 
 
 # Every symbol include/scendp_cuda.h declares, with its ctypes signature.

@@ -583,6 +583,7 @@ scendp_status scendp_ctx_memory(scendp_ctx* ctx, scendp_memory_info* info) {
     info->device_total = tot;
     info->oom_retries = ctx->oom_retries;
     info->last_wave = ctx->last_wave;
+    info->tnormal_host_columns = ctx->tnormal_host_columns;
   });
 }
 

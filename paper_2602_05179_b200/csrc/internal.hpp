@@ -108,6 +108,7 @@ struct scendp_ctx {
   uint64_t scratch_peak = 0;   // high-water mark of scratch_total
   uint64_t oom_retries = 0;    // waves halved after cudaErrorMemoryAllocation
   uint64_t last_wave = 0;      // wave size of the last split / DSIRP call
+  uint64_t tnormal_host_columns = 0;  // tnormal columns resolved on the host
   // Scenarios per wave from the device footprint model: fixed + per_scenario
   // x wave must fit the budget -- scratch_limit if set, else the scratch
   // already held plus the free device memory (less 1/16 headroom); also

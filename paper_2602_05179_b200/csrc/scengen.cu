@@ -10,6 +10,7 @@
 // is generated sequentially per column (one thread per scenario).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -59,15 +60,51 @@ gen_counter_kernel(GenParams g, uint64_t rows, uint64_t count, uint32_t* out) {
 
 // tnormal (scenario.cpp:30-39): Box-Muller, llround, <= 64 rejections, then
 // clamp(llround(mean)).  No FMA contraction (built with -fmad=false).
+//
+// Exactness by construction.  The reference's value depends on glibc's log
+// and cos, which CUDA's libm does not reproduce bit for bit.  Every draw
+// therefore also computes an interval certain to contain glibc's
+// mean + stddev * z: log and cos are each within 2^-46 relative of the
+// device's results (CUDA: <= 1 and 2 ulp; glibc: <= 1 ulp; 2^-46 is 64
+// ulp), and the remaining operations (-2 x, sqrt, product, stddev * z,
+// mean + ...) are monotone, so directed-rounding bounds carry through.  When
+// llround of both ends agree, that integer is the reference's (and the
+// rejection decision with it).  A column with any draw whose interval
+// straddles a rounding boundary (about 1e-13 per draw) is listed for the
+// host, which regenerates that column with the reference's own arithmetic
+// (glibc, tnormal_column_host) and writes it over the device's.
+__device__ __forceinline__ bool tnormal_draw(double u1, double u2, double mean, double stddev,
+                                             long long& r) {
+  const double two_pi = 2.0 * 0x1.921fb54442d18p+1;  // 2.0 * std::numbers::pi
+  const double L = -2.0 * log(u1);
+  const double c = cos(two_pi * u2);
+  const double z = sqrt(L) * c;
+  r = llround(mean + stddev * z);
+  constexpr double e = 0x1p-46;
+  const double Slo = __dsqrt_rn(__dmul_rd(L, 1.0 - e)), Shi = __dsqrt_rn(__dmul_ru(L, 1.0 + e));
+  const double ce = __dmul_ru(fabs(c), e);
+  const double clo = __dsub_rd(c, ce), chi = __dadd_ru(c, ce);
+  const double zlo = fmin(fmin(__dmul_rd(Slo, clo), __dmul_rd(Slo, chi)),
+                          fmin(__dmul_rd(Shi, clo), __dmul_rd(Shi, chi)));
+  const double zhi = fmax(fmax(__dmul_ru(Slo, clo), __dmul_ru(Slo, chi)),
+                          fmax(__dmul_ru(Shi, clo), __dmul_ru(Shi, chi)));
+  const long long rlo = llround(__dadd_rn(mean, __dmul_rn(stddev, zlo)));
+  const long long rhi = llround(__dadd_rn(mean, __dmul_rn(stddev, zhi)));
+  return rlo == rhi;
+}
+
 __global__ void __launch_bounds__(kGenThreads)
 gen_tnormal_kernel(int64_t lo, int64_t hi, double mean, double stddev,
                    uint64_t seed, uint64_t first_index, uint64_t rows,
-                   uint64_t count, uint32_t* out) {
+                   uint64_t count, uint32_t* out, unsigned int* n_amb,
+                   unsigned long long* amb, uint32_t amb_cap, uint32_t force_every) {
   const uint64_t w = blockIdx.x * uint64_t(kGenThreads) + threadIdx.x;
   if (w >= count) return;
   uint64_t st = derive_stream(seed, kStreamScenario, first_index + w);
   uint32_t* dst = out + (w >> 5) * rows * kTile + (w & 31);
-  const double two_pi = 2.0 * 0x1.921fb54442d18p+1;  // 2.0 * std::numbers::pi
+  // SCENDP_TNORMAL_HOST_EVERY=k (tests): every k-th column takes the host
+  // path as if ambiguous
+  bool certain = !(force_every && (first_index + w) % force_every == 0);
   for (uint64_t r = 0; r < rows; ++r) {
     uint32_t v = 0;
     bool done = false;
@@ -78,8 +115,8 @@ gen_tnormal_kernel(int64_t lo, int64_t hi, double mean, double stddev,
       st += kGamma;
       const double u1 = static_cast<double>((x1 >> 11) + 1) * 0x1.0p-53;
       const double u2 = static_cast<double>((x2 >> 11) + 1) * 0x1.0p-53;
-      const double z = sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
-      const long long rr = llround(mean + stddev * z);
+      long long rr;
+      certain &= tnormal_draw(u1, u2, mean, stddev, rr);
       if (rr >= lo && rr <= hi) {
         v = static_cast<uint32_t>(rr);
         done = true;
@@ -91,6 +128,10 @@ gen_tnormal_kernel(int64_t lo, int64_t hi, double mean, double stddev,
       v = static_cast<uint32_t>(rr);
     }
     dst[r * kTile] = v;
+  }
+  if (!certain) {
+    const unsigned int slot = atomicAdd(n_amb, 1u);
+    if (slot < amb_cap) amb[slot] = w;
   }
 }
 
@@ -188,6 +229,34 @@ GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_
   return g;
 }
 
+// One tnormal column with the reference's own arithmetic (SplitMix64 over
+// derive_stream(seed, kStreamScenario, w), DistributionSpec::sample,
+// scenario.cpp:22-40; glibc log / cos / sqrt / llround): the host side of
+// the certified generator above.
+void tnormal_column_host(const scendp_dist* d, uint64_t w, uint64_t rows, uint32_t* col) {
+  uint64_t st = derive_stream(d->seed, kStreamScenario, w);
+  auto next_unit = [&st] {
+    const uint64_t x = mix64(st);
+    st += kGamma;
+    return static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
+  };
+  const double two_pi = 2.0 * 0x1.921fb54442d18p+1;
+  for (uint64_t r = 0; r < rows; ++r) {
+    bool done = false;
+    for (int attempt = 0; attempt < 64 && !done; ++attempt) {
+      const double u1 = next_unit();
+      const double u2 = next_unit();
+      const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(two_pi * u2);
+      const long long rr = std::llround(d->mean + d->stddev * z);
+      if (rr >= d->lo && rr <= d->hi) {
+        col[r] = static_cast<uint32_t>(rr);
+        done = true;
+      }
+    }
+    if (!done) col[r] = static_cast<uint32_t>(std::clamp<long long>(std::llround(d->mean), d->lo, d->hi));
+  }
+}
+
 void launch_generate_tiled(scendp_ctx* ctx, const scendp_dist* d, uint64_t rows,
                            uint64_t w0, uint64_t count, uint32_t* out) {
   if (count == 0) return;
@@ -195,8 +264,44 @@ void launch_generate_tiled(scendp_ctx* ctx, const scendp_dist* d, uint64_t rows,
   const int tok = ctx->timing_begin(1);
   if (d->kind == SCENDP_DIST_TNORMAL) {
     check_dist(d);
+    constexpr uint32_t kAmbCap = 4096;
+    auto* amb = static_cast<char*>(ctx->scratch_get(kScrCdf, 16 + kAmbCap * 8ull));
+    CUDA_CHECK(cudaMemsetAsync(amb, 0, 16, ctx->stream));
+    static const uint32_t force_every = [] {
+      const char* e = std::getenv("SCENDP_TNORMAL_HOST_EVERY");
+      return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
+    }();
     gen_tnormal_kernel<<<blocks, kGenThreads, 0, ctx->stream>>>(
-        d->lo, d->hi, d->mean, d->stddev, d->seed, w0, rows, count, out);
+        d->lo, d->hi, d->mean, d->stddev, d->seed, w0, rows, count, out,
+        reinterpret_cast<unsigned int*>(amb), reinterpret_cast<unsigned long long*>(amb + 16),
+        kAmbCap, force_every);
+    CUDA_CHECK(cudaGetLastError());
+    ctx->timing_end(tok);
+    ctx->count_launch();
+    // columns the device could not certify: regenerate them on the host
+    // with the reference's arithmetic (all of them if the list overflowed)
+    uint32_t n_amb = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&n_amb, amb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (n_amb == 0) return;
+    std::vector<uint64_t> cols;
+    if (n_amb <= kAmbCap) {
+      cols.resize(n_amb);
+      CUDA_CHECK(cudaMemcpy(cols.data(), amb + 16, n_amb * 8ull, cudaMemcpyDeviceToHost));
+    } else {
+      cols.resize(count);
+      for (uint64_t w = 0; w < count; ++w) cols[w] = w;
+    }
+    std::vector<uint32_t> col(rows);
+    for (uint64_t w : cols) {
+      tnormal_column_host(d, w0 + w, rows, col.data());
+      // column w of the tiled layout: rows values 128 bytes apart
+      CUDA_CHECK(cudaMemcpy2DAsync(out + (w >> 5) * rows * kTile + (w & 31), kTile * 4, col.data(),
+                                   4, 4, rows, cudaMemcpyHostToDevice, ctx->stream));
+      CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // col is reused
+      ctx->tnormal_host_columns += 1;
+    }
+    return;
   } else {
     GenParams g = make_gen_params(ctx, d, w0);
     const size_t smem = g.kind == SCENDP_DIST_POISSON ? g.cdf_len * sizeof(double) : 0;
@@ -443,7 +548,10 @@ void reserve_stage(scendp_ctx* ctx, const scendp_scenarios* sc, uint64_t mw) {
   const uint64_t rows = sc->rows, tiled = scendp_tiled_bytes(rows, mw);
   switch (sc->mem_kind) {
     case SCENDP_MEM_GENERATED:
-      if (sc->dist && sc->dist->kind == SCENDP_DIST_TNORMAL) ctx->scratch_get(kScrScenarios, tiled);
+      if (sc->dist && sc->dist->kind == SCENDP_DIST_TNORMAL) {
+        ctx->scratch_get(kScrScenarios, tiled);
+        ctx->scratch_get(kScrCdf, 16 + 4096 * 8);  // uncertified-column list
+      }
       return;
     case SCENDP_MEM_HOST: {
       ctx->scratch_get(kScrScenarios, tiled);
