@@ -376,9 +376,24 @@ scendp_status scendp_nccl_unique_id(uint8_t out[SCENDP_NCCL_UNIQUE_ID_BYTES]);
 scendp_status scendp_comm_init_rank(scendp_ctx* ctx,
                                     const uint8_t id[SCENDP_NCCL_UNIQUE_ID_BYTES],
                                     int32_t nranks, int32_t rank);
-/* single process driving several devices (ncclCommInitAll) */
+/* single process driving several devices (ncclCommInitAll).  The contexts
+ * of such a group must be driven concurrently, each from its own host
+ * thread: a call on one context blocks until every rank joins its
+ * all-reduce, so one thread calling scendp_split_eval on context 0, then 1,
+ * ... deadlocks on context 0.  scendp_split_eval_multi / _dsirp_eval_multi
+ * do the threading: one host thread per context, each evaluating its shard
+ * (sc[i], out[i]); they return after every shard, with every context's
+ * aggregates all-reduced (identical on all of them). */
 scendp_status scendp_comm_init_all(scendp_ctx** ctxs, int32_t n);
 scendp_status scendp_comm_destroy(scendp_ctx* ctx);
+scendp_status scendp_split_eval_multi(scendp_ctx** ctxs, int32_t n, const scendp_routing* inst,
+                                      const int32_t* tours, uint32_t k_tours,
+                                      const scendp_scenarios* sc, uint32_t flags,
+                                      const scendp_split_out* out);
+scendp_status scendp_dsirp_eval_multi(scendp_ctx** ctxs, int32_t n,
+                                      const scendp_customer* customers, uint32_t n_customers,
+                                      const scendp_scenarios* sc, uint32_t flags,
+                                      const scendp_dsirp_out* out);
 
 /* ---- timing (bench) -----------------------------------------------------
  * CUDA events on the context stream. */

@@ -173,6 +173,12 @@ SIGNATURES = {
                                          C.POINTER(Scenarios), C.c_uint32, C.POINTER(DsirpOut),
                                          C.POINTER(Footprint)]),
     "scendp_ctx_memory": (C.c_int, [C.c_void_p, C.POINTER(MemoryInfo)]),
+    "scendp_split_eval_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(Routing),
+                                          C.c_void_p, C.c_uint32, C.POINTER(Scenarios),
+                                          C.c_uint32, C.POINTER(SplitOut)]),
+    "scendp_dsirp_eval_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32,
+                                          C.POINTER(Customer), C.c_uint32, C.POINTER(Scenarios),
+                                          C.c_uint32, C.POINTER(DsirpOut)]),
 }
 
 _lib = None

@@ -10,6 +10,7 @@
 
 #include <condition_variable>
 #include <exception>
+#include <functional>
 #include <thread>
 
 #include "common.cuh"
@@ -430,6 +431,27 @@ void scendp_ctx::agg_readback(void* host, const void* dev, uint64_t bytes) {
   }
 }
 
+// One host thread per context (the NCCL contract for a single-process
+// group): each evaluates its own shard; the first failure is reported.
+static scendp_status run_per_context(int32_t n,
+                                     const std::function<scendp_status(int32_t)>& call) {
+  return guard([&] {
+    if (n < 1) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one context");
+    std::vector<scendp_status> st(static_cast<size_t>(n), SCENDP_OK);
+    std::vector<std::string> msg(static_cast<size_t>(n));
+    std::vector<std::thread> th;
+    th.reserve(static_cast<size_t>(n));
+    for (int32_t i = 0; i < n; ++i)
+      th.emplace_back([&, i] {
+        st[i] = call(i);
+        if (st[i] != SCENDP_OK) msg[i] = scendp_last_error();  // thread-local
+      });
+    for (auto& t : th) t.join();
+    for (int32_t i = 0; i < n; ++i)
+      if (st[i] != SCENDP_OK) fail(st[i], "context " + std::to_string(i) + ": " + msg[i]);
+  });
+}
+
 // ---- C-ABI -------------------------------------------------------------------
 extern "C" {
 
@@ -647,6 +669,32 @@ scendp_status scendp_comm_init_all(scendp_ctx** ctxs, int32_t n) {
       ctxs[i]->force_overlap = std::getenv("SCENDP_OVERLAP_ALLREDUCE") != nullptr;
       ctxs[i]->rank = i;
     }
+  });
+}
+
+scendp_status scendp_split_eval_multi(scendp_ctx** ctxs, int32_t n, const scendp_routing* inst,
+                                      const int32_t* tours, uint32_t k_tours,
+                                      const scendp_scenarios* sc, uint32_t flags,
+                                      const scendp_split_out* out) {
+  if (!ctxs || !sc || !out) {
+    set_last_error("null contexts / scenarios / outputs");
+    return SCENDP_ERR_INVALID_ARGUMENT;
+  }
+  return run_per_context(n, [&](int32_t i) {
+    return scendp_split_eval(ctxs[i], inst, tours, k_tours, sc + i, flags, out + i);
+  });
+}
+
+scendp_status scendp_dsirp_eval_multi(scendp_ctx** ctxs, int32_t n,
+                                      const scendp_customer* customers, uint32_t n_customers,
+                                      const scendp_scenarios* sc, uint32_t flags,
+                                      const scendp_dsirp_out* out) {
+  if (!ctxs || !sc || !out) {
+    set_last_error("null contexts / scenarios / outputs");
+    return SCENDP_ERR_INVALID_ARGUMENT;
+  }
+  return run_per_context(n, [&](int32_t i) {
+    return scendp_dsirp_eval(ctxs[i], customers, n_customers, sc + i, flags, out + i);
   });
 }
 

@@ -110,3 +110,52 @@ print("overlap ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "overlap ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_multi_context_entry_points(oracle):
+    """scendp_split_eval_multi / scendp_dsirp_eval_multi: one host thread per
+    context of a scendp_comm_init_all group (the deadlock-free way to drive
+    one process's GPUs), each on its own scenario shard; here a one-device
+    group with the shard = the whole set, equal to the plain call."""
+    inst, tours, dem = _workload(oracle)
+    lib = A.load()
+    ctx = Context(0)
+    try:
+        want = ctx.split_eval(inst, tours, dem)
+        arr = (C.c_void_p * 1)(ctx.handle)
+        A.check(lib.scendp_comm_init_all(arr, 1))
+        dem_c = np.ascontiguousarray(dem, np.uint32)
+        sc = (A.Scenarios * 1)(A.Scenarios(A.MEM_HOST, dem_c.ctypes.data, dem.shape[1],
+                                           dem.shape[0], 0, None))
+        k, m = tours.shape[0], dem.shape[0]
+        totals = np.empty((k, m))
+        agg = (A.Agg * k)()
+        out = (A.SplitOut * 1)(A.SplitOut(A.MEM_HOST, totals.ctypes.data, None, None, None, None,
+                                          agg, None))
+        rinst = inst.as_c()
+        A.check(lib.scendp_split_eval_multi(arr, 1, C.byref(rinst), tours.ctypes.data, k, sc, 0,
+                                            out))
+        np.testing.assert_array_equal(totals, want["totals"])
+        assert [agg[i].finite_count for i in range(k)] == [a["finite_count"] for a in want["agg"]]
+        assert [agg[i].mean for i in range(k)] == [a["mean"] for a in want["agg"]]
+        H = 6
+        cust = Customer(U=60, I0=30, H=H, fixed=np.full((H, 2), 20.0), unit=np.full((H, 2), 0.5))
+        dd = np.ascontiguousarray(oracle.generate(UNIFORM, 0, 25, 3, H, 777), np.uint32)
+        plain = ctx.dsirp_eval([cust], dd)
+        carr = (A.Customer * 1)(cust.as_c())
+        sc2 = (A.Scenarios * 1)(A.Scenarios(A.MEM_HOST, dd.ctypes.data, H, dd.shape[0], 0, None))
+        tot2 = np.empty(dd.shape[0])
+        agg2 = (A.Agg * 1)()
+        out2 = (A.DsirpOut * 1)(A.DsirpOut(A.MEM_HOST, tot2.ctypes.data, None, None, None, None,
+                                           None, agg2, None))
+        A.check(lib.scendp_dsirp_eval_multi(arr, 1, carr, 1, sc2, 0, out2))
+        np.testing.assert_array_equal(tot2, plain["totals"][0])
+        assert agg2[0].mean == plain["agg"][0]["mean"]
+        # errors surface with the context index
+        bad = (A.Scenarios * 1)(A.Scenarios(A.MEM_HOST, dem_c.ctypes.data, 7, dem.shape[0], 0,
+                                            None))
+        st = lib.scendp_split_eval_multi(arr, 1, C.byref(rinst), tours.ctypes.data, k, bad, 0, out)
+        assert st == 1 and b"context 0" in lib.scendp_last_error()
+        A.check(lib.scendp_comm_destroy(ctx.handle))
+    finally:
+        ctx.close()
