@@ -16,6 +16,7 @@ using namespace scendp_dev;
 constexpr double kInfD = __builtin_huge_val();
 constexpr int kDsirpThreads = 128;
 constexpr int kDsirpIntUnits = 4;  // 128-scenario blocks per CTA (exact-integer kernel)
+constexpr int kDsirpFastMaxUnits = 32;  // 128-scenario blocks per CTA (fast form), upper bound
 
 struct CustDev {
   int32_t U, I0, H, R;
@@ -38,6 +39,7 @@ struct DsirpArgs {
   uint32_t nc;
   int32_t H;
   int32_t all_std_hold;  // every customer uses the standard holding model
+  int32_t units;         // fast form: 128-scenario blocks per CTA
   uint64_t rows;         // nc * H
   uint64_t m_wave, w_base;
   // outputs are addressed by w = w_base + wl (the host passes them at the
@@ -539,10 +541,11 @@ dsirp_fast_kernel(DsirpArgs a) {
   // aggregates: INT sums the scaled integer totals per thread (one exact
   // add per CTA and warp at the end); fp64 keeps a per-warp register
   // accumulator.  Units run by dsirp_unit_fp64 go through agg_warp_add.
-  uint32_t isum = 0u, icnt = 0u;  // < 4 units x 2^22 per thread
+  uint32_t isum = 0u, icnt = 0u;  // < 32 units x 2^22 per thread
   unsigned long long wacc = 0ull;
-  for (int rep = 0; rep < kDsirpIntUnits; ++rep) {
-    const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(kDsirpIntUnits) + rep) * kDsirpThreads +
+  const int units = a.units;
+  for (int rep = 0; rep < units; ++rep) {
+    const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(units) + rep) * kDsirpThreads +
                         threadIdx.x;
     const bool active = wl < a.m_wave;
     const uint64_t w = a.w_base + wl;
@@ -671,7 +674,7 @@ dsirp_fast_kernel(DsirpArgs a) {
     }
   }
   if constexpr (INT) {
-    const uint32_t S = __reduce_add_sync(0xffffffffu, isum);  // < 2^29
+    const uint32_t S = __reduce_add_sync(0xffffffffu, isum);  // < 32 x 32 x 2^22 = 2^32
     const uint32_t n = __reduce_add_sync(0xffffffffu, icnt);
     if ((threadIdx.x & 31) == 0) agg_cta_add_scaled(s_agg, S, cd.shift, n);
   } else {
@@ -705,8 +708,17 @@ void launch_exact(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_pat
 // Fast form for horizons 1..8 (dsirp_fast_a.cu / dsirp_fast_b.cu): INT with
 // or without schedules, fp64 cost-only.  smem = the customer tables.
 template <int H>
-void launch_fast_h(scendp_ctx* ctx, const DsirpArgs& a, size_t smem, bool int_path, bool full) {
-  auto go = [&](auto kernel) { launch_kernel(ctx, kernel, a, smem, kDsirpIntUnits); };
+void launch_fast_h(scendp_ctx* ctx, const DsirpArgs& a_in, size_t smem, bool int_path, bool full) {
+  // blocks per CTA: as many as keep >= 2.5 waves of CTAs (the customer
+  // table load and the aggregate flush are per CTA; measured C4 2.46 ->
+  // 2.16 ms with 32, C3 best with 8)
+  DsirpArgs a = a_in;
+  const uint64_t slots = static_cast<uint64_t>(ctx->sm_count) * (int_path ? 12 : 10);
+  int units = kDsirpFastMaxUnits;
+  while (units > 1 && 2 * a.nc * ((a.m_wave + 128ull * units - 1) / (128ull * units)) < 5 * slots)
+    units /= 2;
+  a.units = units;
+  auto go = [&](auto kernel) { launch_kernel(ctx, kernel, a, smem, units); };
   if (int_path) {
     if (a.all_std_hold) {
       if (full) go(dsirp_fast_kernel<H, true, true, true, true>);
