@@ -6,10 +6,10 @@
 #   3. one `ncu --set full` capture per hot kernel on the fixed workloads of
 #      profiles/cases.py (-lineinfo builds: the source page maps to csrc/).
 # Run from the repo root under gpurun:
-#   gpurun --timeout 3000 -- 'bash profiles/capture.sh r01'
+#   gpurun --timeout 3000 -- 'bash profiles/capture.sh r02'
 # then, in the container:
-#   python profiles/summarize.py r01 --launches gpurun_out/launches.csv
-#   python profiles/summarize.py r01 gpurun_out/k1_r01.ncu-rep:split_linear_c2 ...
+#   python profiles/summarize.py 2 --launches gpurun_out/launches.csv
+#   python profiles/summarize.py 2 gpurun_out/k1_r02.ncu-rep:split_linear_c2 ...
 set -u
 TAG=${1:-r01}
 OUT=gpurun_out
@@ -32,6 +32,12 @@ cap() {  # cap <name> <kernel regex> <case>
 cap k1 split_linear_kernel c2
 cap k1gen split_linear_kernel c2gen
 cap k1f split_linear_kernel c2float
+cap k1r split_linear_kernel c2rand
+cap k1rf split_linear_kernel c2randf
 cap k2 split_penal_kernel c5
-cap k3 dsirp_int_kernel c3
+cap k3 dsirp_fast_kernel c3
+cap k3f dsirp_fast_kernel c3float
+cap k3c4 dsirp_fast_kernel c4
 cap k5 minplus_stage_kernel k5
+python profiles/footprint.py > "$OUT/footprint.txt" 2>&1
+echo "footprint rc=$?"
