@@ -16,18 +16,29 @@ OUT=gpurun_out
 mkdir -p "$OUT"
 NCU="ncu --clock-control none --import-source on"
 
-python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
-echo "bench rc=$?"
-
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file "$OUT/launches.csv" \
-    python bench.py --steps 2 --warmup 1 > "$OUT/bench_ncu.log" 2>&1
-echo "launch list rc=$?"
+# SKIP_BENCH=1: captures only; CASES=k1,k2: only the named captures
+if [ -z "${SKIP_BENCH:-}" ]; then
+  python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+  echo "bench rc=$?"
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file "$OUT/launches.csv" \
+      python bench.py --steps 2 --warmup 1 > "$OUT/bench_ncu.log" 2>&1
+  echo "launch list rc=$?"
+fi
 
 cap() {  # cap <name> <kernel regex> <case>
+  [ -z "${CASES:-}" ] || [[ ",$CASES," == *",$1,"* ]] || return 0
   timeout 900 $NCU --set full -k "regex:$2" -s 1 -c 1 -f -o "$OUT/$1_$TAG" \
       python profiles/cases.py "$3" > "$OUT/$1.log" 2>&1
   echo "$1 rc=$?"
+  # the reports exceed gpurun's copy-back limit together: export the raw and
+  # source pages (text) and keep the report itself outside gpurun_out/
+  if [ -f "$OUT/$1_$TAG.ncu-rep" ]; then
+    ncu -i "$OUT/$1_$TAG.ncu-rep" --page raw --csv > "$OUT/$1_$TAG.raw.csv" 2>/dev/null
+    ncu -i "$OUT/$1_$TAG.ncu-rep" --page source --csv --print-source sass \
+        > "$OUT/$1_$TAG.sass.csv" 2>/dev/null
+    mkdir -p /tmp/ncu_reps && mv "$OUT/$1_$TAG.ncu-rep" /tmp/ncu_reps/
+  fi
 }
 cap k1 split_linear_kernel c2
 cap k1gen split_linear_kernel c2gen
@@ -39,5 +50,7 @@ cap k3 dsirp_fast_kernel c3
 cap k3f dsirp_fast_kernel c3float
 cap k3c4 dsirp_fast_kernel c4
 cap k5 minplus_stage_kernel k5
-python profiles/footprint.py > "$OUT/footprint.txt" 2>&1
-echo "footprint rc=$?"
+if [ -z "${SKIP_BENCH:-}" ]; then
+  python profiles/footprint.py > "$OUT/footprint.txt" 2>&1
+  echo "footprint rc=$?"
+fi

@@ -43,8 +43,12 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    # a .csv is the raw page exported on the GPU box (capture.sh), else ncu -i
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -114,7 +118,7 @@ def main():
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
     for a in args:
         rep, _, name = a.partition(":")
-        name = name or os.path.splitext(os.path.basename(rep))[0]
+        name = name or os.path.basename(rep).split(".")[0]
         traffic[name] = summarize(rep, name, rnd)
     with open(tj, "w") as f:
         json.dump(traffic, f, indent=1)
