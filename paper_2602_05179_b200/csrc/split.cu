@@ -740,7 +740,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     const size_t vt = intv ? 4 : 8;
     // column table (non-identity tours), position tables, per-thread rings
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + (intv ? 2 : 4) * vt) +
-                        static_cast<size_t>(kRing) * T * (vt + 4 + (FULL ? 8 : 0));
+                        static_cast<size_t>(k1_ring(a.ident)) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {
       set_smem(kernel, smem);

@@ -31,20 +31,84 @@ constexpr int32_t kIntInf = 1 << 30;      // value of an emptied window
 constexpr int32_t kIntFinite = 1 << 29;   // v < kIntFinite  <=>  finite
 constexpr int kK1Threads = 128;           // CTA size (ring stride)
 constexpr int kK1Prefetch = 2;            // demand chunks in flight ahead
-constexpr int kRingSpan = kRing * kK1Threads;  // ring elements per array
-constexpr int kStep = kK1Threads * 4;           // counters: byte offsets of 4-byte slots
-constexpr int kMask = kRing * kStep - 1;
+constexpr int kStep = kK1Threads * 4;     // bytes between a thread's consecutive ring slots
+// Deque slots per thread (sentinel included; any count -- the ring is not
+// circular).  Identity tours: 12.  At C2 the deque holds <= 6 entries at a
+// chunk start (simulated over 2000 scenarios), so 12 slots keep the 4-push
+// path and let 16 instead of 12 CTAs share an SM (latency of the demand
+// loads: 0.238 -> 0.227 ms; 11 slots: same, 10: hand-offs).  Column-table
+// (random) tours keep longer deques: 16 (12 hands off at C2).
+__host__ __device__ constexpr int k1_ring(bool ident) { return ident ? 12 : 16; }
+template <int RING>
+constexpr int kPlaneOf = RING * kStep;   // bytes per ring plane (all threads)
 
-// Ring slot at counter c (bytes for 4-byte elements, scaled for wider ones).
-template <typename E>
-__device__ __forceinline__ E& ring_at(E* base, int c) {
-  return *reinterpret_cast<E*>(reinterpret_cast<char*>(base) + (sizeof(E) / 4) * (c & kMask));
+// The deque ring.  Every field is a plane of 4-byte slots, thread-minor
+// ([slot][thread], bank-conflict-free): f (int32, or the low word of the
+// fp64 value), f's high word (fp64 only), load, and for full solutions the
+// predecessor index and route count.  The deque's ends are 32-bit shared-
+// memory addresses of f-plane slots of this thread, so an access is one
+// LDS/STS with an immediate plane offset -- no wrap mask, no base add, and
+// one register per end (generic pointers would take two).  The ring is not
+// circular: when a chunk's pushes would run past the last slot, the few live
+// entries move back to the bottom (k1_room); the front end advances only by
+// evictions, so that is rare.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+template <int OFF>
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0+%1], %2;" ::"r"(a), "n"(OFF), "r"(v));
+}
+
+template <typename VT, int RING>
+struct K1Ring {
+  static constexpr int kPlane = kPlaneOf<RING>;
+  static constexpr bool kInt = std::is_same<VT, int32_t>::value;
+  static constexpr int kHi = 1;            // fp64 high word
+  static constexpr int kL = kInt ? 1 : 2;  // load
+  static constexpr int kI = kL + 1, kR = kL + 2;  // FULL
+  static __device__ __forceinline__ VT f(uint32_t p) {
+    if constexpr (kInt) return static_cast<int32_t>(lds32<0>(p));
+    else return __hiloint2double(lds32<kHi * kPlane>(p), lds32<0>(p));
+  }
+  static __device__ __forceinline__ void set_f(uint32_t p, VT v) {
+    if constexpr (kInt) {
+      sts32<0>(p, static_cast<uint32_t>(v));
+    } else {
+      sts32<0>(p, static_cast<uint32_t>(__double2loint(v)));
+      sts32<kHi * kPlane>(p, static_cast<uint32_t>(__double2hiint(v)));
+    }
+  }
+  static __device__ __forceinline__ uint32_t l(uint32_t p) { return lds32<kL * kPlane>(p); }
+  static __device__ __forceinline__ void set_l(uint32_t p, uint32_t v) { sts32<kL * kPlane>(p, v); }
+  static __device__ __forceinline__ int32_t idx(uint32_t p) { return static_cast<int32_t>(lds32<kI * kPlane>(p)); }
+  static __device__ __forceinline__ void set_idx(uint32_t p, int32_t v) { sts32<kI * kPlane>(p, static_cast<uint32_t>(v)); }
+  static __device__ __forceinline__ int32_t rc(uint32_t p) { return static_cast<int32_t>(lds32<kR * kPlane>(p)); }
+  static __device__ __forceinline__ void set_rc(uint32_t p, int32_t v) { sts32<kR * kPlane>(p, static_cast<uint32_t>(v)); }
+  // copy every plane of slot src to slot dst
+  template <bool FULL>
+  static __device__ __forceinline__ void move(uint32_t dst, uint32_t src) {
+    sts32<0>(dst, lds32<0>(src));
+    if constexpr (!kInt) sts32<kHi * kPlane>(dst, lds32<kHi * kPlane>(src));
+    set_l(dst, l(src));
+    if constexpr (FULL) {
+      set_idx(dst, idx(src));
+      set_rc(dst, rc(src));
+    }
+  }
+};
 
 template <typename VT>
 struct K1State {
   uint32_t load;
-  int head, tail;  // slot * kStep (byte offsets), unbounded, masked on access
+  uint32_t head;  // f-plane slot of the deque front (the slot below holds -inf)
+  uint32_t tail;  // first free slot
   VT front_f, back_f, v;
   uint32_t front_l;
   int32_t front_i, front_rc, rc;
@@ -75,8 +139,27 @@ __device__ __forceinline__ VT k1_neg_inf() {
   else return -kInfD;
 }
 
-// One DP position.  PUSH = (i < n).  Ring slot s of this thread lives at
-// ring_at(rf, s) (rf/rl/ri/rr are per-thread base pointers).
+// Make room for `pushes` more entries below the ring's end: when the tail
+// would run past slot RING-1, move the sentinel and the live entries down
+// to slots 0..len (rare: the head advances only by evictions).  Returns
+// false when even the compacted deque has no room (the scenario then takes
+// the generic path).
+template <typename VT, bool FULL, int RING>
+__device__ __forceinline__ bool k1_room(K1State<VT>& s, uint32_t base, int pushes) {
+  if (s.tail + pushes * kStep <= base + kPlaneOf<RING>) return true;
+  using R = K1Ring<VT, RING>;
+  const int len = static_cast<int>(s.tail - s.head) / kStep;
+  if (len + 1 + pushes > RING) return false;
+  uint32_t dst = base + kStep;
+  for (uint32_t src = s.head; src < s.tail; src += kStep, dst += kStep)
+    R::template move<FULL>(dst, src);
+  R::set_f(base, k1_neg_inf<VT>());
+  s.head = base + kStep;
+  s.tail = dst;
+  return true;
+}
+
+// One DP position.  PUSH = (i < n).
 //
 // SAFE = false is the fast form for a position with d_i <= Q (checked per
 // chunk): entry i-1, at the back, then survives the eviction, so the window
@@ -86,11 +169,11 @@ __device__ __forceinline__ VT k1_neg_inf() {
 // SAFE = true handles any d_i (window emptied when d_i > Q).
 // NOEVICT (with SAFE = false): the caller proved no eviction can happen at
 // this position (see the chunk loop), so the window test is skipped.
-template <typename VT, bool FULL, bool PUSH, bool SAFE = true, bool NOEVICT = false>
+// The caller guarantees a free slot at the tail (k1_room).
+template <typename VT, bool FULL, bool PUSH, bool SAFE, bool NOEVICT, int RING>
 __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
-                                        VT t1, VT t2, VT t3, VT* __restrict__ rf,
-                                        uint32_t* __restrict__ rl, int32_t* __restrict__ ri,
-                                        int32_t* __restrict__ rr, double* Vout, int32_t* Cout) {
+                                        VT t1, VT t2, VT t3, double* Vout, int32_t* Cout) {
+  using R = K1Ring<VT, RING>;
   s.load += d;
   // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96); the
   // evicted slot becomes the -inf sentinel below the new head
@@ -100,7 +183,7 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
       // d itself -- the u32 difference load - front_l wraps once d_i >=
       // 2^32 - Q (loads are int64 in the reference, split.cpp:93); with
       // d_i <= Q every window difference is < 2Q < 2^32 and exact mod 2^32
-      ring_at(rf, s.tail - kStep) = k1_neg_inf<VT>();
+      R::set_f(s.tail - kStep, k1_neg_inf<VT>());
       s.head = s.tail;
       s.back_f = k1_neg_inf<VT>();
       s.front_f = k1_inf<VT>();
@@ -111,7 +194,7 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
       }
     }
     while (s.load - s.front_l > Qc) {
-      ring_at(rf, s.head) = k1_neg_inf<VT>();
+      R::set_f(s.head, k1_neg_inf<VT>());
       s.head += kStep;
       if (s.head == s.tail) {
         // only when d_i > Q: every route into i overflows, V(i) = +inf.  The
@@ -126,26 +209,24 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
         }
         break;
       }
-      const int hs = s.head;
-      s.front_f = ring_at(rf, hs);
-      s.front_l = ring_at(rl, hs);
+      s.front_f = R::f(s.head);
+      s.front_l = R::l(s.head);
       if (FULL) {
-        s.front_i = ring_at(ri, hs);
-        s.front_rc = ring_at(rr, hs);
+        s.front_i = R::idx(s.head);
+        s.front_rc = R::rc(s.head);
       }
     }
   } else if constexpr (!NOEVICT) {
     if (s.load - s.front_l > Qc) {
       do {
-        ring_at(rf, s.head) = k1_neg_inf<VT>();
+        R::set_f(s.head, k1_neg_inf<VT>());
         s.head += kStep;
-        s.front_l = ring_at(rl, s.head);
+        s.front_l = R::l(s.head);
       } while (s.load - s.front_l > Qc);
-      const int hs = s.head;
-      s.front_f = ring_at(rf, hs);
+      s.front_f = R::f(s.head);
       if (FULL) {
-        s.front_i = ring_at(ri, hs);
-        s.front_rc = ring_at(rr, hs);
+        s.front_i = R::idx(s.head);
+        s.front_rc = R::rc(s.head);
       }
     }
   }
@@ -175,24 +256,23 @@ __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint3
     if constexpr (SAFE) {
       while (s.back_f > fi) {
         s.tail -= kStep;
-        s.back_f = ring_at(rf, s.tail - kStep);
+        s.back_f = R::f(s.tail - kStep);
       }
       if (s.tail == s.head) become_front();
     } else {
       if (s.back_f > fi) {
         do {
           s.tail -= kStep;
-          s.back_f = ring_at(rf, s.tail - kStep);
+          s.back_f = R::f(s.tail - kStep);
         } while (s.back_f > fi);
         if (s.tail == s.head) become_front();
       }
     }
-    const int ts = s.tail;
-    ring_at(rf, ts) = fi;
-    ring_at(rl, ts) = s.load;
+    R::set_f(s.tail, fi);
+    R::set_l(s.tail, s.load);
     if (FULL) {
-      ring_at(ri, ts) = i;
-      ring_at(rr, ts) = s.rc;
+      R::set_idx(s.tail, i);
+      R::set_rc(s.tail, s.rc);
     }
     s.tail += kStep;
     s.back_f = fi;
@@ -240,6 +320,7 @@ __global__ void __launch_bounds__(kK1Threads)
 split_linear_kernel(SplitArgs a) {
   using VT = typename std::conditional<INTV, int32_t, double>::type;
   constexpr int T = kK1Threads;
+  constexpr int RING = k1_ring(IDENT);
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned long long s_agg[kAggSlots];
   const uint32_t k = blockIdx.y;
@@ -261,10 +342,8 @@ split_linear_kernel(SplitArgs a) {
     }
   }
   const int tid = threadIdx.x;
-  VT* rf = reinterpret_cast<VT*>(s_tab + ntab * npad) + tid;                 // [kRing][T]
-  uint32_t* rl = reinterpret_cast<uint32_t*>(rf - tid + kRingSpan) + tid;   // [kRing][T]
-  int32_t* ri = reinterpret_cast<int32_t*>(rl - tid + kRingSpan) + tid;     // FULL
-  int32_t* rr = ri + kRingSpan;                                             // FULL
+  // this thread's ring: slot 0 of its f plane (planes follow, see K1Ring)
+  const uint32_t rbase = smem_addr(s_tab + ntab * npad) + 4 * tid;
   agg_cta_init(s_agg);
   __syncthreads();
 
@@ -302,23 +381,23 @@ split_linear_kernel(SplitArgs a) {
     s.v = VT(0);
     s.load = 0u;
     // slot 0: -inf sentinel (always the slot below the head); slot 1: p = 0
-    s.head = kStep;
-    s.tail = 2 * kStep;
-    rf[0] = k1_neg_inf<VT>();
-    ring_at(rf, kStep) = s.front_f;
-    ring_at(rl, kStep) = 0u;
+    using R = K1Ring<VT, RING>;
+    s.head = rbase + kStep;
+    s.tail = rbase + 2 * kStep;
+    R::set_f(rbase, k1_neg_inf<VT>());
+    R::set_f(s.head, s.front_f);
+    R::set_l(s.head, 0u);
     if (FULL) {
-      ring_at(ri, kStep) = 0;
-      ring_at(rr, kStep) = 0;
+      R::set_idx(s.head, 0);
+      R::set_rc(s.head, 0);
     }
 
     // positions 1..n-1 push; full chunks of 4 first, demands one chunk ahead
     const int npush = n - 1;
     const int nfull = npush >> 2;
-    // the ring holds the sentinel + at most kRing-1 entries, so a push needs
-    // <= kRing-2 live entries; a chunk pushes 4, hence <= kRing-5 at its start
-    // -- otherwise the scenario takes the generic path
-    constexpr int kChunkRoom = (kRing - 5) * kStep;
+    // a chunk pushes 4: room for them below the ring's end (compacting the
+    // deque when needed), else the scenario takes the generic path
+    auto room4 = [&] { return k1_room<VT, FULL, RING>(s, rbase, 4); };
     auto chunk = [&](int s0, uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {
       // position constants for the chunk, loaded up front (latency hidden
       // behind the first steps): int32 A/B as two 128-bit loads, fp64
@@ -347,11 +426,11 @@ split_linear_kernel(SplitArgs a) {
         if constexpr (!INTV && !IDENT) {
           const double2 p = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j));
           const double2 q = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j) + 2);
-          k1_step<VT, FULL, true, kSafe, kNoEvict>(s, s0 + j + 1, d, Qc, p.x, p.y, q.x, q.y, rf, rl,
-                                                   ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, kSafe, kNoEvict, RING>(s, s0 + j + 1, d, Qc, p.x, p.y, q.x, q.y, Vout,
+                                                   Cout);
         } else {
-          k1_step<VT, FULL, true, kSafe, kNoEvict>(s, s0 + j + 1, d, Qc, t0[j], t1[j], t2[j],
-                                                   t3[j], rf, rl, ri, rr, Vout, Cout);
+          k1_step<VT, FULL, true, kSafe, kNoEvict, RING>(s, s0 + j + 1, d, Qc, t0[j], t1[j], t2[j],
+                                                   t3[j], Vout, Cout);
         }
       };
       using T_ = std::true_type;
@@ -390,6 +469,8 @@ split_linear_kernel(SplitArgs a) {
     // PF = 2: a register ring indexed at compile time (the loop body is
     // unrolled over the ring) -- more loads in flight per warp for the
     // latency of out-of-order row gathers (random giant tours) and fp64.
+    // (identity int32 with two chunks in flight measured slower: 0.264 vs
+    // 0.238 ms with the 16-slot ring)
     constexpr int PF = (SRC != kSrcTiled || (IDENT && INTV)) ? 1 : kK1Prefetch;
     if constexpr (PF == 1) {
       uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
@@ -397,13 +478,13 @@ split_linear_kernel(SplitArgs a) {
       int cidx = 0;
       for (; cidx + 1 < nfull; cidx += 2) {
         const int s0 = cidx * 4;
-        if (s.tail - s.head > kChunkRoom) {
+        if (!room4()) {
           ok = false;
           break;
         }
         k1_demand4<SRC, IDENT>(a, stream, tile_base, s_col, s0 + 4, b0, b1, b2, b3);
         chunk(s0, a0, a1, a2, a3);
-        if (s.tail - s.head > kChunkRoom) {
+        if (!room4()) {
           ok = false;
           break;
         }
@@ -412,7 +493,7 @@ split_linear_kernel(SplitArgs a) {
         chunk(s0 + 4, b0, b1, b2, b3);
       }
       if (ok && cidx < nfull) {
-        if (s.tail - s.head > kChunkRoom) ok = false;
+        if (!room4()) ok = false;
         else chunk(cidx * 4, a0, a1, a2, a3);
       }
     } else {
@@ -429,7 +510,7 @@ split_linear_kernel(SplitArgs a) {
         for (int u = 0; u <= PF; ++u) {
           const int cc = cidx + u;
           if (cc >= nfull) break;
-          if (s.tail - s.head > kChunkRoom) {
+          if (!room4()) {
             ok = false;
             break;
           }
@@ -443,7 +524,7 @@ split_linear_kernel(SplitArgs a) {
     }
     // remaining pushing positions (< 4), then position n (no push)
     for (int i = nfull * 4 + 1; ok && i <= n; ++i) {
-      if (s.tail - s.head > (kRing - 2) * kStep) {
+      if (!k1_room<VT, FULL, RING>(s, rbase, 1)) {
         ok = false;
         break;
       }
@@ -459,8 +540,8 @@ split_linear_kernel(SplitArgs a) {
         x2 = s_tab[4 * sl + 2];
         x3 = s_tab[4 * sl + 3];
       }
-      if (i < n) k1_step<VT, FULL, true>(s, i, d, Qc, x0, x1, x2, x3, rf, rl, ri, rr, Vout, Cout);
-      else k1_step<VT, FULL, false>(s, i, d, Qc, x0, x1, x2, x3, rf, rl, ri, rr, Vout, Cout);
+      if (i < n) k1_step<VT, FULL, true, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
+      else k1_step<VT, FULL, false, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
     }
     if (!ok) {
       push_overflow(a, k, wl);

@@ -21,6 +21,7 @@ e.g. `ncu --set full -k regex:split_linear -s 1 -c 1 python profiles/cases.py c2
 import argparse
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -117,13 +118,15 @@ def main():
         fn()
         ctx.sync()
         ctx.kernel_stats(reset=True)
+        t0 = time.perf_counter()
         for _ in range(args.reps):
             fn()
         ctx.sync()
+        wall_ms = (time.perf_counter() - t0) * 1e3 / args.reps
         st = ctx.kernel_stats(reset=True)
         k_ms = st["dp_ms"] / max(1, st["dp_launches"])
         frac = f" frac={nbytes / (k_ms / 1e3) / 1e9 / HBM:.3f}" if nbytes else ""
-        print(f"{c}: kernel_ms={k_ms:.4f}{frac} {st}", flush=True)
+        print(f"{c}: kernel_ms={k_ms:.4f}{frac} call_ms={wall_ms:.4f} {st}", flush=True)
     ctx.close()
 
 

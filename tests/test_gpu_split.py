@@ -390,3 +390,37 @@ def test_hard_demands_near_u32_max(ctx, oracle, reference, Q, costs):
         co = ctx.split_eval(inst, tour, dem)
         np.testing.assert_array_equal(co["totals"][0], tot)
         assert co["agg"][0]["finite_count"] == fc and co["agg"][0]["infeasible_count"] == ic
+
+
+@pytest.mark.parametrize("costs", ["int", "float"])
+def test_hard_deque_compaction(ctx, oracle, reference, costs):
+    """K1's deque ring is not circular: the front advances by evictions and
+    the live entries move back to the ring's bottom when a chunk's pushes
+    would run past its end.  A line metric (f increasing along the tour:
+    nothing pops) with a window of ~3 positions (Q = 12, demands 3..5)
+    evicts at almost every position, so the entries are compacted every few
+    chunks; cost-only and full solutions, identity (12-slot ring) and random
+    (16-slot ring) tours."""
+    n, m, Q = 203, 4133, 12
+    idx = np.arange(n + 2, dtype=np.float64)
+    c = np.abs(idx[:, None] - idx[None, :])
+    if costs == "float":
+        c = c * 1.37 + np.triu(np.random.default_rng(4).random((n + 2, n + 2)), 1) * 0.01
+        c = np.triu(c, 1)
+        c = c + c.T
+    inst = RoutingInstance(n, Q, True, 0.0, c)
+    dem = oracle.generate(UNIFORM, 3, 5, 77, n, m)
+    for tour in (np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 8)):
+        got = ctx.split_eval(inst, tour, dem)
+        ref_tot, (ref_mean, fc, ic) = reference.split_costs(n, Q, 1, 0.0, c, tour, dem, 16)
+        np.testing.assert_array_equal(got["totals"][0], ref_tot)
+        a = got["agg"][0]
+        assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
+        check_mean(a, ref_mean)
+        sub = dem[:512]
+        full = ctx.split_eval(inst, tour, sub, full=True)
+        tot, V, cuts, rc, feas, _ = reference.expected_split(n, Q, 1, 0.0, c, tour, sub)
+        np.testing.assert_array_equal(full["totals"][0], tot)
+        np.testing.assert_array_equal(full["V"], V)
+        np.testing.assert_array_equal(full["cuts"], cuts)
+        np.testing.assert_array_equal(full["route_count"], rc)
