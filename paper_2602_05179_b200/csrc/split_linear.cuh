@@ -315,6 +315,10 @@ __device__ __forceinline__ void k1_demand4(const SplitArgs& a, uint64_t stream,
   }
 }
 
+template <typename P>
+__device__ __forceinline__ double2 ldtab2(const P* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
 template <bool FULL, int SRC, bool INTV, bool IDENT>
 __global__ void __launch_bounds__(kK1Threads)
 split_linear_kernel(SplitArgs a) {
@@ -330,6 +334,9 @@ split_linear_kernel(SplitArgs a) {
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem);
   VT* s_tab = reinterpret_cast<VT*>(s_col + (IDENT ? 0 : npad));  // IDENT: no column table
   constexpr int ntab = INTV ? 2 : 4;
+  // (fp64 tables read through L1 instead of shared memory, for more CTAs:
+  // measured slower, C2 float 0.327 -> 0.405 ms)
+  const VT* tab = s_tab;
   {
     const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
     if (!IDENT) for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
@@ -399,9 +406,9 @@ split_linear_kernel(SplitArgs a) {
     // deque when needed), else the scenario takes the generic path
     auto room4 = [&] { return k1_room<VT, FULL, RING>(s, rbase, 4); };
     auto chunk = [&](int s0, uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {
-      // position constants for the chunk, loaded up front (latency hidden
-      // behind the first steps): int32 A/B as two 128-bit loads, fp64
-      // (dist, ret, c0, dist_next) interleaved per position, eight loads
+      // position constants: int32 A/B for the chunk as two 128-bit loads up
+      // front (latency hidden behind the first steps); fp64 (dist, ret, c0,
+      // dist_next, interleaved) per position just before its step
       VT t0[4], t1[4], t2[4], t3[4];
       if constexpr (INTV) {
         const int4 x0 = *reinterpret_cast<const int4*>(s_tab + s0);
@@ -410,22 +417,14 @@ split_linear_kernel(SplitArgs a) {
         t1[0] = x1.x; t1[1] = x1.y; t1[2] = x1.z; t1[3] = x1.w;
 #pragma unroll
         for (int j = 0; j < 4; ++j) t2[j] = t3[j] = VT(0);
-      } else if constexpr (IDENT) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double2 p = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j));
-          const double2 q = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j) + 2);
-          t0[j] = p.x; t1[j] = p.y; t2[j] = q.x; t3[j] = q.y;
-        }
       }
-      // (fp64 with a column table and two chunks of demands in flight: each
-      // position's doubles are loaded just before its step -- 64 -> 54
-      // registers, measured 0.45 -> 0.37 ms at C2 with a random tour)
+      // (fp64 per position: 64 -> 48 registers; measured 0.45 -> 0.37 ms at
+      // C2 with a random tour, 0.351 -> 0.328 ms with the identity tour)
       auto step = [&](auto safe, auto noevict, int j, uint32_t d) {
         constexpr bool kSafe = decltype(safe)::value, kNoEvict = decltype(noevict)::value;
-        if constexpr (!INTV && !IDENT) {
-          const double2 p = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j));
-          const double2 q = *reinterpret_cast<const double2*>(s_tab + 4 * (s0 + j) + 2);
+        if constexpr (!INTV) {
+          const double2 p = ldtab2(tab + 4 * (s0 + j));
+          const double2 q = ldtab2(tab + 4 * (s0 + j) + 2);
           k1_step<VT, FULL, true, kSafe, kNoEvict, RING>(s, s0 + j + 1, d, Qc, p.x, p.y, q.x, q.y, Vout,
                                                    Cout);
         } else {
@@ -478,6 +477,17 @@ split_linear_kernel(SplitArgs a) {
       int cidx = 0;
       for (; cidx + 1 < nfull; cidx += 2) {
         const int s0 = cidx * 4;
+        if constexpr (FULL && IDENT && SRC == kSrcTiled) {
+          // rows s0+16 .. s0+23 of this warp's tile into L2 (one bulk
+          // prefetch per warp per 8 positions, no registers held).  Full
+          // solutions only: C2 full 0.564 -> 0.549 ms; the cost-only form
+          // measured slower with it (0.228 -> 0.239 ms)
+          if ((tid & 31) == 0 && s0 + 24 <= n)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             tile_base + static_cast<uint64_t>(s0 + 16) * kTile),
+                         "r"(8 * kTile * 4)
+                         : "memory");
+        }
         if (!room4()) {
           ok = false;
           break;
@@ -535,10 +545,10 @@ split_linear_kernel(SplitArgs a) {
         x0 = s_tab[sl];
         x1 = s_tab[npad + sl];
       } else {
-        x0 = s_tab[4 * sl];
-        x1 = s_tab[4 * sl + 1];
-        x2 = s_tab[4 * sl + 2];
-        x3 = s_tab[4 * sl + 3];
+        x0 = tab[4 * sl];
+        x1 = tab[4 * sl + 1];
+        x2 = tab[4 * sl + 2];
+        x3 = tab[4 * sl + 3];
       }
       if (i < n) k1_step<VT, FULL, true, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
       else k1_step<VT, FULL, false, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);

@@ -174,7 +174,7 @@ split_penal_kernel(SplitArgs a) {
         }
         // deque entries before lo leave from the front (entry i-1 stays);
         // the vacated slot becomes the -inf sentinel below the head
-        const int lo = lo_c / kH;
+        const int lo = static_cast<int>(static_cast<unsigned>(lo_c) / kH);
         if (front_p < lo) {
           do {
             at32(dq_f, head, kDqMaskH) = INT32_MIN;
