@@ -306,25 +306,39 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
       Vout[0] = 0.0;
       Cout[0] = 0;
     }
-    ld[0] = 0;
-    for (int i = 1; i <= n; ++i)
-      ld[i] = ld[i - 1] + static_cast<int64_t>(demand_at(a, SRC, stream, tile_base, col[i]));
-    f[0] = __dsub_rn(__dadd_rn(0.0, c0[0]), dist[1]);
-    rcs[0] = 0;
+    const double f0 = __dsub_rn(__dadd_rn(0.0, c0[0]), dist[1]);
     if (a.linear) {
-      int head = 0, tail = 0;
-      dq[tail++] = 0;
-      for (int i = 1; i <= n; ++i) {
-        while (head < tail && ld[i] - ld[dq[head]] > a.Q) ++head;
+      // the reference's deque (split.cpp:77-118) with its entries' f, load,
+      // index and route count stored in the deque slots (scratch planes
+      // reused: f | ld | dq | rcs) and both ends cached in registers, so a
+      // position touches global scratch only when an end moves -- not
+      // through dependent dq -> f / ld lookups (5x fewer round trips)
+      int head = 0, tail = 1;
+      f[0] = f0;
+      ld[0] = 0;
+      dq[0] = 0;
+      rcs[0] = 0;
+      double front_f = f0, back_f = f0;
+      int64_t front_l = 0, load = 0;
+      int32_t front_i = 0, front_rc = 0, rc = 0;
+      auto step = [&](int i, uint32_t d) {
+        load += static_cast<int64_t>(d);
+        while (head < tail && load - front_l > a.Q) {
+          if (++head < tail) {
+            front_f = f[head];
+            front_l = ld[head];
+            front_i = dq[head];
+            front_rc = rcs[head];
+          }
+        }
         int32_t cut = -1;
         if (head >= tail) {
           v = kInfD;
-          rcs[i] = 0;
+          rc = 0;
         } else {
-          const int p = dq[head];
-          v = __dadd_rn(__dadd_rn(f[p], dist[i]), ret[i]);
-          cut = v < kInfD ? p : -1;
-          rcs[i] = v < kInfD ? rcs[p] + 1 : 0;
+          v = __dadd_rn(__dadd_rn(front_f, dist[i]), ret[i]);
+          cut = v < kInfD ? front_i : -1;
+          rc = v < kInfD ? front_rc + 1 : 0;
         }
         if (FULL) {
           Vout[static_cast<uint64_t>(i) * kTile] = v;
@@ -332,12 +346,55 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
         }
         if (i < n) {
           const double fi = __dsub_rn(__dadd_rn(v, c0[i]), dist[i + 1]);
-          while (tail > head && f[dq[tail - 1]] > fi) --tail;
-          dq[tail++] = i;
-          f[i] = fi;
+          while (tail > head && back_f > fi) {
+            --tail;
+            back_f = tail > head ? f[tail - 1] : -kInfD;
+          }
+          f[tail] = fi;
+          ld[tail] = load;
+          dq[tail] = i;
+          rcs[tail] = rc;
+          if (tail == head) {
+            front_f = fi;
+            front_l = load;
+            front_i = i;
+            front_rc = rc;
+          }
+          ++tail;
+          back_f = fi;
         }
+      };
+      // demands are loaded one chunk of 4 positions ahead of their use
+      auto dem4 = [&](int i0, uint32_t (&dd)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dd[j] = i0 + j <= n ? demand_at(a, SRC, stream, tile_base, col[i0 + j]) : 0u;
+      };
+      uint32_t dc[4], dn[4];
+      dem4(1, dc);
+      for (int i0 = 1; i0 <= n; i0 += 4) {
+        dem4(i0 + 4, dn);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (i0 + j <= n) step(i0 + j, dc[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dc[j] = dn[j];
       }
-    } else if (!a.hard && a.pen_lmax > 0 && ld[n] <= static_cast<int64_t>(a.pen_lmax)) {
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = v;
+      if (FULL) {
+        const bool fin = v < kInfD;
+        a.route_count[w] = fin ? rc : 0;
+        a.feasible[w] = fin ? 1 : 0;
+      }
+      agg_item_global(a.agg + static_cast<uint64_t>(k) * kAggWords, v, true);
+      return;
+    }
+    ld[0] = 0;
+    for (int i = 1; i <= n; ++i)
+      ld[i] = ld[i - 1] + static_cast<int64_t>(demand_at(a, SRC, stream, tile_base, col[i]));
+    f[0] = f0;
+    rcs[0] = 0;
+    if (!a.hard && a.pen_lmax > 0 && ld[n] <= static_cast<int64_t>(a.pen_lmax)) {
       // penalized, exact integral data: the O(n) decomposition of
       // split_penal.cuh without its ring limits -- window A = {L_i - L_p
       // <= Q} (deque of f, earliest minimum) and prefix B before it (running
@@ -425,16 +482,20 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
   }
   if (cnt > a.ovf_cap) {
     // the list was full: the remaining items are flagged in the bitmap
-    // (bit = k * m_wave + wl); each word is cleared once processed, so the
-    // bitmap is all-zero again for the next wave / call
+    // (bit = k * m_wave + wl).  Lane j of a warp takes bit j of a word (an
+    // item per thread -- not a word per thread, which ran 32 items in
+    // sequence), and lane 0 clears the word once the warp has read it, so
+    // the bitmap is all-zero again for the next wave / call
     const uint64_t words = (static_cast<uint64_t>(a.k) * a.m_wave + 31) / 32;
-    for (uint64_t wd = gtid; wd < words; wd += nthreads) {
-      uint32_t bits = a.ovf_bits[wd];
+    const uint64_t gwarp = gtid >> 5, nwarps = nthreads >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t wd = gwarp; wd < words; wd += nwarps) {
+      const uint32_t bits = a.ovf_bits[wd];
+      __syncwarp();
       if (!bits) continue;
-      a.ovf_bits[wd] = 0u;
-      while (bits) {
-        const uint64_t item = wd * 32 + (__ffs(bits) - 1);
-        bits &= bits - 1;
+      if (lane == 0) a.ovf_bits[wd] = 0u;
+      if ((bits >> lane) & 1u) {
+        const uint64_t item = wd * 32 + lane;
         run_item(static_cast<uint32_t>(item / a.m_wave), item % a.m_wave);
       }
     }
@@ -770,7 +831,10 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
 }
 
 // Generic (hand-off) kernel scratch: latency-bound (dependent global-scratch
-// accesses), so as many threads as ~64 MB of scratch allows, 2..8 CTAs/SM.
+// accesses), so as many threads as ~512 MB of scratch allows (an eighth of
+// scratch_limit when one is set), 2..16 CTAs/SM.  (64 MB until round 2:
+// 2 CTAs/SM at n = 200 -- a zero-heavy demand set that sends most scenarios
+// to this pass ran 5-8x slower.)
 struct GenericLayout {
   uint64_t stride;
   int blocks;
@@ -782,8 +846,10 @@ GenericLayout generic_layout(const scendp_ctx* ctx, int n) {
   GenericLayout g;
   g.stride = ((n1 * (8 + 8 + 4 + 4)) + 127) & ~uint64_t{127};
   const uint64_t per_sm = static_cast<uint64_t>(ctx->sm_count) * kGenericThreads * g.stride;
+  uint64_t cap = uint64_t{512} << 20;
+  if (ctx->opts.scratch_limit) cap = std::min(cap, ctx->opts.scratch_limit / 8);
   g.blocks = ctx->sm_count *
-             static_cast<int>(std::clamp<uint64_t>((64ull << 20) / per_sm, kGenericBlocksPerSm, 8));
+             static_cast<int>(std::clamp<uint64_t>(cap / per_sm, kGenericBlocksPerSm, 16));
   return g;
 }
 

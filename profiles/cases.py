@@ -9,6 +9,10 @@ Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
   c2gen     C2 with in-kernel generation (the e2e call, batched_split_costs_generated)
   c2rand    C2 with a random giant tour (the SAA case), integer costs
   c2randf   the same with non-integral costs (K1 fp64, column gather)
+  c2zero    adversarial: line metric (f increasing along the identity tour:
+            nothing pops), zero-heavy demands uniform:0:2, 10^5 scenarios --
+            windows of ~100 positions, every deque outgrows the ring and
+            takes the hand-off (generic) pass
   c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
   c3float   the non-dyadic C3 twin (K3 fp64 path)
   c4        DSIRP 200 customers x 10^6 scenarios (one GPU)
@@ -36,6 +40,15 @@ def build(ctx, c):
     from paper_2602_05179_b200 import (Customer, Distribution, RoutingInstance,
                                        derive_stream, make_random_instance, pinned_empty)
     from paper_2602_05179_b200 import _capi as A
+    if c == "c2zero":
+        n, m = 200, 100_000
+        tour = np.arange(1, n + 1, dtype=np.int32)
+        idx = np.arange(n + 2, dtype=np.float64)
+        inst = RoutingInstance(n, 100, True, 0.0, np.abs(idx[:, None] - idx[None, :]))
+        dist = Distribution("uniform", 0, 2, seed=derive_stream(1, 0x5343454E, 0))
+        sc = ctx.gen_scenarios(dist, n, m)
+        fn = lambda: ctx.split_eval(inst, tour, (sc, A.MEM_DEVICE_TILED), count=m, totals=False)
+        return fn, None
     if c.startswith("c2"):
         n, m = 200, 1_000_000
         tour = np.arange(1, n + 1, dtype=np.int32)
