@@ -533,6 +533,22 @@ def secondary(ctx, d: Dist, args):
     out["split_c2_penalized"] = {"value": G * mp / (step_ms / 1e3), "unit": UNIT,
                                  "kernel_ms": k_ms, "scenarios_per_gpu": mp, "scaling": "weak",
                                  "dense_candidates_per_s": G * mp * n * (n + 1) / 2 / (step_ms / 1e3)}
+    # adversarial hand-off cliff: a line metric (f increases along the
+    # identity tour, nothing pops) with zero-heavy demands uniform:0:2 keeps
+    # ~100 entries in every deque -- no scenario fits K1's ring, all 10^5
+    # take the hand-off (generic) pass.  Timed per call (K1 + the pass).
+    ma = min(m, 100_000)
+    idx = np.arange(n + 2, dtype=np.float64)
+    ainst = RoutingInstance(n, Q_C2, True, 0.0, np.abs(idx[:, None] - idx[None, :]))
+    scena = ctx.gen_scenarios(Distribution("uniform", 0, 2, seed=91), n, ma, w0=lo)
+    step_ms, k_ms = kernel_rate(ctx.split_eval(
+        ainst, ident, (scena, A.MEM_DEVICE_TILED), count=ma, first_index=lo,
+        out_kind="device_tiled", device_out={"totals": tot}, sync=False, prepare=True), 5, 1)
+    out["split_c2_adversarial_handoff"] = {
+        "value": G * ma / (step_ms / 1e3), "unit": UNIT, "ms_per_call": step_ms,
+        "k1_kernel_ms": k_ms, "scenarios_per_gpu": ma, "scaling": "weak",
+        "config": "n=200 Q=100 line metric, identity tour, uniform:0:2: every scenario handed off"}
+    scena.free()
     scen.free()
     scen2.free()
     tot.free()
@@ -688,6 +704,13 @@ def cpu_reference_secondary():
     out["split_c2_penalized"] = (rate(lambda: R.split_costs(n, Q_C2, 0, 10.0, icost, tour,
                                                              dem[:mp], threads), mp),
                                  f"batched_split_costs penalized beta=10, {mp} scenarios")
+    idx = np.arange(n + 2, dtype=np.float64)
+    lcost = np.abs(idx[:, None] - idx[None, :])
+    dema = R.generate(UNIFORM, 0, 2, 91, n, 1, ms)
+    out["split_c2_adversarial_handoff"] = (rate(lambda: R.split_costs(n, Q_C2, 1, 0.0, lcost, tour,
+                                                                       dema, threads), ms),
+                                           f"batched_split_costs, line metric, uniform:0:2, "
+                                           f"{ms} scenarios")
     # C5: K calls of batched_split_costs (saa.cpp:127-131), timed on 4 tours
     n5, m5, k5 = 50, 100_000, 4
     cost5 = R.make_random_instance(n5, 5)
