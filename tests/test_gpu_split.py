@@ -424,3 +424,29 @@ def test_hard_deque_compaction(ctx, oracle, reference, costs):
         np.testing.assert_array_equal(full["V"], V)
         np.testing.assert_array_equal(full["cuts"], cuts)
         np.testing.assert_array_equal(full["route_count"], rc)
+
+
+@pytest.mark.parametrize("costs", ["int", "float"])
+def test_handoff_full_solutions(ctx, oracle, reference, costs):
+    """Full solutions (V, cuts, route counts) of scenarios that all take the
+    hand-off pass: line metric with zero-heavy demands keeps up to ~60
+    entries in every deque (K1's ring holds 12/16); the generic kernel's
+    deque carries each entry's f, load, index and route count.  Identity and
+    random tours, 70,000 scenarios: beyond the 65,536-entry hand-off list,
+    so the bitmap path (one item per lane) runs too."""
+    n, m, Q = 60, 70_000, 100
+    idx = np.arange(n + 2, dtype=np.float64)
+    c = np.abs(idx[:, None] - idx[None, :])
+    if costs == "float":
+        c = c * 1.37
+    inst = RoutingInstance(n, Q, True, 0.0, c)
+    dem = oracle.generate(UNIFORM, 0, 2, 31, n, m)
+    for tour in (np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 5)):
+        got = ctx.split_eval(inst, tour, dem, full=True)
+        tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(n, Q, 1, 0.0, c, tour, dem)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
+        np.testing.assert_array_equal(got["feasible"], feas)
+        check_mean(got["agg"][0], mean)
