@@ -285,8 +285,9 @@ BatchResultSet<ScheduleResult> batched_expected_cost(const CustomerSpec& spec,
   out.evaluated.assign(m, 0);
   if (m == 0) return out;
   const scendp_customer c = to_c(spec, delivery, holding);
-  const auto shards = detail::make_shards(m, detail::devices_of(cfg));
-  detail::run_shards(shards, [&](const detail::Shard& s, scendp_ctx* ctx) {
+  const auto waves = detail::make_waves(detail::make_shards(m, detail::devices_of(cfg)), wave);
+  detail::run_waves(waves, oudp_per_scenario_bytes(spec), &out.timings,
+                    [&](std::size_t, const detail::Shard& s, scendp_ctx* ctx) {
     detail::check(scendp_ctx_set_max_batch(ctx, wave));
     schedules(ctx, c, scenarios.data.data() + s.lo * scenarios.rows, s.hi - s.lo,
               out.per_scenario.data() + s.lo, out.evaluated.data() + s.lo);

@@ -221,6 +221,64 @@ void run_shards(const std::vector<Shard>& shards,
     if (e) std::rethrow_exception(e);
 }
 
+std::vector<Shard> make_waves(const std::vector<Shard>& shards, std::size_t wave) {
+  std::vector<Shard> out;
+  const std::size_t w = std::max<std::size_t>(wave, 1);
+  for (const Shard& s : shards) {
+    if (s.hi == s.lo) {
+      out.push_back(s);
+      continue;
+    }
+    for (std::size_t lo = s.lo; lo < s.hi; lo += w)
+      out.push_back(Shard{lo, std::min(s.hi, lo + w), s.device});
+  }
+  return out;
+}
+
+void run_waves(const std::vector<Shard>& waves, std::uint64_t per_scenario_bytes,
+               std::vector<BatchTiming>* timings,
+               const std::function<void(std::size_t, const Shard&, scendp_ctx*)>& fn) {
+  std::vector<double> ms(waves.size(), 0.0);
+  // per device: the indices of its waves (contiguous, in scenario order)
+  std::vector<std::pair<int, std::vector<std::size_t>>> groups;
+  for (std::size_t i = 0; i < waves.size(); ++i) {
+    if (groups.empty() || groups.back().first != waves[i].device)
+      groups.push_back({waves[i].device, {}});
+    groups.back().second.push_back(i);
+  }
+  auto run_group = [&](const std::vector<std::size_t>& idx, int device) {
+    DeviceSlot& slot = device_slot(device);
+    std::lock_guard<std::mutex> g(slot.mu);
+    for (std::size_t i : idx) {
+      const std::uint64_t t0 = now_ns();
+      fn(i, waves[i], slot.ctx);
+      ms[i] = ms_since(t0);
+    }
+  };
+  if (groups.size() == 1) {
+    run_group(groups[0].second, groups[0].first);
+  } else {
+    std::vector<std::exception_ptr> errs(groups.size());
+    std::vector<std::thread> pool;
+    for (std::size_t gi = 0; gi < groups.size(); ++gi)
+      pool.emplace_back([&, gi] {
+        try {
+          run_group(groups[gi].second, groups[gi].first);
+        } catch (...) {
+          errs[gi] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  }
+  if (timings)
+    for (std::size_t i = 0; i < waves.size(); ++i) {
+      const std::size_t size = waves[i].hi - waves[i].lo;
+      timings->push_back({i, size, ms[i], static_cast<std::uint64_t>(size) * per_scenario_bytes});
+    }
+}
+
 std::size_t wave_size(const BackendConfig& cfg, std::size_t count,
                       std::uint64_t per_scenario_bytes, std::vector<std::string>* warnings) {
   cfg.validate();

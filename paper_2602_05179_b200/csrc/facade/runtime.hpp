@@ -47,6 +47,18 @@ std::vector<Shard> make_shards(std::size_t m, const std::vector<int>& devs);
 void run_shards(const std::vector<Shard>& shards,
                 const std::function<void(const Shard&, scendp_ctx*)>& fn);
 
+// The reference's run_batched batches (engine.hpp:150-192) on the GPU: every
+// device shard is cut into waves of `wave` scenarios (in scenario order), one
+// C-ABI call per wave, each timed.  run_waves runs fn(index, wave, ctx) for
+// every wave -- one host thread per device, its waves in order under the
+// device's call mutex -- and appends one BatchTiming per wave to `timings`
+// (batch index = wave index, bytes = size x per_scenario_bytes), in scenario
+// order like the reference's.
+std::vector<Shard> make_waves(const std::vector<Shard>& shards, std::size_t wave);
+void run_waves(const std::vector<Shard>& waves, std::uint64_t per_scenario_bytes,
+               std::vector<BatchTiming>* timings,
+               const std::function<void(std::size_t, const Shard&, scendp_ctx*)>& fn);
+
 // BackendConfig::batch_size / memory_budget -> per-call wave size
 // (adjust_batch_size, engine.cpp:7-20); appends the reference's warning.
 std::size_t wave_size(const BackendConfig& cfg, std::size_t count,

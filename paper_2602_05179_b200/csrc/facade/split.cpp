@@ -39,8 +39,9 @@ void check_inputs(const RoutingInstance& inst, const GiantTour& tour, std::size_
                                 " customers");
 }
 
-// Cost-only totals for scenarios given by `make_sc(shard)`, sharded over the
-// config's devices.
+// Cost-only totals for scenarios given by `make_sc(range)`, sharded over the
+// config's devices and cut into the reference's batches (one call and one
+// BatchTiming per wave, detail::run_waves).
 template <typename MakeSc>
 BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const GiantTour& tour,
                                         std::size_t count, MakeSc make_sc,
@@ -54,16 +55,15 @@ BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const Giant
     return out;
   }
   const scendp_routing r = to_c(inst);
-  const auto shards = detail::make_shards(count, detail::devices_of(cfg));
-  std::vector<double> shard_ms(shards.size());
-  std::vector<scendp_agg_raw> raws(shards.size());
+  const auto waves = detail::make_waves(detail::make_shards(count, detail::devices_of(cfg)), wave);
+  std::vector<scendp_agg_raw> raws(waves.size());
   // the reference's mean is a sequential fp64 sum (engine.hpp:195-211); when
   // every finite total is an integer and count * max|total| < 2^53, no
   // partial sum rounds, so it equals the engine's exact aggregate
   std::atomic<bool> integral{true};
   std::atomic<double> max_abs{0.0};
-  detail::run_shards(shards, [&](const detail::Shard& s, scendp_ctx* ctx) {
-    const std::uint64_t t0 = detail::now_ns();
+  detail::run_waves(waves, sizeof(ExtendedCost), &out.timings,
+                    [&](std::size_t wi, const detail::Shard& s, scendp_ctx* ctx) {
     detail::check(scendp_ctx_set_max_batch(ctx, wave));
     scendp_scenarios sc = make_sc(s);
     // totals land in the device slot's page-locked buffer (stored by the
@@ -72,7 +72,7 @@ BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const Giant
     scendp_split_out o{};
     o.mem_kind = SCENDP_MEM_HOST;
     o.totals = tot;
-    o.agg_raw = &raws[&s - shards.data()];
+    o.agg_raw = &raws[wi];
     detail::check(scendp_split_eval(ctx, &r, tour.order.data(), 1, &sc, SCENDP_SPLIT_COST_ONLY, &o));
     detail::parallel_for(s.hi - s.lo, [&](std::size_t a, std::size_t b) {
       bool whole = true;
@@ -91,11 +91,7 @@ BatchResultSet<ExtendedCost> costs_impl(const RoutingInstance& inst, const Giant
       while (mx > cur && !max_abs.compare_exchange_weak(cur, mx)) {
       }
     });
-    shard_ms[&s - shards.data()] = detail::ms_since(t0);
   });
-  for (std::size_t g = 0; g < shards.size(); ++g)
-    out.timings.push_back({g, shards[g].hi - shards[g].lo, shard_ms[g],
-                           (shards[g].hi - shards[g].lo) * sizeof(ExtendedCost)});
   scendp_agg agg{};
   detail::check(scendp_agg_finalize(raws.data(), static_cast<std::uint32_t>(raws.size()), 1, &agg));
   if (integral && agg.range_errors == 0 &&
@@ -352,14 +348,13 @@ BatchResultSet<SplitSolution> batched_expected_split(const RoutingInstance& inst
     return out;
   }
   const scendp_routing r = to_c(inst);
-  const auto shards = detail::make_shards(m, detail::devices_of(cfg));
-  detail::run_shards(shards, [&](const detail::Shard& s, scendp_ctx* ctx) {
-    const std::uint64_t t0 = detail::now_ns();
+  const auto waves = detail::make_waves(detail::make_shards(m, detail::devices_of(cfg)), wave);
+  detail::run_waves(waves, split_per_scenario_bytes(inst.n), &out.timings,
+                    [&](std::size_t, const detail::Shard& s, scendp_ctx* ctx) {
     detail::check(scendp_ctx_set_max_batch(ctx, wave));
     // hard -> linear deque, penalized -> quadratic (split.cpp:316-318)
     full_impl(ctx, r, tour, scenarios.data.data() + s.lo * scenarios.rows, s.hi - s.lo, false,
               out.per_scenario.data() + s.lo, detail::device_slot(s.device));
-    (void)t0;
   });
   detail::sequential_aggregate(out, [](const SplitSolution& s) { return s.total.value; });
   return out;

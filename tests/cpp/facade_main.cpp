@@ -109,6 +109,26 @@ int run_split(char** a) {
         same = x.values.values[i].value == y.values.values[i].value;
     }
     std::printf("sharded_equal %d\n", same ? 1 : 0);
+    // one BatchTiming per batch (engine.hpp:150-192): waves of 300 within
+    // each device shard, and on one device exactly the reference's batches
+    auto timing_sizes = [](const char* name, const std::vector<BatchTiming>& t, std::size_t per) {
+      std::vector<int> sz;
+      bool ok = true;
+      for (std::size_t i = 0; i < t.size(); ++i) {
+        sz.push_back(static_cast<int>(t[i].size));
+        ok = ok && t[i].batch_index == i && t[i].bytes_estimate == t[i].size * per &&
+             t[i].wall_ms >= 0.0;
+      }
+      print_ivec(name, sz);
+      std::printf("%s_ok %d\n", name, ok ? 1 : 0);
+    };
+    timing_sizes("timings_sharded", c2.timings, sizeof(ExtendedCost));
+    BackendConfig one = BackendConfig::gpu();
+    one.batch_size = 300;
+    timing_sizes("timings_one", batched_split_costs(inst, tour, batch, one).timings,
+                 sizeof(ExtendedCost));
+    timing_sizes("timings_full", batched_expected_split(inst, tour, batch, one).timings,
+                 split_per_scenario_bytes(n));
   }
   std::vector<double> v0;
   std::vector<int> c0, rcs;

@@ -30,7 +30,8 @@ def run(*args):
         elif t[0] in ("totals", "V4", "gen_totals", "trajectory", "frontiers", "batch_last"):
             res[t[0]] = np.array([float(x) for x in t[2:]])
         elif t[0] in ("cuts4", "route_count", "tour", "deliver", "quantity", "end_inventory",
-                      "route_option", "data", "col3"):
+                      "route_option", "data", "col3", "timings_sharded", "timings_one",
+                      "timings_full"):
             res[t[0]] = np.array([int(x) for x in t[2:]])
         elif t[0] == "route":
             res.setdefault("routes", []).append((int(t[1]), int(t[2])))
@@ -78,6 +79,14 @@ def test_facade_split_matches_reference(reference, n, Q, hard, beta, m, tseed):
     np.testing.assert_array_equal(got["route_count"], rc)
     assert got["full_mean"] == mean2
     assert got["sharded_equal"] == 1  # devices {0, 0}, batch_size 300: same bits
+    # one BatchTiming per batch: the reference's batches of 300 on one device
+    # (engine.hpp:150-192), and per device shard in the sharded call
+    ref_batches = [min(300, m - lo) for lo in range(0, m, 300)]
+    assert list(got["timings_one"]) == ref_batches and got["timings_one_ok"] == 1
+    assert list(got["timings_full"]) == ref_batches and got["timings_full_ok"] == 1
+    half = [m // 2, m - m // 2]
+    assert list(got["timings_sharded"]) == [min(300, h - lo) for h in half for lo in range(0, h, 300)]
+    assert got["timings_sharded_ok"] == 1
 
 
 def test_facade_dsirp_matches_reference(reference):
