@@ -64,7 +64,11 @@ def test_small_budget_runs_in_waves_identically(oracle):
         ra = a.split_eval(inst, tours, dem)
         fa = a.split_eval(inst, tour, dem, full=True)
         da = a.dsirp_eval(custs, dd, full=True)
-    budget = 80 << 20  # the fixed part (fallback scratch, staging chunk) plus ~1/8 of the call
+    # the fixed part under a small budget (the fallback scratch is sized to
+    # 1/8 of the budget, at least 2 CTAs per SM) plus ~1/8 of the call
+    with Context(0, scratch_limit=64 << 20) as p:
+        fp0 = p.split_eval(inst, tour, dem, full=True, footprint=True)
+    budget = fp0["fixed"] + fp0["per_scenario"] * (m // 8)
     with Context(0, scratch_limit=budget) as b:
         fp = b.split_eval(inst, tour, dem, full=True, footprint=True)
         assert fp["wave"] < m and fp["budget"] == budget
