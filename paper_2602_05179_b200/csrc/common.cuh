@@ -77,6 +77,31 @@ __device__ __forceinline__ uint32_t uniform_draw32(const GenParams& g, uint64_t 
   return static_cast<uint32_t>(g.lo) + static_cast<uint32_t>(hi >> 32);
 }
 
+// uniform_draw32(g, mix64(z)) with the low word of mix64's result computed
+// only when it can matter.  The draw is (x_hi*span + c) >> 32 with the carry
+// term c = (x_lo*span) >> 32 < span, so it differs from (x_hi*span) >> 32
+// only when the low word of x_hi*span is >= 2^32 - span + 1 (probability
+// ~span / 2^32 per draw: a branch that is almost never taken).  x_hi needs
+// only the high word of z (x = z ^ (z >> 31)); the low word costs the
+// shift/xor pair and a wide multiply it no longer always pays.  Same result
+// as uniform_draw32(g, mix64(z)) for every z.
+__device__ __forceinline__ uint32_t mix_uniform32(const GenParams& g, uint64_t z) {
+  z += kGamma;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  const uint32_t zh = static_cast<uint32_t>(z >> 32), zl = static_cast<uint32_t>(z);
+  const uint32_t xh = zh ^ (zh >> 31);
+  const uint64_t q = static_cast<uint64_t>(xh) * g.span32;
+  uint32_t r = static_cast<uint32_t>(q >> 32);
+  const uint32_t ql = static_cast<uint32_t>(q);
+  if (ql > 0xffffffffu - g.span32 + 1u) {
+    const uint32_t xl = zl ^ ((zl >> 31) | (zh << 1));
+    const uint32_t c = static_cast<uint32_t>((static_cast<uint64_t>(xl) * g.span32) >> 32);
+    r += (static_cast<uint64_t>(ql) + c) >> 32 ? 1u : 0u;
+  }
+  return static_cast<uint32_t>(g.lo) + r;
+}
+
 // One counter-based draw: DistributionSpec::sample for the kinds that use
 // exactly one next() per value (scenario.cpp:23-26; poisson: SURVEY App. A).
 __device__ __forceinline__ uint32_t draw_counter(const GenParams& g,

@@ -102,7 +102,7 @@ struct SplitArgs {
 __device__ __forceinline__ uint32_t demand_at(const SplitArgs& a, int src, uint64_t stream,
                                               const uint32_t* tile_base, uint32_t row) {
   if (src == kSrcTiled) return __ldg(tile_base + static_cast<uint64_t>(row) * kTile);
-  if (src == kSrcGenU32) return uniform_draw32(a.gen, mix64(stream + row * kGamma));
+  if (src == kSrcGenU32) return mix_uniform32(a.gen, stream + row * kGamma);
   return draw_counter(a.gen, stream, row);
 }
 

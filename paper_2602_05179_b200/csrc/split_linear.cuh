@@ -296,14 +296,14 @@ __device__ __forceinline__ void k1_demand4(const SplitArgs& a, uint64_t stream,
   } else if constexpr (IDENT && SRC != kSrcTiled) {
     // rows s0..s0+3: consecutive SplitMix64 counters, one multiply per chunk
     const uint64_t ctr = stream + static_cast<uint64_t>(static_cast<uint32_t>(s0)) * kGamma;
-    auto val = [&](uint64_t x) {
-      if constexpr (SRC == kSrcGenU32) return uniform_draw32(a.gen, x);
-      else return draw_value(a.gen, x);
+    auto val = [&](uint64_t z) {
+      if constexpr (SRC == kSrcGenU32) return mix_uniform32(a.gen, z);
+      else return draw_value(a.gen, mix64(z));
     };
-    d0 = val(mix64(ctr));
-    d1 = val(mix64(ctr + kGamma));
-    d2 = val(mix64(ctr + 2 * kGamma));
-    d3 = val(mix64(ctr + 3 * kGamma));
+    d0 = val(ctr);
+    d1 = val(ctr + kGamma);
+    d2 = val(ctr + 2 * kGamma);
+    d3 = val(ctr + 3 * kGamma);
   } else {
     uint4 c;
     if constexpr (IDENT) c = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);

@@ -450,3 +450,21 @@ def test_handoff_full_solutions(ctx, oracle, reference, costs):
         np.testing.assert_array_equal(got["route_count"], rc)
         np.testing.assert_array_equal(got["feasible"], feas)
         check_mean(got["agg"][0], mean)
+
+
+@pytest.mark.parametrize("lo,hi,Q", [(0, 1, 3), (1, 10, 100), (0, 999_999, 3_000_000),
+                                     (5, (1 << 31) + 6, (1 << 31) - 1),
+                                     (0, (1 << 32) - 2, (1 << 31) - 1)])
+def test_fused_uniform_draws_all_spans(ctx, oracle, lo, hi, Q):
+    """K1's fused generator computes mix64's low word only when the draw's
+    carry term can matter (probability ~span / 2^32); identity and random
+    tours over spans 2 .. 2^32-1 give the reference's demands, hence its
+    totals (checked against the materialized host batch)."""
+    n, m = 60, 40_000
+    inst = RoutingInstance(n, Q, True, 0.0, oracle.make_random_instance(n, 2))
+    dist = Distribution("uniform", lo, hi, seed=oracle.derive_stream(7, TAG_SCENARIO, hi))
+    host = oracle.generate(UNIFORM, lo, hi, dist.seed, n, m)
+    for tour in (np.arange(1, n + 1, dtype=np.int32), rand_tour(n, 4)):
+        want = oracle.split_batch(n, Q, 1, 0.0, inst.costs, tour, host)
+        got = ctx.split_eval(inst, tour, dist, count=m)
+        np.testing.assert_array_equal(got["totals"][0], want)
