@@ -77,6 +77,7 @@ struct SplitArgs {
   int32_t npad;
   int32_t ident;         // every tour is the identity 1..n
   uint32_t pen_lmax;     // K2-int: loads above this leave the exact int32 range
+  int32_t pen_bits;      // K2-bits (window bitmap): Q <= 127, demands known in [1, 31]
   const uint32_t* ccol;  // customer row of position s+1
   const int32_t* itab;   // [k][2][npad]: A = dist+ret, B = c0 - dist_next (int path)
   const double* dtab;    // [k][npad][4]: dist, ret, c0, dist_next (interleaved)
@@ -149,6 +150,28 @@ __device__ __forceinline__ void push_overflow(const SplitArgs& a, uint32_t k, ui
 
 #include "split_linear.cuh"
 #include "split_penal.cuh"
+#include "split_penal_bits.cuh"
+
+// K2-bits eligibility of a materialized wave: does any valid scenario hold a
+// demand outside [dlo, dhi]?  One pass over the tiled wave (lanes beyond m
+// of the last tile are padding and skipped); a warp vote, one atomic per
+// warp that saw one.
+__global__ void demand_range_kernel(const uint32_t* __restrict__ tiled, uint32_t rows, uint64_t m,
+                                    uint32_t dlo, uint32_t dhi, unsigned int* outside) {
+  const uint64_t total = ((m + 31) / 32) * static_cast<uint64_t>(rows) * kTile;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 4;
+  bool bad = false;
+  for (uint64_t e = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 4; e < total;
+       e += stride) {
+    // 4 consecutive lanes of one row (kTile is a multiple of 4)
+    const uint4 v = *reinterpret_cast<const uint4*>(tiled + e);
+    const uint64_t w = (e / (static_cast<uint64_t>(rows) * kTile)) * kTile + (e & 31);
+    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bad |= w + j < m && (vv[j] < dlo || vv[j] > dhi);
+  }
+  if (__any_sync(__activemask(), bad) && (threadIdx.x & 31) == 0) atomicOr(outside, 1u);
+}
 
 // ---------------------------------------------------------------------------
 // K2: O(n^2) Bellman min (split.cpp:45-75), penalized (or forced) mode.
@@ -779,14 +802,20 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   if (!linear && !a.hard && a.pen_lmax > 0 && small_tables) {
     const int T = kPenThreads;
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + 2 * 4) +
-                        static_cast<size_t>(T) * penal_ring_bytes(FULL);
+                        static_cast<size_t>(T) * (a.pen_bits ? penal_bits_ring_bytes(FULL)
+                                                             : penal_ring_bytes(FULL));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {
       set_smem(kernel, smem);
       kernel<<<grid, T, smem, ctx->stream>>>(a);
     };
-    if (a.ident) go(split_penal_kernel<FULL, SRC, true>);
-    else go(split_penal_kernel<FULL, SRC, false>);
+    if (a.pen_bits) {
+      if (a.ident) go(split_penal_bits_kernel<FULL, SRC, true>);
+      else go(split_penal_bits_kernel<FULL, SRC, false>);
+    } else {
+      if (a.ident) go(split_penal_kernel<FULL, SRC, true>);
+      else go(split_penal_kernel<FULL, SRC, false>);
+    }
   } else if (use_generic_range || !small_tables) {
     const uint64_t items = static_cast<uint64_t>(a.k) * a.m_wave;
     split_generic_kernel<FULL, SRC><<<generic_blocks, kGenericThreads, 0, ctx->stream>>>(
@@ -1165,6 +1194,7 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
         const double lm = inst->penalty_beta > 0.0 ? room / inst->penalty_beta : 2147483647.0;
         a.pen_lmax = static_cast<uint32_t>(std::min(lm, 2147483647.0 - static_cast<double>(inst->capacity)));
       }
+      a.pen_bits = 0;
       a.ccol = reinterpret_cast<const uint32_t*>(dtab + o_ccol);
       a.itab = tt.intv ? reinterpret_cast<const int32_t*>(dtab + o_itab) : nullptr;
       a.dtab = reinterpret_cast<const double*>(dtab + o_dtab);
@@ -1187,6 +1217,31 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       a.ovf_bits = reinterpret_cast<uint32_t*>(wb.handoff);
       if (w0 > 0) CUDA_CHECK(cudaMemsetAsync(d_ovf_count, 0, 4, ctx->stream));
       const bool u32 = fused && gp.kind == SCENDP_DIST_UNIFORM && gp.span32 != 0;
+      // K2-bits (window bitmap) when Q <= 127 and every demand of the wave is
+      // known to lie in [1, min(31, Q)]: from the distribution for generated
+      // demands, else from one pass over the materialized wave (a 4-byte
+      // read-back; the penalized pass it selects for runs ~100x longer)
+      if (!linear && !inst->hard && a.pen_lmax > 0 && inst->capacity <= 127 &&
+          !std::getenv("SCENDP_K2_NO_BITS")) {
+        const uint32_t dhi = static_cast<uint32_t>(std::min<int64_t>(31, inst->capacity));
+        if (fused) {
+          a.pen_bits = gp.kind == SCENDP_DIST_UNIFORM && gp.lo >= 1 &&
+                       static_cast<uint64_t>(gp.lo) + gp.span - 1 <= dhi;
+        } else {
+          unsigned int* d_out = d_ovf_count + 2;
+          CUDA_CHECK(cudaMemsetAsync(d_out, 0, 4, ctx->stream));
+          const int blocks = std::max(1, std::min<int>(ctx->sm_count * 8,
+              static_cast<int>((((mw + 31) / 32) * n * 32 / 4 + 255) / 256)));
+          demand_range_kernel<<<blocks, 256, 0, ctx->stream>>>(tiled, static_cast<uint32_t>(n), mw,
+                                                               1u, dhi, d_out);
+          CUDA_CHECK(cudaGetLastError());
+          ctx->count_launch();
+          unsigned int outside = 1;
+          CUDA_CHECK(cudaMemcpyAsync(&outside, d_out, 4, cudaMemcpyDeviceToHost, ctx->stream));
+          CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+          a.pen_bits = outside == 0;
+        }
+      }
       last_a = a;
       last_src = u32 ? kSrcGenU32 : fused ? kSrcGen : kSrcTiled;
       defer_ovf = syncs && !full && w0 == 0 && mw == m && !ctx->nccl_comm;

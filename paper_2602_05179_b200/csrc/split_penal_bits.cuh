@@ -1,0 +1,275 @@
+// split_penal_bits.cuh -- K2-bits: the penalized O(n) split (split_penal.cuh)
+// with the window start counted from a register bitmap instead of walked.
+// Included by split.cu after split_penal.cuh.  Reference:
+// split_core_quadratic, proj/src/split.cpp:45-75.
+//
+// Same decomposition as K2-int (window A = {L_i - L_p <= Q}: the deque front;
+// prefix B = [0, lo): PM(lo-1) + beta (L_i - Q)); what changes is how lo, the
+// number of positions whose load is below the threshold T_i = L_i - Q, is
+// kept.  When every demand of a scenario is in [1, 31] the loads are
+// strictly increasing, so each position owns one load value, and a 128-bit
+// register bitmap R holds the positions inside the window relative to the
+// threshold: bit k <-> load T + k.  Per position i (d = d_i, T' = T + d):
+//   * the positions leaving the window are those with loads in [T, T'):
+//     bits 0 .. d-1, so lo += popc(R & (2^d - 1));
+//   * R >>= d (the threshold moved by d);
+//   * position i, load L_i = T' + Q, enters at bit Q (Q <= 127).
+// Branch-free, no per-lane loop: the round-1 kernel walked the window start
+// through a ring of loads, a data-dependent loop under SIMT divergence
+// (K2).  The ring of loads is gone (2 B per position per
+// thread), so more CTAs fit on an SM.  A demand outside [1, 31] (a zero
+// demand merges load values; d > 31 spans bitmap words) sends the scenario
+// to the generic kernel, like a ring overflow; the host takes this kernel
+// only when the call's demands are known to lie in [1, 31] and Q <= 127.
+#pragma once
+
+// Host side: bytes of the K2-bits rings per thread (split.cu sizes the CTA):
+// deque f (4) [| rc (4)] and positions (2); PM ring (4) [| index, rc (8)].
+__host__ __device__ constexpr int penal_bits_ring_bytes(bool full) {
+  return kRing * (4 + 2 + (full ? 4 : 0)) + kPosRing * (4 + (full ? 8 : 0));
+}
+
+template <bool FULL, int SRC, bool IDENT>
+__global__ void __launch_bounds__(kPenThreads)
+split_penal_bits_kernel(SplitArgs a) {
+  constexpr int T = kPenThreads;
+  extern __shared__ __align__(16) char smem[];
+  __shared__ unsigned long long s_agg[kAggSlots];
+  const uint32_t k = blockIdx.y;
+  const int n = a.n;
+  const int npad = a.npad;
+  const int tid = threadIdx.x;
+  // thread-minor rings, 4-byte arrays first: deque f [| rc], PM [| PM index
+  // | PM rc]; then the 2-byte deque positions.  Counters are byte offsets of
+  // 2-byte slots (at16 / at32 of split_penal.cuh).
+  int32_t* dq_f = reinterpret_cast<int32_t*>(smem) + tid;
+  int32_t* dq_r = dq_f + kRing * T;                                            // FULL
+  int32_t* ps_pm = dq_f + (FULL ? 2 : 1) * kRing * T;
+  int32_t* ps_pi = ps_pm + kPosRing * T;                                       // FULL
+  int32_t* ps_pr = ps_pi + kPosRing * T;                                       // FULL
+  uint16_t* dq_p = reinterpret_cast<uint16_t*>(ps_pm - tid + (FULL ? 3 : 1) * kPosRing * T) + tid;
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + T * penal_bits_ring_bytes(FULL));
+  int32_t* s_tab = reinterpret_cast<int32_t*>(s_col + (IDENT ? 0 : npad));  // A | B
+  {
+    const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
+    if (!IDENT)
+      for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
+    const int32_t* g = a.itab + static_cast<uint64_t>(k) * 2 * npad;
+    for (int x = threadIdx.x; x < 2 * npad; x += T) s_tab[x] = g[x];
+  }
+  agg_cta_init(s_agg);
+  __syncthreads();
+
+  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;
+  uint32_t Qc = static_cast<uint32_t>(a.Q);  // host: Q <= 127
+  Qc += static_cast<uint32_t>(a.m_total >> 62);  // + 0, keeps Q in a register
+  const int32_t beta = static_cast<int32_t>(a.beta);
+  const uint32_t lmax = a.pen_lmax;  // loads above this leave the exact range
+  // bit Q of the 128-bit bitmap, as four word masks (one is non-zero)
+  const uint32_t qb = 1u << (Qc & 31);
+  const uint32_t qm0 = (Qc >> 5) == 0 ? qb : 0u, qm1 = (Qc >> 5) == 1 ? qb : 0u,
+                 qm2 = (Qc >> 5) == 2 ? qb : 0u, qm3 = (Qc >> 5) == 3 ? qb : 0u;
+
+  int32_t v = 0;
+  bool ok = true;
+  int32_t rc = 0;
+  if (active) {
+    const uint32_t* tile_base = nullptr;
+    uint64_t stream = 0;
+    if (SRC == kSrcTiled) tile_base = a.tiled + (wl >> 5) * static_cast<uint64_t>(n) * kTile + (wl & 31);
+    else stream = derive_stream(a.gen.seed, kStreamScenario, a.gen.first_index + wl);
+    double* Vout = nullptr;
+    int32_t* Cout = nullptr;
+    if (FULL) {
+      const uint64_t base = ((w >> 5) * static_cast<uint64_t>(n + 1)) * kTile + (w & 31);
+      Vout = a.V + base;
+      Cout = a.cuts + base;
+      Vout[0] = 0.0;
+      Cout[0] = 0;
+    }
+    // position 0: f(0) = (0.0 + c(0, s_1)) - dist[1], L_0 = 0, g(0) = f(0)
+    const int32_t f0 = a.f0i[k];
+    ps_pm[0] = f0;
+    if (FULL) {
+      ps_pi[0] = 0;
+      ps_pr[0] = 0;
+    }
+    // deque: -inf sentinel in slot 0, entry p = 0 in slot 1 (K1 layout)
+    dq_f[0] = INT32_MIN;
+    dq_f[T] = f0;
+    dq_p[T] = 0;
+    if (FULL) dq_r[T] = 0;
+    int head = kH, tail = 2 * kH;       // deque slot counters
+    int32_t front_f = f0, back_f = f0;
+    int front_p = 0;                    // position of the deque front
+    int32_t front_rc = 0;
+    int lo_c = 0;                       // window start lo, as a position counter (lo * kH)
+    int32_t bmin = kPenInf;             // PM(lo - 1); kPenInf while lo == 0
+    int32_t bidx = -1, brc = 0;
+    int32_t pm = f0, pm_i = 0, pm_rc = 0;  // running prefix minimum of g
+    uint32_t load = 0;
+    // window bitmap: bit j <-> load T + j (T = load - Q); position 0 (load 0)
+    // sits at bit Q
+    uint32_t R0 = qm0, R1 = qm1, R2 = qm2, R3 = qm3;
+
+    // one DP position (i_c = i * kH); d in [1, 31] and ring room are checked
+    // per chunk by the caller
+    auto step = [&](int i, int i_c, uint32_t d, int32_t Ai, int32_t Bi, auto push_tag) {
+      constexpr bool PUSH = decltype(push_tag)::value;
+      load += d;
+      // positions whose load fell below the new threshold: bits 0 .. d-1
+      const int leave = __popc(R0 & ((1u << d) - 1u));
+      R0 = __funnelshift_r(R0, R1, d);
+      R1 = __funnelshift_r(R1, R2, d);
+      R2 = __funnelshift_r(R2, R3, d);
+      R3 >>= d;
+      if (leave) {
+        lo_c += leave * kH;
+        const int pc = lo_c - kH;  // lo - 1
+        bmin = at32(ps_pm, pc, kPosMaskH);
+        if (FULL) {
+          bidx = at32(ps_pi, pc, kPosMaskH);
+          brc = at32(ps_pr, pc, kPosMaskH);
+        }
+        // deque entries before lo leave from the front (entry i-1 stays:
+        // d_i <= 31 < ... its load is >= T' since d_i <= Q); the vacated slot
+        // becomes the -inf sentinel below the head
+        const int lo = static_cast<int>(static_cast<unsigned>(lo_c) / kH);
+        if (front_p < lo) {
+          do {
+            at32(dq_f, head, kDqMaskH) = INT32_MIN;
+            head += kH;
+            front_p = at16(dq_p, head, kDqMaskH);
+          } while (front_p < lo);
+          front_f = at32(dq_f, head, kDqMaskH);
+          if (FULL) front_rc = at32(dq_r, head, kDqMaskH);
+        }
+      }
+      // candidates: window A (deque front) and prefix B (prefix minimum)
+      const int32_t candA = front_f + Ai;
+      const int32_t candB = lo_c > 0 ? bmin + Ai + beta * static_cast<int32_t>(load - Qc) : kPenInf;
+      const bool useB = candB <= candA;  // B's indices come first: ties go to B
+      v = useB ? candB : candA;
+      if (FULL) {
+        rc = (useB ? brc : front_rc) + 1;
+        Vout[static_cast<uint64_t>(i) * kTile] = static_cast<double>(v);
+        Cout[static_cast<uint64_t>(i) * kTile] = useB ? bidx : front_p;
+      }
+      if constexpr (PUSH) {
+        const int32_t fi = v + Bi;
+        const int32_t g = fi - beta * static_cast<int32_t>(load);
+        if (g < pm) {  // strict: the earliest minimum stays
+          pm = g;
+          if (FULL) {
+            pm_i = i;
+            pm_rc = rc;
+          }
+        }
+        at32(ps_pm, i_c, kPosMaskH) = pm;
+        if (FULL) {
+          at32(ps_pi, i_c, kPosMaskH) = pm_i;
+          at32(ps_pr, i_c, kPosMaskH) = pm_rc;
+        }
+        // position i enters the window bitmap at bit Q (load T' + Q)
+        R0 |= qm0;
+        R1 |= qm1;
+        R2 |= qm2;
+        R3 |= qm3;
+        // strict pop (sentinel-terminated), then push (K1 deque); the deque
+        // is non-empty here, so it can only empty by popping
+        if (back_f > fi) {
+          do {
+            tail -= kH;
+            back_f = at32(dq_f, tail - kH, kDqMaskH);
+          } while (back_f > fi);
+          if (tail == head) {
+            front_f = fi;
+            front_p = i;
+            if (FULL) front_rc = rc;
+          }
+        }
+        at32(dq_f, tail, kDqMaskH) = fi;
+        at16(dq_p, tail, kDqMaskH) = static_cast<uint16_t>(i);
+        if (FULL) at32(dq_r, tail, kDqMaskH) = rc;
+        tail += kH;
+        back_f = fi;
+      }
+    };
+    auto load4 = [&](int s0, uint32_t (&dd)[4]) {
+      uint4 cr = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
+      if (!IDENT) cr = *reinterpret_cast<const uint4*>(s_col + s0);
+      const uint32_t rows[4] = {cr.x, cr.y, cr.z, cr.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        dd[j] = s0 + j < n ? demand_at(a, SRC, stream, tile_base, rows[j]) : 1u;
+    };
+    auto tab4 = [&](int s0, int4& A4, int4& B4) {
+      A4 = *reinterpret_cast<const int4*>(s_tab + s0);
+      B4 = *reinterpret_cast<const int4*>(s_tab + npad + s0);
+    };
+    using Push = std::true_type;
+    using Last = std::false_type;
+    // room for 4 pushes: the PM ring must hold [lo-1, i] for every i of the
+    // chunk, the deque its live entries + 4 + the sentinel slot
+    auto room = [&](int s0) {
+      return (s0 + 4) * kH - lo_c <= (kPosRing - 2) * kH &&
+             (tail - head) + 4 * kH <= (kRing - 1) * kH;
+    };
+    // every demand of the chunk in [1, 31] (and <= Q: 31 < Q is not
+    // required -- Q >= 1 and d <= Q keeps entry i-1 in the window, checked)
+    auto dem_ok = [&](const uint32_t (&dd)[4]) {
+      const uint32_t mx = max(max(dd[0], dd[1]), max(dd[2], dd[3]));
+      const uint32_t mn = min(min(dd[0], dd[1]), min(dd[2], dd[3]));
+      return mn >= 1u && mx <= min(31u, Qc);
+    };
+    const int npush = n - 1;
+    uint32_t dc[4], dn[4] = {1u, 1u, 1u, 1u};
+    load4(0, dc);
+    int s0 = 0;
+    for (; s0 + 4 <= npush; s0 += 4) {
+      if (s0 + 4 < n) load4(s0 + 4, dn);
+      if (!dem_ok(dc) || !room(s0)) {
+        ok = false;
+        break;
+      }
+      int4 A4, B4;
+      tab4(s0, A4, B4);
+      step(s0 + 1, (s0 + 1) * kH, dc[0], A4.x, B4.x, Push{});
+      step(s0 + 2, (s0 + 2) * kH, dc[1], A4.y, B4.y, Push{});
+      step(s0 + 3, (s0 + 3) * kH, dc[2], A4.z, B4.z, Push{});
+      step(s0 + 4, (s0 + 4) * kH, dc[3], A4.w, B4.w, Push{});
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dc[j] = dn[j];
+    }
+    if (ok) {
+      if (!dem_ok(dc) || !room(s0)) {
+        ok = false;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = s0 + j + 1;
+          const int32_t Ai = s_tab[i - 1], Bi = s_tab[npad + i - 1];
+          if (i < n) step(i, i * kH, dc[j], Ai, Bi, Push{});
+          else if (i == n) step(i, i * kH, dc[j], Ai, Bi, Last{});
+        }
+      }
+    }
+    if (ok && load > lmax) ok = false;  // values may have left the exact range
+    if (!ok) {
+      push_overflow(a, k, wl);
+    } else {
+      if (a.totals) a.totals[static_cast<uint64_t>(k) * a.m_total + w] = static_cast<double>(v);
+      if (FULL) {
+        a.route_count[w] = rc;
+        a.feasible[w] = 1;
+      }
+    }
+  }
+  const double vout = active && ok ? static_cast<double>(v) : 0.0;
+  __syncwarp();
+  agg_warp_add(s_agg, agg_pieces(vout, true), active && ok);
+  __syncthreads();
+  agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
+}

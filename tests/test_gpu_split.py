@@ -468,3 +468,40 @@ def test_fused_uniform_draws_all_spans(ctx, oracle, lo, hi, Q):
         want = oracle.split_batch(n, Q, 1, 0.0, inst.costs, tour, host)
         got = ctx.split_eval(inst, tour, dist, count=m)
         np.testing.assert_array_equal(got["totals"][0], want)
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_penalized_window_bitmap_kernel(ctx, oracle, reference, full):
+    """K2-bits: penalized split with the window start counted from a 128-bit
+    register bitmap, taken when Q <= 127 and every demand of the wave lies in
+    [1, min(31, Q)] -- decided from the distribution (generated demands) or
+    from a pass over the materialized wave.  Both kernels are exact, so a
+    wave with one zero demand (old kernel) and one without (bitmap kernel)
+    must both match the reference; Q = 127 puts the entry bit at the top of
+    the bitmap, demands up to 31 shift it by a full word less one."""
+    n, m = 57, 3000
+    for Q, lo, hi in ((127, 1, 31), (100, 1, 10), (40, 3, 31)):
+        inst = RoutingInstance(n, Q, False, 7.0, oracle.make_random_instance(n, Q))
+        tour = rand_tour(n, Q)
+        dem = oracle.generate(UNIFORM, lo, hi, 17 + Q, n, m)
+        variants = [dem]
+        z = dem.copy()
+        z[m - 1, n // 2] = 0  # the last scenario: a zero demand -> the ring kernel
+        variants.append(z)
+        for d in variants:
+            got = ctx.split_eval(inst, tour, d, full=full)
+            if full:
+                tot, V, cuts, rc, feas, (mean, fc, ic) = reference.expected_split(
+                    n, Q, 0, 7.0, inst.costs, tour, d)
+                np.testing.assert_array_equal(got["V"], V)
+                np.testing.assert_array_equal(got["cuts"], cuts)
+                np.testing.assert_array_equal(got["route_count"], rc)
+            else:
+                tot, (mean, fc, ic) = reference.split_costs(n, Q, 0, 7.0, inst.costs, tour, d)
+            np.testing.assert_array_equal(got["totals"][0], tot)
+            check_mean(got["agg"][0], mean)
+        # generated demands: the decision comes from the distribution
+        dist = Distribution("uniform", lo, hi, seed=oracle.derive_stream(3, TAG_SCENARIO, Q))
+        host = oracle.generate(UNIFORM, lo, hi, dist.seed, n, m)
+        want = oracle.split_batch(n, Q, 0, 7.0, inst.costs, tour, host)
+        np.testing.assert_array_equal(ctx.split_eval(inst, tour, dist, count=m)["totals"][0], want)
