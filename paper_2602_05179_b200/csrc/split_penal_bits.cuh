@@ -29,6 +29,16 @@ __host__ __device__ constexpr int penal_bits_ring_bytes(bool full) {
   return kRing * (4 + 2 + (full ? 4 : 0)) + kPosRing * (4 + (full ? 8 : 0));
 }
 
+template <int OFF>
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)));
+}
+
 template <bool FULL, int SRC, bool IDENT>
 __global__ void __launch_bounds__(kPenThreads)
 split_penal_bits_kernel(SplitArgs a) {
@@ -96,12 +106,22 @@ split_penal_bits_kernel(SplitArgs a) {
       ps_pi[0] = 0;
       ps_pr[0] = 0;
     }
-    // deque: -inf sentinel in slot 0, entry p = 0 in slot 1 (K1 layout)
+    // deque: -inf sentinel in slot 0, entry p = 0 in slot 1 (K1 layout).  As
+    // in K1 the ring is not circular and its ends are 32-bit shared
+    // addresses of f-plane slots (one LDS/STS with an immediate offset per
+    // access, rc plane at +kDqPlane); the 2-byte position plane of a slot is
+    // at (f address >> 1) + pofs.  Live entries move back to the bottom when
+    // a chunk's pushes would run past the end (rare: the head advances only
+    // by window evictions of the front).
+    constexpr int kDqStep = T * 4, kDqPlane = kRing * kDqStep;
+    const uint32_t fbase = smem_addr(dq_f);
+    const uint32_t pofs = smem_addr(dq_p) - (fbase >> 1);
+    auto pa = [&](uint32_t fa) { return (fa >> 1) + pofs; };
     dq_f[0] = INT32_MIN;
     dq_f[T] = f0;
     dq_p[T] = 0;
     if (FULL) dq_r[T] = 0;
-    int head = kH, tail = 2 * kH;       // deque slot counters
+    uint32_t head = fbase + kDqStep, tail = fbase + 2 * kDqStep;
     int32_t front_f = f0, back_f = f0;
     int front_p = 0;                    // position of the deque front
     int32_t front_rc = 0;
@@ -139,12 +159,12 @@ split_penal_bits_kernel(SplitArgs a) {
         const int lo = static_cast<int>(static_cast<unsigned>(lo_c) / kH);
         if (front_p < lo) {
           do {
-            at32(dq_f, head, kDqMaskH) = INT32_MIN;
-            head += kH;
-            front_p = at16(dq_p, head, kDqMaskH);
+            sts32<0>(head, static_cast<uint32_t>(INT32_MIN));
+            head += kDqStep;
+            front_p = static_cast<int>(lds16<0>(pa(head)));
           } while (front_p < lo);
-          front_f = at32(dq_f, head, kDqMaskH);
-          if (FULL) front_rc = at32(dq_r, head, kDqMaskH);
+          front_f = static_cast<int32_t>(lds32<0>(head));
+          if (FULL) front_rc = static_cast<int32_t>(lds32<kDqPlane>(head));
         }
       }
       // candidates: window A (deque front) and prefix B (prefix minimum)
@@ -181,8 +201,8 @@ split_penal_bits_kernel(SplitArgs a) {
         // is non-empty here, so it can only empty by popping
         if (back_f > fi) {
           do {
-            tail -= kH;
-            back_f = at32(dq_f, tail - kH, kDqMaskH);
+            tail -= kDqStep;
+            back_f = static_cast<int32_t>(lds32<-kDqStep>(tail));
           } while (back_f > fi);
           if (tail == head) {
             front_f = fi;
@@ -190,10 +210,10 @@ split_penal_bits_kernel(SplitArgs a) {
             if (FULL) front_rc = rc;
           }
         }
-        at32(dq_f, tail, kDqMaskH) = fi;
-        at16(dq_p, tail, kDqMaskH) = static_cast<uint16_t>(i);
-        if (FULL) at32(dq_r, tail, kDqMaskH) = rc;
-        tail += kH;
+        sts32<0>(tail, static_cast<uint32_t>(fi));
+        sts16(pa(tail), static_cast<uint32_t>(i));
+        if (FULL) sts32<kDqPlane>(tail, static_cast<uint32_t>(rc));
+        tail += kDqStep;
         back_f = fi;
       }
     };
@@ -214,8 +234,21 @@ split_penal_bits_kernel(SplitArgs a) {
     // room for 4 pushes: the PM ring must hold [lo-1, i] for every i of the
     // chunk, the deque its live entries + 4 + the sentinel slot
     auto room = [&](int s0) {
-      return (s0 + 4) * kH - lo_c <= (kPosRing - 2) * kH &&
-             (tail - head) + 4 * kH <= (kRing - 1) * kH;
+      if ((s0 + 4) * kH - lo_c > (kPosRing - 2) * kH) return false;
+      if (tail + 4 * kDqStep <= fbase + kDqPlane) return true;
+      // compact: the sentinel and the live entries back to slots 0..len
+      const uint32_t len = (tail - head) / kDqStep;
+      if (len + 5 > static_cast<uint32_t>(kRing)) return false;
+      uint32_t dst = fbase + kDqStep;
+      for (uint32_t src = head; src < tail; src += kDqStep, dst += kDqStep) {
+        sts32<0>(dst, lds32<0>(src));
+        sts16(pa(dst), lds16<0>(pa(src)));
+        if (FULL) sts32<kDqPlane>(dst, lds32<kDqPlane>(src));
+      }
+      sts32<0>(fbase, static_cast<uint32_t>(INT32_MIN));
+      head = fbase + kDqStep;
+      tail = dst;
+      return true;
     };
     // every demand of the chunk in [1, 31] (and <= Q: 31 < Q is not
     // required -- Q >= 1 and d <= Q keeps entry i-1 in the window, checked)

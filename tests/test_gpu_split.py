@@ -505,3 +505,20 @@ def test_penalized_window_bitmap_kernel(ctx, oracle, reference, full):
         host = oracle.generate(UNIFORM, lo, hi, dist.seed, n, m)
         want = oracle.split_batch(n, Q, 0, 7.0, inst.costs, tour, host)
         np.testing.assert_array_equal(ctx.split_eval(inst, tour, dist, count=m)["totals"][0], want)
+    # deque compaction: a line metric (f grows along the identity tour, the
+    # front leaves by window exits) with a ~3-position window moves the
+    # deque's head at almost every position, so its entries are moved back
+    # to the ring's bottom every few chunks
+    n2, Q2 = 203, 12
+    idx = np.arange(n2 + 2, dtype=np.float64)
+    line = RoutingInstance(n2, Q2, False, 3.0, np.abs(idx[:, None] - idx[None, :]))
+    d2 = oracle.generate(UNIFORM, 3, 5, 29, n2, 2000)
+    t2 = np.arange(1, n2 + 1, dtype=np.int32)
+    got = ctx.split_eval(line, t2, d2, full=full)
+    tot, (mean, fc, ic) = reference.split_costs(n2, Q2, 0, 3.0, line.costs, t2, d2)
+    np.testing.assert_array_equal(got["totals"][0], tot)
+    if full:
+        _, V, cuts, rc, _, _ = reference.expected_split(n2, Q2, 0, 3.0, line.costs, t2, d2)
+        np.testing.assert_array_equal(got["V"], V)
+        np.testing.assert_array_equal(got["cuts"], cuts)
+        np.testing.assert_array_equal(got["route_count"], rc)
