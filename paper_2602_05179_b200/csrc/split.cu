@@ -810,8 +810,17 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
       kernel<<<grid, T, smem, ctx->stream>>>(a);
     };
     if (a.pen_bits) {
-      if (a.ident) go(split_penal_bits_kernel<FULL, SRC, true>);
-      else go(split_penal_bits_kernel<FULL, SRC, false>);
+      auto bits = [&](auto ident) {
+        constexpr bool I = decltype(ident)::value;
+        switch (a.Q >> 5) {
+          case 0: go(split_penal_bits_kernel<FULL, SRC, I, 1>); break;
+          case 1: go(split_penal_bits_kernel<FULL, SRC, I, 2>); break;
+          case 2: go(split_penal_bits_kernel<FULL, SRC, I, 3>); break;
+          default: go(split_penal_bits_kernel<FULL, SRC, I, 4>); break;
+        }
+      };
+      if (a.ident) bits(std::true_type{});
+      else bits(std::false_type{});
     } else {
       if (a.ident) go(split_penal_kernel<FULL, SRC, true>);
       else go(split_penal_kernel<FULL, SRC, false>);

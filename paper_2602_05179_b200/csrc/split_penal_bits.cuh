@@ -13,7 +13,9 @@
 //   * the positions leaving the window are those with loads in [T, T'):
 //     bits 0 .. d-1, so lo += popc(R & (2^d - 1));
 //   * R >>= d (the threshold moved by d);
-//   * position i, load L_i = T' + Q, enters at bit Q (Q <= 127).
+//   * position i, load L_i = T' + Q, enters at bit Q (Q <= 127; the kernel
+//     is instantiated per bitmap width W = Q/32 + 1 words, so bit Q is in
+//     the top word: one OR).
 // Branch-free, no per-lane loop: the round-1 kernel walked the window start
 // through a ring of loads, a data-dependent loop under SIMT divergence
 // (K2).  The ring of loads is gone (2 B per position per
@@ -39,7 +41,9 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)));
 }
 
-template <bool FULL, int SRC, bool IDENT>
+// W: bitmap words, Q in [32 (W-1), 32 W) -- the entry bit Q then always sits
+// in the top word (one OR per position, W funnel shifts)
+template <bool FULL, int SRC, bool IDENT, int W>
 __global__ void __launch_bounds__(kPenThreads)
 split_penal_bits_kernel(SplitArgs a) {
   constexpr int T = kPenThreads;
@@ -77,10 +81,8 @@ split_penal_bits_kernel(SplitArgs a) {
   Qc += static_cast<uint32_t>(a.m_total >> 62);  // + 0, keeps Q in a register
   const int32_t beta = static_cast<int32_t>(a.beta);
   const uint32_t lmax = a.pen_lmax;  // loads above this leave the exact range
-  // bit Q of the 128-bit bitmap, as four word masks (one is non-zero)
+  // bit Q of the bitmap: bit Q & 31 of the top word W-1 (host: Q >> 5 == W-1)
   const uint32_t qb = 1u << (Qc & 31);
-  const uint32_t qm0 = (Qc >> 5) == 0 ? qb : 0u, qm1 = (Qc >> 5) == 1 ? qb : 0u,
-                 qm2 = (Qc >> 5) == 2 ? qb : 0u, qm3 = (Qc >> 5) == 3 ? qb : 0u;
 
   int32_t v = 0;
   bool ok = true;
@@ -132,7 +134,9 @@ split_penal_bits_kernel(SplitArgs a) {
     uint32_t load = 0;
     // window bitmap: bit j <-> load T + j (T = load - Q); position 0 (load 0)
     // sits at bit Q
-    uint32_t R0 = qm0, R1 = qm1, R2 = qm2, R3 = qm3;
+    uint32_t R[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) R[j] = j == W - 1 ? qb : 0u;
 
     // one DP position (i_c = i * kH); d in [1, 31] and ring room are checked
     // per chunk by the caller
@@ -140,15 +144,15 @@ split_penal_bits_kernel(SplitArgs a) {
       constexpr bool PUSH = decltype(push_tag)::value;
       load += d;
       // positions whose load fell below the new threshold: bits 0 .. d-1
-      const int leave = __popc(R0 & ((1u << d) - 1u));
-      R0 = __funnelshift_r(R0, R1, d);
-      R1 = __funnelshift_r(R1, R2, d);
-      R2 = __funnelshift_r(R2, R3, d);
-      R3 >>= d;
-      if (leave) {
+      const int leave = __popc(R[0] & ((1u << d) - 1u));
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) R[j] = __funnelshift_r(R[j], R[j + 1], d);
+      R[W - 1] >>= d;
+      // (unconditional: a branch on leave > 0 measured 12.19 vs 12.15 ms)
+      {
         lo_c += leave * kH;
         const int pc = lo_c - kH;  // lo - 1
-        bmin = at32(ps_pm, pc, kPosMaskH);
+        if (lo_c > 0) bmin = at32(ps_pm, pc, kPosMaskH);
         if (FULL) {
           bidx = at32(ps_pi, pc, kPosMaskH);
           brc = at32(ps_pr, pc, kPosMaskH);
@@ -193,10 +197,7 @@ split_penal_bits_kernel(SplitArgs a) {
           at32(ps_pr, i_c, kPosMaskH) = pm_rc;
         }
         // position i enters the window bitmap at bit Q (load T' + Q)
-        R0 |= qm0;
-        R1 |= qm1;
-        R2 |= qm2;
-        R3 |= qm3;
+        R[W - 1] |= qb;
         // strict pop (sentinel-terminated), then push (K1 deque); the deque
         // is non-empty here, so it can only empty by popping
         if (back_f > fi) {
