@@ -609,13 +609,14 @@ void validate_instance(const scendp_routing* inst) {
     fail(SCENDP_ERR_INVALID_ARGUMENT, "penalty beta must be >= 0");
 }
 
-void validate_tour(const int32_t* tour, int n) {
-  std::vector<char> seen(static_cast<size_t>(n) + 1, 0);
+// seen[c] == stamp marks customer c as visited by this tour; one array for
+// all tours of a call (stamp = tour index + 1), no clearing per tour
+void validate_tour(const int32_t* tour, int n, std::vector<uint32_t>& seen, uint32_t stamp) {
   for (int i = 0; i < n; ++i) {
     const int c = tour[i];
-    if (c < 1 || c > n || seen[c])
+    if (c < 1 || c > n || seen[c] == stamp)
       fail(SCENDP_ERR_INVALID_ARGUMENT, "tour is not a permutation of 1.." + std::to_string(n));
-    seen[c] = 1;
+    seen[c] = stamp;
   }
 }
 
@@ -1032,7 +1033,11 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
     const int n = inst->n;
     if (!tours || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one tour");
     if (k_tours >= (1u << 23)) fail(SCENDP_ERR_UNSUPPORTED, "too many tours per call");
-    for (uint32_t q = 0; q < k_tours; ++q) validate_tour(tours + static_cast<size_t>(q) * n, n);
+    {
+      std::vector<uint32_t> seen(static_cast<size_t>(n) + 1, 0u);
+      for (uint32_t q = 0; q < k_tours; ++q)
+        validate_tour(tours + static_cast<size_t>(q) * n, n, seen, q + 1);
+    }
     if (sc->rows != static_cast<uint64_t>(n))
       fail(SCENDP_ERR_INVALID_ARGUMENT, "demand column has " + std::to_string(sc->rows) +
                                             " entries, instance has " + std::to_string(n) +
