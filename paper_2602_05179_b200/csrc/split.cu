@@ -803,7 +803,7 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
   if (!linear && !a.hard && a.pen_lmax > 0 && small_tables) {
     const int T = kPenThreads;
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + 2 * 4) +
-                        static_cast<size_t>(T) * (a.pen_bits ? penal_bits_ring_bytes(FULL)
+                        static_cast<size_t>(T) * (a.pen_bits ? penal_bits_ring_bytes(FULL, a.n >= 100 ? 64 : 32)
                                                              : penal_ring_bytes(FULL));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {
@@ -811,17 +811,25 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
       kernel<<<grid, T, smem, ctx->stream>>>(a);
     };
     if (a.pen_bits) {
-      auto bits = [&](auto ident) {
+      auto bits = [&](auto ident, auto pr) {
         constexpr bool I = decltype(ident)::value;
+        constexpr int PR = decltype(pr)::value;
         switch (a.Q >> 5) {
-          case 0: go(split_penal_bits_kernel<FULL, SRC, I, 1>); break;
-          case 1: go(split_penal_bits_kernel<FULL, SRC, I, 2>); break;
-          case 2: go(split_penal_bits_kernel<FULL, SRC, I, 3>); break;
-          default: go(split_penal_bits_kernel<FULL, SRC, I, 4>); break;
+          case 0: go(split_penal_bits_kernel<FULL, SRC, I, 1, PR>); break;
+          case 1: go(split_penal_bits_kernel<FULL, SRC, I, 2, PR>); break;
+          case 2: go(split_penal_bits_kernel<FULL, SRC, I, 3, PR>); break;
+          default: go(split_penal_bits_kernel<FULL, SRC, I, 4, PR>); break;
         }
       };
-      if (a.ident) bits(std::true_type{});
-      else bits(std::false_type{});
+      using P32 = std::integral_constant<int, 32>;
+      using P64 = std::integral_constant<int, 64>;
+      if (a.n >= 100) {
+        if (a.ident) bits(std::true_type{}, P64{});
+        else bits(std::false_type{}, P64{});
+      } else {
+        if (a.ident) bits(std::true_type{}, P32{});
+        else bits(std::false_type{}, P32{});
+      }
     } else {
       if (a.ident) go(split_penal_kernel<FULL, SRC, true>);
       else go(split_penal_kernel<FULL, SRC, false>);

@@ -27,8 +27,14 @@
 
 // Host side: bytes of the K2-bits rings per thread (split.cu sizes the CTA):
 // deque f (4) [| rc (4)] and positions (2); PM ring (4) [| index, rc (8)].
-__host__ __device__ constexpr int penal_bits_ring_bytes(bool full) {
-  return kRing * (4 + 2 + (full ? 4 : 0)) + kPosRing * (4 + (full ? 8 : 0));
+// PR: prefix-minimum ring slots per thread (it holds [lo-1, i+4]).  32 keeps
+// 7 CTAs/SM; 64 (5 CTAs/SM) removes the hand-offs of long windows, which
+// grow with n: measured C5 (n = 50) 11.4 ms + 0.33 ms hand-off pass with 32
+// vs 14.3 ms with 64; C2 penalized (n = 200, 2x10^5) 0.61 ms per call with
+// 32 (7.5 % of scenarios handed off) vs 0.25 ms with 64.  The host takes 64
+// for n >= 100.
+__host__ __device__ constexpr int penal_bits_ring_bytes(bool full, int pr) {
+  return kRing * (4 + 2 + (full ? 4 : 0)) + pr * (4 + (full ? 8 : 0));
 }
 
 template <int OFF>
@@ -43,10 +49,12 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 
 // W: bitmap words, Q in [32 (W-1), 32 W) -- the entry bit Q then always sits
 // in the top word (one OR per position, W funnel shifts)
-template <bool FULL, int SRC, bool IDENT, int W>
+template <bool FULL, int SRC, bool IDENT, int W, int PR>
 __global__ void __launch_bounds__(kPenThreads)
 split_penal_bits_kernel(SplitArgs a) {
   constexpr int T = kPenThreads;
+  constexpr int kBPosRing = PR;
+  constexpr int kBPosMaskH = kBPosRing * kH - 1;
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned long long s_agg[kAggSlots];
   const uint32_t k = blockIdx.y;
@@ -59,10 +67,10 @@ split_penal_bits_kernel(SplitArgs a) {
   int32_t* dq_f = reinterpret_cast<int32_t*>(smem) + tid;
   int32_t* dq_r = dq_f + kRing * T;                                            // FULL
   int32_t* ps_pm = dq_f + (FULL ? 2 : 1) * kRing * T;
-  int32_t* ps_pi = ps_pm + kPosRing * T;                                       // FULL
-  int32_t* ps_pr = ps_pi + kPosRing * T;                                       // FULL
-  uint16_t* dq_p = reinterpret_cast<uint16_t*>(ps_pm - tid + (FULL ? 3 : 1) * kPosRing * T) + tid;
-  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + T * penal_bits_ring_bytes(FULL));
+  int32_t* ps_pi = ps_pm + kBPosRing * T;                                       // FULL
+  int32_t* ps_pr = ps_pi + kBPosRing * T;                                       // FULL
+  uint16_t* dq_p = reinterpret_cast<uint16_t*>(ps_pm - tid + (FULL ? 3 : 1) * kBPosRing * T) + tid;
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + T * penal_bits_ring_bytes(FULL, PR));
   int32_t* s_tab = reinterpret_cast<int32_t*>(s_col + (IDENT ? 0 : npad));  // A | B
   {
     const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
@@ -152,10 +160,10 @@ split_penal_bits_kernel(SplitArgs a) {
       {
         lo_c += leave * kH;
         const int pc = lo_c - kH;  // lo - 1
-        if (lo_c > 0) bmin = at32(ps_pm, pc, kPosMaskH);
+        if (lo_c > 0) bmin = at32(ps_pm, pc, kBPosMaskH);
         if (FULL) {
-          bidx = at32(ps_pi, pc, kPosMaskH);
-          brc = at32(ps_pr, pc, kPosMaskH);
+          bidx = at32(ps_pi, pc, kBPosMaskH);
+          brc = at32(ps_pr, pc, kBPosMaskH);
         }
         // deque entries before lo leave from the front (entry i-1 stays:
         // d_i <= 31 < ... its load is >= T' since d_i <= Q); the vacated slot
@@ -191,10 +199,10 @@ split_penal_bits_kernel(SplitArgs a) {
             pm_rc = rc;
           }
         }
-        at32(ps_pm, i_c, kPosMaskH) = pm;
+        at32(ps_pm, i_c, kBPosMaskH) = pm;
         if (FULL) {
-          at32(ps_pi, i_c, kPosMaskH) = pm_i;
-          at32(ps_pr, i_c, kPosMaskH) = pm_rc;
+          at32(ps_pi, i_c, kBPosMaskH) = pm_i;
+          at32(ps_pr, i_c, kBPosMaskH) = pm_rc;
         }
         // position i enters the window bitmap at bit Q (load T' + Q)
         R[W - 1] |= qb;
@@ -235,7 +243,7 @@ split_penal_bits_kernel(SplitArgs a) {
     // room for 4 pushes: the PM ring must hold [lo-1, i] for every i of the
     // chunk, the deque its live entries + 4 + the sentinel slot
     auto room = [&](int s0) {
-      if ((s0 + 4) * kH - lo_c > (kPosRing - 2) * kH) return false;
+      if ((s0 + 4) * kH - lo_c > (kBPosRing - 2) * kH) return false;
       if (tail + 4 * kDqStep <= fbase + kDqPlane) return true;
       // compact: the sentinel and the live entries back to slots 0..len
       const uint32_t len = (tail - head) / kDqStep;

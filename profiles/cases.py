@@ -13,6 +13,7 @@ Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
             nothing pops), zero-heavy demands uniform:0:2, 10^5 scenarios --
             windows of ~100 positions, every deque outgrows the ring and
             takes the hand-off (generic) pass
+  c2pen     C2 penalized (beta=10), 2x10^5 scenarios, identity tour
   c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
   c3float   the non-dyadic C3 twin (K3 fp64 path)
   c4        DSIRP 200 customers x 10^6 scenarios (one GPU)
@@ -46,6 +47,14 @@ def build(ctx, c):
         idx = np.arange(n + 2, dtype=np.float64)
         inst = RoutingInstance(n, 100, True, 0.0, np.abs(idx[:, None] - idx[None, :]))
         dist = Distribution("uniform", 0, 2, seed=derive_stream(1, 0x5343454E, 0))
+        sc = ctx.gen_scenarios(dist, n, m)
+        fn = lambda: ctx.split_eval(inst, tour, (sc, A.MEM_DEVICE_TILED), count=m, totals=False)
+        return fn, None
+    if c == "c2pen":
+        n, m = 200, 200_000
+        tour = np.arange(1, n + 1, dtype=np.int32)
+        inst = make_random_instance(n, 1, 100, False, 10.0)
+        dist = Distribution("uniform", 1, 10, seed=derive_stream(1, 0x5343454E, 0))
         sc = ctx.gen_scenarios(dist, n, m)
         fn = lambda: ctx.split_eval(inst, tour, (sc, A.MEM_DEVICE_TILED), count=m, totals=False)
         return fn, None
