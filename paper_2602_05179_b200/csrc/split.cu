@@ -424,37 +424,68 @@ split_generic_kernel(SplitArgs a, int list_mode, uint64_t n_range_items,
       // minimum of g(p) = f(p) - beta L_p); B wins ties (earlier indices).
       // Every value is an integer below 2^31, so each fp64 op is exact and
       // equals the reference's ((f + dist_i) + ret_i) + beta * excess.
+      // The deque's front (f, position, routes), its back f and the B
+      // candidate's routes live in registers: a position reads global
+      // scratch only when the window start advances (f, load of the leaving
+      // position) or an entry pops.
       int head = 0, tail = 0, lo = 0, bidx = -1;
       double bmin = kInfD;
+      int32_t brc = 0;
       dq[tail++] = 0;
+      double front_f = f0, back_f = f0;
+      int32_t front_p = 0, front_rc = 0;
+      int64_t lo_ld = 0;  // ld[lo]
       const double beta = a.beta;
       for (int i = 1; i <= n; ++i) {
-        while (lo < i && ld[i] - ld[lo] > a.Q) {
-          const double g = f[lo] - beta * static_cast<double>(ld[lo]);
+        const int64_t li = ld[i];
+        while (lo < i && li - lo_ld > a.Q) {
+          const double g = f[lo] - beta * static_cast<double>(lo_ld);
           if (g < bmin) {
             bmin = g;
             bidx = lo;
+            brc = rcs[lo];
           }
           ++lo;
+          lo_ld = ld[lo];
         }
-        while (head < tail && dq[head] < lo) ++head;
-        const double candA = head < tail ? (f[dq[head]] + dist[i]) + ret[i] : kInfD;
+        if (front_p < lo) {
+          do {
+            ++head;
+            front_p = head < tail ? dq[head] : 0x7fffffff;
+          } while (front_p < lo);
+          if (head < tail) {
+            front_f = f[front_p];
+            front_rc = rcs[front_p];
+          }
+        }
+        const double candA = head < tail ? (front_f + dist[i]) + ret[i] : kInfD;
         const double candB = bidx >= 0 ? ((bmin + dist[i]) + ret[i]) +
-                                             beta * static_cast<double>(ld[i] - a.Q)
+                                             beta * static_cast<double>(li - a.Q)
                                        : kInfD;
         const bool useB = candB <= candA;
         v = useB ? candB : candA;
-        const int32_t bestp = useB ? bidx : dq[head];
-        rcs[i] = rcs[bestp] + 1;
+        const int32_t bestp = useB ? bidx : front_p;
+        const int32_t rci = (useB ? brc : front_rc) + 1;
+        rcs[i] = rci;
         if (FULL) {
           Vout[static_cast<uint64_t>(i) * kTile] = v;
           Cout[static_cast<uint64_t>(i) * kTile] = bestp;
         }
         if (i < n) {
           const double fi = (v + c0[i]) - dist[i + 1];
-          while (tail > head && f[dq[tail - 1]] > fi) --tail;
-          dq[tail++] = i;
+          while (tail > head && back_f > fi) {
+            --tail;
+            back_f = tail > head ? f[dq[tail - 1]] : -kInfD;
+          }
+          dq[tail] = i;
           f[i] = fi;
+          if (tail == head) {
+            front_f = fi;
+            front_p = i;
+            front_rc = rci;
+          }
+          ++tail;
+          back_f = fi;
         }
       }
     } else {
