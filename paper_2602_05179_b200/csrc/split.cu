@@ -874,8 +874,8 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     ctx->timing_end(tok);
     return;
   } else if (linear) {
-    const int T = kK1Threads;
     const bool intv = a.itab != nullptr;
+    const int T = k1_threads(intv);
     const size_t vt = intv ? 4 : 8;
     // column table (non-identity tours), position tables, per-thread rings
     const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + (intv ? 2 : 4) * vt) +

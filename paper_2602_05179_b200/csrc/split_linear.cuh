@@ -29,9 +29,12 @@
 
 constexpr int32_t kIntInf = 1 << 30;      // value of an emptied window
 constexpr int32_t kIntFinite = 1 << 29;   // v < kIntFinite  <=>  finite
-constexpr int kK1Threads = 128;           // CTA size (ring stride)
+// CTA size: 128 for the int32 path; 256 for fp64, whose per-CTA tour table
+// (32 B per position) then costs half the shared memory per warp -- 40
+// instead of 32 warps per SM (C2 float 0.327 -> 0.306 ms; the int32 forms
+// gain nothing, the random-tour one loses: 0.247 -> 0.261 ms)
+__host__ __device__ constexpr int k1_threads(bool intv) { return intv ? 128 : 256; }
 constexpr int kK1Prefetch = 2;            // demand chunks in flight ahead
-constexpr int kStep = kK1Threads * 4;     // bytes between a thread's consecutive ring slots
 // Deque slots per thread (sentinel included; any count -- the ring is not
 // circular).  Identity tours: 12.  At C2 the deque holds <= 6 entries at a
 // chunk start (simulated over 2000 scenarios), so 12 slots keep the 4-push
@@ -39,8 +42,12 @@ constexpr int kStep = kK1Threads * 4;     // bytes between a thread's consecutiv
 // loads: 0.238 -> 0.227 ms; 11 slots: same, 10: hand-offs).  Column-table
 // (random) tours keep longer deques: 16 (12 hands off at C2).
 __host__ __device__ constexpr int k1_ring(bool ident) { return ident ? 12 : 16; }
-template <int RING>
-constexpr int kPlaneOf = RING * kStep;   // bytes per ring plane (all threads)
+// bytes between a thread's consecutive ring slots (4-byte planes, T threads)
+// and per ring plane
+template <int T>
+constexpr int kStepOf = T * 4;
+template <int RING, int T>
+constexpr int kPlaneOf = RING * kStepOf<T>;
 
 // The deque ring.  Every field is a plane of 4-byte slots, thread-minor
 // ([slot][thread], bank-conflict-free): f (int32, or the low word of the
@@ -66,9 +73,9 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.b32 [%0+%1], %2;" ::"r"(a), "n"(OFF), "r"(v));
 }
 
-template <typename VT, int RING>
+template <typename VT, int RING, int T>
 struct K1Ring {
-  static constexpr int kPlane = kPlaneOf<RING>;
+  static constexpr int kPlane = kPlaneOf<RING, T>;
   static constexpr bool kInt = std::is_same<VT, int32_t>::value;
   static constexpr int kHi = 1;            // fp64 high word
   static constexpr int kL = kInt ? 1 : 2;  // load
@@ -144,10 +151,11 @@ __device__ __forceinline__ VT k1_neg_inf() {
 // to slots 0..len (rare: the head advances only by evictions).  Returns
 // false when even the compacted deque has no room (the scenario then takes
 // the generic path).
-template <typename VT, bool FULL, int RING>
+template <typename VT, bool FULL, int RING, int T>
 __device__ __forceinline__ bool k1_room(K1State<VT>& s, uint32_t base, int pushes) {
-  if (s.tail + pushes * kStep <= base + kPlaneOf<RING>) return true;
-  using R = K1Ring<VT, RING>;
+  constexpr int kStep = kStepOf<T>;
+  if (s.tail + pushes * kStep <= base + kPlaneOf<RING, T>) return true;
+  using R = K1Ring<VT, RING, T>;
   const int len = static_cast<int>(s.tail - s.head) / kStep;
   if (len + 1 + pushes > RING) return false;
   uint32_t dst = base + kStep;
@@ -170,10 +178,11 @@ __device__ __forceinline__ bool k1_room(K1State<VT>& s, uint32_t base, int pushe
 // NOEVICT (with SAFE = false): the caller proved no eviction can happen at
 // this position (see the chunk loop), so the window test is skipped.
 // The caller guarantees a free slot at the tail (k1_room).
-template <typename VT, bool FULL, bool PUSH, bool SAFE, bool NOEVICT, int RING>
+template <typename VT, bool FULL, bool PUSH, bool SAFE, bool NOEVICT, int RING, int T>
 __device__ __forceinline__ void k1_step(K1State<VT>& s, int i, uint32_t d, uint32_t Qc, VT t0,
                                         VT t1, VT t2, VT t3, double* Vout, int32_t* Cout) {
-  using R = K1Ring<VT, RING>;
+  using R = K1Ring<VT, RING, T>;
+  constexpr int kStep = kStepOf<T>;
   s.load += d;
   // evict predecessors whose route (p, i] exceeds Q (split.cpp:93-96); the
   // evicted slot becomes the -inf sentinel below the new head
@@ -320,10 +329,11 @@ __device__ __forceinline__ double2 ldtab2(const P* p) {
   return *reinterpret_cast<const double2*>(p);
 }
 template <bool FULL, int SRC, bool INTV, bool IDENT>
-__global__ void __launch_bounds__(kK1Threads)
+__global__ void __launch_bounds__(k1_threads(INTV))
 split_linear_kernel(SplitArgs a) {
   using VT = typename std::conditional<INTV, int32_t, double>::type;
-  constexpr int T = kK1Threads;
+  constexpr int T = k1_threads(INTV);
+  constexpr int kStep = kStepOf<T>;
   constexpr int RING = k1_ring(IDENT);
   extern __shared__ __align__(16) char smem[];
   __shared__ unsigned long long s_agg[kAggSlots];
@@ -388,7 +398,7 @@ split_linear_kernel(SplitArgs a) {
     s.v = VT(0);
     s.load = 0u;
     // slot 0: -inf sentinel (always the slot below the head); slot 1: p = 0
-    using R = K1Ring<VT, RING>;
+    using R = K1Ring<VT, RING, T>;
     s.head = rbase + kStep;
     s.tail = rbase + 2 * kStep;
     R::set_f(rbase, k1_neg_inf<VT>());
@@ -404,7 +414,7 @@ split_linear_kernel(SplitArgs a) {
     const int nfull = npush >> 2;
     // a chunk pushes 4: room for them below the ring's end (compacting the
     // deque when needed), else the scenario takes the generic path
-    auto room4 = [&] { return k1_room<VT, FULL, RING>(s, rbase, 4); };
+    auto room4 = [&] { return k1_room<VT, FULL, RING, T>(s, rbase, 4); };
     auto chunk = [&](int s0, uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {
       // position constants: int32 A/B for the chunk as two 128-bit loads up
       // front (latency hidden behind the first steps); fp64 (dist, ret, c0,
@@ -425,10 +435,10 @@ split_linear_kernel(SplitArgs a) {
         if constexpr (!INTV) {
           const double2 p = ldtab2(tab + 4 * (s0 + j));
           const double2 q = ldtab2(tab + 4 * (s0 + j) + 2);
-          k1_step<VT, FULL, true, kSafe, kNoEvict, RING>(s, s0 + j + 1, d, Qc, p.x, p.y, q.x, q.y, Vout,
+          k1_step<VT, FULL, true, kSafe, kNoEvict, RING, T>(s, s0 + j + 1, d, Qc, p.x, p.y, q.x, q.y, Vout,
                                                    Cout);
         } else {
-          k1_step<VT, FULL, true, kSafe, kNoEvict, RING>(s, s0 + j + 1, d, Qc, t0[j], t1[j], t2[j],
+          k1_step<VT, FULL, true, kSafe, kNoEvict, RING, T>(s, s0 + j + 1, d, Qc, t0[j], t1[j], t2[j],
                                                    t3[j], Vout, Cout);
         }
       };
@@ -534,7 +544,7 @@ split_linear_kernel(SplitArgs a) {
     }
     // remaining pushing positions (< 4), then position n (no push)
     for (int i = nfull * 4 + 1; ok && i <= n; ++i) {
-      if (!k1_room<VT, FULL, RING>(s, rbase, 1)) {
+      if (!k1_room<VT, FULL, RING, T>(s, rbase, 1)) {
         ok = false;
         break;
       }
@@ -550,8 +560,8 @@ split_linear_kernel(SplitArgs a) {
         x2 = tab[4 * sl + 2];
         x3 = tab[4 * sl + 3];
       }
-      if (i < n) k1_step<VT, FULL, true, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
-      else k1_step<VT, FULL, false, true, false, RING>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
+      if (i < n) k1_step<VT, FULL, true, true, false, RING, T>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
+      else k1_step<VT, FULL, false, true, false, RING, T>(s, i, d, Qc, x0, x1, x2, x3, Vout, Cout);
     }
     if (!ok) {
       push_overflow(a, k, wl);
