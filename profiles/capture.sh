@@ -45,7 +45,7 @@ cap k1gen split_linear_kernel c2gen
 cap k1f split_linear_kernel c2float
 cap k1r split_linear_kernel c2rand
 cap k1rf split_linear_kernel c2randf
-cap k2 split_penal_kernel c5
+cap k2 split_penal c5
 cap k3 dsirp_fast_kernel c3
 cap k3f dsirp_fast_kernel c3float
 cap k3c4 dsirp_fast_kernel c4

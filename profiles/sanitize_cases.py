@@ -4,8 +4,9 @@
     compute-sanitizer --tool memcheck python profiles/sanitize_cases.py
 
 Covers K1 (int/fp64, cost-only/full, tiled/generated, identity/permuted
-tours, overflow to the generic kernel), K2-int and its O(n) generic
-fallback, the quadratic kernel, K3 (int/fp64, cost-only/full, several
+tours, deque compaction, overflow to the generic kernel incl. its bitmap
+path), K2-int, K2-bits (scanned and generated eligibility, compaction) and
+the O(n) generic fallback, the quadratic kernel, K3 (int/fp64, cost-only/full, several
 horizons), K4 (uniform/poisson/tnormal, both layouts), the tiled
 transforms, SCNB loading, K5 and the DSIRP long-horizon kernel.
 """
@@ -43,6 +44,25 @@ def main():
             ctx.split_eval(pen, tours, dem)
             ctx.split_eval(pen, tours[1], dem, full=True)
             ctx.split_eval(RoutingInstance(n, 30, False, 2.5, fc), tours, dem)
+            # K2-bits (Q <= 127, demands in [1, 31]): scanned and generated
+            pen2 = make_random_instance(n, 1, 100, False, 10.0)
+            dem2 = rng.integers(1, 11, size=(m, n)).astype(np.uint32)
+            ctx.split_eval(pen2, tours, dem2)
+            ctx.split_eval(pen2, tours[1], dem2, full=True)
+            ctx.split_eval(pen2, tours, Distribution("uniform", 1, 31, seed=4), count=m)
+        # deque compaction (K1 and K2-bits) and mass hand-offs (list + bitmap)
+        n3 = 203
+        idx = np.arange(n3 + 2, dtype=np.float64)
+        line = np.abs(idx[:, None] - idx[None, :])
+        t3 = np.arange(1, n3 + 1, dtype=np.int32)
+        d3 = rng.integers(3, 6, size=(300, n3)).astype(np.uint32)
+        for hard in (True, False):
+            ctx.split_eval(RoutingInstance(n3, 12, hard, 3.0, line), t3, d3)
+            ctx.split_eval(RoutingInstance(n3, 12, hard, 3.0, line), t3, d3, full=True)
+        dz = rng.integers(0, 3, size=(70_000, 60)).astype(np.uint32)
+        idx = np.arange(62, dtype=np.float64)
+        ctx.split_eval(RoutingInstance(60, 100, True, 0.0, np.abs(idx[:, None] - idx[None, :])),
+                       np.arange(1, 61, dtype=np.int32), dz)
         for H in (1, 6, 11, 40):  # 40: the dense long-horizon kernel
             cs = [Customer(U=20, I0=5, H=H, fixed=np.full((H, 2), 7.0), unit=np.full((H, 2), 0.5)),
                   Customer(U=15, I0=3, H=H, fixed=np.full((H, 3), 3.1), unit=np.full((H, 3), 0.3))]
