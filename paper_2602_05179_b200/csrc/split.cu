@@ -163,12 +163,16 @@ __global__ void demand_range_kernel(const uint32_t* __restrict__ tiled, uint32_t
   bool bad = false;
   for (uint64_t e = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 4; e < total;
        e += stride) {
-    // 4 consecutive lanes of one row (kTile is a multiple of 4)
-    const uint4 v = *reinterpret_cast<const uint4*>(tiled + e);
+    // 4 consecutive lanes of one row (kTile is a multiple of 4); the padding
+    // lanes of the last tile are never read (they may be uninitialized)
     const uint64_t w = (e / (static_cast<uint64_t>(rows) * kTile)) * kTile + (e & 31);
-    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bad |= w + j < m && (vv[j] < dlo || vv[j] > dhi);
+    if (w + 3 < m) {
+      const uint4 v = *reinterpret_cast<const uint4*>(tiled + e);
+      bad |= v.x < dlo || v.x > dhi || v.y < dlo || v.y > dhi || v.z < dlo || v.z > dhi ||
+             v.w < dlo || v.w > dhi;
+    } else {
+      for (int j = 0; w + j < m; ++j) bad |= tiled[e + j] < dlo || tiled[e + j] > dhi;
+    }
   }
   if (__any_sync(__activemask(), bad) && (threadIdx.x & 31) == 0) atomicOr(outside, 1u);
 }
