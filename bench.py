@@ -461,7 +461,8 @@ def cpu_baseline():
 
 
 def secondary(ctx, d: Dist, args):
-    from paper_2602_05179_b200 import Customer, Distribution, RoutingInstance, make_random_instance
+    from paper_2602_05179_b200 import (Customer, Distribution, RoutingInstance, derive_stream,
+                                       make_random_instance, pinned_empty)
     from paper_2602_05179_b200 import _capi as A
     out = {}
     hbm_peak, _ = peaks()
@@ -552,6 +553,23 @@ def secondary(ctx, d: Dist, args):
     scen.free()
     scen2.free()
     tot.free()
+
+    # C1 (BASELINE configs[0], the reference's CPU-runnable case): n = 50,
+    # Q = 100, one fixed giant tour, 1,024 seeded Poisson(5) scenarios
+    # generated inside the DP kernel; a synchronous call with host totals --
+    # launch-latency-bound at this size, so timed per call
+    from paper_2602_05179_b200 import poisson_hi
+    n1, m1 = 50, 1024
+    inst1 = make_random_instance(n1, 1, Q_C2, True)
+    d1 = Distribution("poisson", 0, poisson_hi(5.0), mean=5.0, seed=derive_stream(1, 0x5343454E, 0))
+    t1 = np.arange(1, n1 + 1, dtype=np.int32)
+    h1 = pinned_empty(m1, np.float64)
+    c1 = ctx.split_eval(inst1, t1, d1, count=m1, host_totals=h1, prepare=True)
+    step_ms, _ = kernel_rate(c1, 200, 5)
+    out["split_c1"] = {"value": m1 / (step_ms / 1e3), "unit": UNIT, "ms_per_call": step_ms,
+                       "scaling": "replicated (whole C1 per rank)",
+                       "config": "C1: n=50 Q=100 hard, identity tour, 1024 Poisson(5) scenarios, "
+                                 "generated in-kernel, host totals"}
 
     # C5: 1000 giant tours x 10^5 scenarios, n = 50, penalized beta = 10, one
     # launch per rank over its scenario shard; the K x 16-word exact aggregate
@@ -711,6 +729,18 @@ def cpu_reference_secondary():
                                                                        dema, threads), ms),
                                            f"batched_split_costs, line metric, uniform:0:2, "
                                            f"{ms} scenarios")
+    # C1: the reference's batched_split_costs on the same 1,024 Poisson(5)
+    # scenarios (the reference has no Poisson kind; the oracle restatement
+    # samples them -- cpu-baseline leg only)
+    from oracle import POISSON, Oracle
+    from paper_2602_05179_b200 import poisson_hi
+    O = Oracle()
+    dem1 = O.generate(POISSON, 0, poisson_hi(5.0), R.derive_stream(1, 0x5343454E, 0), 50, 1024,
+                      mean=5.0)
+    c1 = R.make_random_instance(50, 1)
+    t1 = np.arange(1, 51, dtype=np.int32)
+    out["split_c1"] = (rate(lambda: R.split_costs(50, Q_C2, 1, 0.0, c1, t1, dem1, threads), 1024),
+                       "batched_split_costs, C1 (n=50, 1024 Poisson(5) scenarios)")
     # C5: K calls of batched_split_costs (saa.cpp:127-131), timed on 4 tours
     n5, m5, k5 = 50, 100_000, 4
     cost5 = R.make_random_instance(n5, 5)
