@@ -16,6 +16,7 @@ Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
   c2pen     C2 penalized (beta=10), 2x10^5 scenarios, identity tour
   c3        DSIRP 50 customers x 10^5 scenarios, H=6, U=100, R=3
   c3float   the non-dyadic C3 twin (K3 fp64 path)
+  c3full    C3 with exact schedules (device tiled outputs)
   c4        DSIRP 200 customers x 10^6 scenarios (one GPU)
   c5        1000 tours x 10^5 scenarios, n=50, penalized beta=10
   k5        dense (min,+) sweep: 6 stages x 3 options x 101x101, 10^5 frontiers
@@ -87,7 +88,7 @@ def build(ctx, c):
                                         full=full, out_kind="device_tiled", device_out=outs,
                                         sync=False)
         return fn, nbytes
-    elif c in ("c3", "c4", "c3float"):
+    elif c in ("c3", "c4", "c3float", "c3full"):
         nc, m, H = (200, 1_000_000, 6) if c == "c4" else (50, 100_000, 6)
         if c == "c3float":
             rng = np.random.default_rng(21)
@@ -100,10 +101,15 @@ def build(ctx, c):
                               unit=np.tile(0.5 + 0.25 * np.arange(3.0), (H, 1))) for _ in range(nc)]
         sc = ctx.gen_scenarios(Distribution("uniform", 0, 33, seed=7), nc * H, m)
         t3 = ctx.alloc(nc * m * 8)
-        fn = lambda: ctx.dsirp_eval(custs, (sc, A.MEM_DEVICE_TILED), count=m,
-                                    out_kind="device_tiled", device_out={"totals": t3},
-                                    sync=False)
-        return fn, nc * m * (4 * H + 8)
+        outs = {"totals": t3}
+        if c == "c3full":  # exact schedules (deliver, quantity, end inventory, option)
+            e = nc * m * H
+            outs.update(evaluated=ctx.alloc(nc * m), deliver=ctx.alloc(e),
+                        quantity=ctx.alloc(4 * e), end_inventory=ctx.alloc(4 * e),
+                        route_option=ctx.alloc(4 * e))
+        fn = lambda: ctx.dsirp_eval(custs, (sc, A.MEM_DEVICE_TILED), count=m, full=c == "c3full",
+                                    out_kind="device_tiled", device_out=outs, sync=False)
+        return fn, nc * m * (4 * H + 8 + (13 * H if c == "c3full" else 0))
     elif c == "c5":
         n5, m5, K5 = 50, 100_000, 1000
         inst5 = make_random_instance(n5, 5, 100, False, 10.0)
