@@ -450,9 +450,12 @@ split_linear_kernel(SplitArgs a) {
       // the converged lanes together (a warp-uniform branch, no per-position
       // window test; taken for most chunks since evictions are rare)
       if (max(max(d0, d1), max(d2, d3)) <= Qc) {
-        // (measured: pays off for the fp64 and full-solution forms; the lean
-        // int32 cost-only form is faster with its per-position test)
-        constexpr bool kSplitEvict = !std::is_same<VT, int32_t>::value || FULL;
+        // (measured: pays off for the fp64, full-solution and -- with the
+        // non-circular ring -- identity-tour int32 forms: C2 0.227 -> 0.215
+        // ms; column-table and generated int32 tours are faster with the
+        // per-position test: 0.247 vs 0.249, 0.412 vs 0.415 ms)
+        constexpr bool kSplitEvict =
+            !std::is_same<VT, int32_t>::value || FULL || (IDENT && SRC == kSrcTiled);
         const uint64_t last = static_cast<uint64_t>(s.load) + d0 + d1 + d2 + d3;
         if (kSplitEvict && __all_sync(__activemask(), last - s.front_l <= Qc)) {
           step(F_{}, T_{}, 0, d0);
