@@ -4,17 +4,19 @@
 //
 // The kernel is issue-bound (its DRAM traffic equals the algorithmic 4n+8
 // bytes per scenario), so the step is written for instruction count:
-//  * tour constants arrive as 128-bit broadcast loads once per 4 positions
-//    (chunked SoA tables in shared memory);
+//  * int32 tour constants arrive as 128-bit broadcast loads once per 4
+//    positions (chunked SoA tables in shared memory), fp64 ones per position;
 //  * the deque's front entry (f, load, idx, routes) and back f-value live in
-//    registers; the per-thread ring in shared memory is read only when an end
-//    moves (eviction / pop) and written once per push;
+//    registers; the per-thread ring in shared memory (not circular, ends
+//    addressed by 32-bit shared pointers, see K1Ring) is read only when an
+//    end moves (eviction / pop) and written once per push;
 //  * the deque is never empty at the start of a position (position i-1 was
 //    just pushed) and, unless d_i > Q, entry i-1 survives the eviction, so
 //    the common path carries no emptiness tests: the rare "window emptied"
 //    and "popped empty" cases are handled inside the eviction / pop bodies;
-//  * ring overflow is checked once per chunk (<= 11 entries before a chunk
-//    of 4 pushes cannot reach 16).
+//  * ring room is checked once per chunk (k1_room: compaction, else the
+//    scenario is handed off), and the window test is skipped for a whole
+//    chunk when a warp vote proves that no lane evicts.
 //
 // Value type VT: double (the reference's arithmetic verbatim), or int32 when
 // the host proved every tour cost is an integer and every partial sum stays
