@@ -292,8 +292,12 @@ uint64_t scendp_ctx::wave_for_model(uint64_t m, uint64_t fixed, uint64_t per_sce
   }
   if (budget_out) *budget_out = budget;
   if (per_scenario) {
-    const uint64_t room = budget > fixed ? budget - fixed : 0;
-    w = std::min(w, std::max<uint64_t>(32, (room / per_scenario) & ~uint64_t{31}));
+    // the model counts requested bytes; scratch_get allocates 1/8 more (and
+    // rounds each block to 4 KB), so the budget is applied to that
+    const uint64_t fixed_alloc = fixed + fixed / 8 + (uint64_t{64} << 10);
+    const uint64_t per_alloc = per_scenario + per_scenario / 8 + 1;
+    const uint64_t room = budget > fixed_alloc ? budget - fixed_alloc : 0;
+    w = std::min(w, std::max<uint64_t>(32, (room / per_alloc) & ~uint64_t{31}));
   }
   return w;
 }
