@@ -283,12 +283,13 @@ uint64_t scendp_ctx::wave_for_model(uint64_t m, uint64_t fixed, uint64_t per_sce
   uint64_t budget = opts.scratch_limit;
   if (!budget) {
     if (fixed + per_scenario * w <= scratch_total) {
-      budget = scratch_total;  // fits what is already held: no driver query
-    } else {
-      size_t fr = 0, tot = 0;
-      CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
-      budget = scratch_total + fr - fr / 16;
+      // fits what is already held: one wave, no driver query
+      if (budget_out) *budget_out = scratch_total;
+      return w;
     }
+    size_t fr = 0, tot = 0;
+    CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+    budget = scratch_total + fr - fr / 16;
   }
   if (budget_out) *budget_out = budget;
   if (per_scenario) {

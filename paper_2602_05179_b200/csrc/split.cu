@@ -882,7 +882,10 @@ void launch_wave(scendp_ctx* ctx, const SplitArgs& a, bool linear, char* generic
     const int T = k1_threads(intv);
     const size_t vt = intv ? 4 : 8;
     // column table (non-identity tours), position tables, per-thread rings
-    const size_t smem = static_cast<size_t>(a.npad) * ((a.ident ? 0 : 4) + (intv ? 2 : 4) * vt) +
+    // (generated demands on a column-table tour: the column table holds
+    // row * gamma as u64)
+    const size_t col_bytes = a.ident ? 0 : KSRC == kSrcTiled ? 4 : 8;
+    const size_t smem = static_cast<size_t>(a.npad) * (col_bytes + (intv ? 2 : 4) * vt) +
                         static_cast<size_t>(k1_ring(a.ident)) * T * (vt + 4 + (FULL ? 8 : 0));
     dim3 grid(static_cast<unsigned>((a.m_wave + T - 1) / T), a.k);
     auto go = [&](auto kernel) {

@@ -315,6 +315,19 @@ __device__ __forceinline__ void k1_demand4(const SplitArgs& a, uint64_t stream,
     d1 = val(ctr + kGamma);
     d2 = val(ctr + 2 * kGamma);
     d3 = val(ctr + 3 * kGamma);
+  } else if constexpr (SRC != kSrcTiled) {
+    // column-table tour, generated demands: s_col holds row * gamma (u64) per
+    // slot, so each counter is one 64-bit add (no per-draw multiply)
+    const ulonglong2* g = reinterpret_cast<const ulonglong2*>(s_col) + s0 / 2;
+    const ulonglong2 g01 = g[0], g23 = g[1];
+    auto val = [&](uint64_t z) {
+      if constexpr (SRC == kSrcGenU32) return mix_uniform32(a.gen, z);
+      else return draw_value(a.gen, mix64(z));
+    };
+    d0 = val(stream + g01.x);
+    d1 = val(stream + g01.y);
+    d2 = val(stream + g23.x);
+    d3 = val(stream + g23.y);
   } else {
     uint4 c;
     if constexpr (IDENT) c = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
@@ -342,16 +355,24 @@ split_linear_kernel(SplitArgs a) {
   const uint32_t k = blockIdx.y;
   const int n = a.n;
   const int npad = a.npad;  // multiple of 4, >= n + 4
-  // chunked tour tables, slot s = position s+1: col | t0..t3
+  // chunked tour tables, slot s = position s+1: col | t0..t3.  The column
+  // table holds rows (u32), or for generated demands row * gamma (u64: the
+  // generator's counter offset); identity tours have none
+  constexpr bool kGam = !IDENT && SRC != kSrcTiled;
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem);
-  VT* s_tab = reinterpret_cast<VT*>(s_col + (IDENT ? 0 : npad));  // IDENT: no column table
+  VT* s_tab = reinterpret_cast<VT*>(s_col + (IDENT ? 0 : kGam ? 2 * npad : npad));
   constexpr int ntab = INTV ? 2 : 4;
   // (fp64 tables read through L1 instead of shared memory, for more CTAs:
   // measured slower, C2 float 0.327 -> 0.405 ms)
   const VT* tab = s_tab;
   {
     const uint32_t* gcol = a.ccol + static_cast<uint64_t>(k) * npad;
-    if (!IDENT) for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
+    if (kGam) {
+      for (int x = threadIdx.x; x < npad; x += T)
+        reinterpret_cast<uint64_t*>(s_col)[x] = static_cast<uint64_t>(gcol[x]) * kGamma;
+    } else if (!IDENT) {
+      for (int x = threadIdx.x; x < npad; x += T) s_col[x] = gcol[x];
+    }
     if (INTV) {
       const int32_t* g = a.itab + static_cast<uint64_t>(k) * 2 * npad;
       for (int x = threadIdx.x; x < 2 * npad; x += T) reinterpret_cast<int32_t*>(s_tab)[x] = g[x];
@@ -554,7 +575,14 @@ split_linear_kernel(SplitArgs a) {
         break;
       }
       const int sl = i - 1;
-      const uint32_t d = demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]);
+      uint32_t d;
+      if constexpr (kGam) {
+        const uint64_t z = stream + reinterpret_cast<const uint64_t*>(s_col)[sl];
+        if constexpr (SRC == kSrcGenU32) d = mix_uniform32(a.gen, z);
+        else d = draw_value(a.gen, mix64(z));
+      } else {
+        d = demand_at(a, SRC, stream, tile_base, IDENT ? sl : s_col[sl]);
+      }
       VT x0, x1, x2 = VT(0), x3 = VT(0);
       if constexpr (INTV) {
         x0 = s_tab[sl];

@@ -7,6 +7,7 @@ Cases (SURVEY 8d shapes; same inputs as bench.py's lines):
   c2float   the same with non-integral costs (K1 fp64)
   c2full    C2 with full solutions (V, cuts)
   c2gen     C2 with in-kernel generation (the e2e call, batched_split_costs_generated)
+  c2genr    c2gen with a random giant tour (the e2e kernel)
   c2rand    C2 with a random giant tour (the SAA case), integer costs
   c2randf   the same with non-integral costs (K1 fp64, column gather)
   c2zero    adversarial: line metric (f increasing along the identity tour:
@@ -62,7 +63,7 @@ def build(ctx, c):
     if c.startswith("c2"):
         n, m = 200, 1_000_000
         tour = np.arange(1, n + 1, dtype=np.int32)
-        if c.startswith("c2rand"):
+        if c.startswith("c2rand") or c == "c2genr":
             tour = (np.random.default_rng(7).permutation(n) + 1).astype(np.int32)
         dist = Distribution("uniform", 1, 10, seed=derive_stream(1, 0x5343454E, 0))
         nbytes = m * (4 * n + 8) + (m * 12 * (n + 1) if c == "c2full" else 0)
@@ -73,7 +74,7 @@ def build(ctx, c):
         else:
             inst = make_random_instance(n, 1, 100, True)
         tot = ctx.alloc(m * 8)
-        if c == "c2gen":
+        if c in ("c2gen", "c2genr"):
             host_tot = pinned_empty(m, np.float64)
             fn = lambda: ctx.split_eval(inst, tour, dist, count=m, host_totals=host_tot)
         else:
