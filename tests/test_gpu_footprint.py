@@ -110,3 +110,35 @@ def test_allocation_failure_halves_the_wave(oracle):
     for key in ("totals", "V", "cuts", "route_count", "feasible"):
         np.testing.assert_array_equal(want[key], got[key])
     assert want["agg"] == got["agg"]
+
+
+@pytest.mark.parametrize("src", ["host", "generated", "tiled"])
+def test_repeated_calls_stay_one_wave(oracle, src):
+    """Without a scratch_limit a call that fits the device runs in one wave,
+    also when it fits the scratch the context already holds (regression: the
+    held-scratch fast path once charged the allocator's headroom against the
+    held total and cut every repeated call into dozens of waves)."""
+    from paper_2602_05179_b200 import Distribution
+    from paper_2602_05179_b200 import _capi as A
+    n, m = 200, 100_000
+    inst, tour, dem = _split_case(oracle, n, m)
+    dist = Distribution("uniform", 1, 10, seed=5)
+    with Context(0) as ctx:
+        keep = None
+        if src == "host":
+            scen = dem
+        elif src == "generated":
+            scen = dist
+        else:
+            keep = ctx.gen_scenarios(dist, n, m)
+            scen = (keep, A.MEM_DEVICE_TILED)
+        for _ in range(3):  # the same call again: its scratch is held exactly
+            ctx.split_eval(inst, tour, scen, count=m)
+            assert ctx.memory_info()["last_wave"] >= m
+        if keep is not None:
+            keep.free()
+    with Context(0) as ctx:
+        dd = oracle.generate(UNIFORM, 0, 33, 9, 24, m)
+        for _ in range(3):
+            ctx.dsirp_eval(_customers(4, 6), dd)
+            assert ctx.memory_info()["last_wave"] >= m
