@@ -178,6 +178,7 @@ struct scendp_ctx {
   void* pinned_tables(uint64_t bytes);
   std::vector<char> tours_blob;  // split tour tables resident at tours_dev
   std::vector<double> valid_costs;  // last cost matrix that passed validation
+  const double* last_costs_ptr = nullptr;  // where the last validated matrix was
   void* tours_dev = nullptr;
   void tables_uploaded();
 };

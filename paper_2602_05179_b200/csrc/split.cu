@@ -1073,8 +1073,14 @@ extern "C" scendp_status scendp_split_eval(scendp_ctx* ctx, const scendp_routing
       validate_instance_scalars(inst);
     } else {
       validate_instance(inst);
-      if (cells <= (size_t{1} << 20)) ctx->valid_costs.assign(inst->costs, inst->costs + cells);
-      else ctx->valid_costs.clear();  // very large matrices: no 8+ MB copy per change
+      // keep a copy for the memcmp only once a matrix is passed again (the
+      // same pointer as the last validated one): callers that hand a new
+      // matrix every call do not pay the copy (very large matrices: never)
+      if (cells <= (size_t{1} << 20) && inst->costs == ctx->last_costs_ptr)
+        ctx->valid_costs.assign(inst->costs, inst->costs + cells);
+      else
+        ctx->valid_costs.clear();
+      ctx->last_costs_ptr = inst->costs;
     }
     const int n = inst->n;
     if (!tours || k_tours == 0) fail(SCENDP_ERR_INVALID_ARGUMENT, "need at least one tour");
