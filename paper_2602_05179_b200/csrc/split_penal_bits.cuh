@@ -82,9 +82,6 @@ split_penal_bits_kernel(SplitArgs a) {
   agg_cta_init(s_agg);
   __syncthreads();
 
-  const uint64_t wl = blockIdx.x * static_cast<uint64_t>(T) + tid;
-  const bool active = wl < a.m_wave;
-  const uint64_t w = a.w_base + wl;
   uint32_t Qc = static_cast<uint32_t>(a.Q);  // host: Q <= 127
   Qc += static_cast<uint32_t>(a.m_total >> 62);  // + 0, keeps Q in a register
   const int32_t beta = static_cast<int32_t>(a.beta);
@@ -92,6 +89,12 @@ split_penal_bits_kernel(SplitArgs a) {
   // bit Q of the bitmap: bit Q & 31 of the top word W-1 (host: Q >> 5 == W-1)
   const uint32_t qb = 1u << (Qc & 31);
 
+  // a.pen_units blocks of T scenarios per CTA (the tour tables and the
+  // aggregate flush are per CTA)
+  for (int unit = 0; unit < a.pen_units; ++unit) {
+  const uint64_t wl = (blockIdx.x * static_cast<uint64_t>(a.pen_units) + unit) * T + tid;
+  const bool active = wl < a.m_wave;
+  const uint64_t w = a.w_base + wl;
   int32_t v = 0;
   bool ok = true;
   int32_t rc = 0;
@@ -312,6 +315,7 @@ split_penal_bits_kernel(SplitArgs a) {
   const double vout = active && ok ? static_cast<double>(v) : 0.0;
   __syncwarp();
   agg_warp_add(s_agg, agg_pieces(vout, true), active && ok);
+  }
   __syncthreads();
   agg_cta_flush(s_agg, a.agg + static_cast<uint64_t>(k) * kAggWords);
 }
