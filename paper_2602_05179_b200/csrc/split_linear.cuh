@@ -480,12 +480,10 @@ split_linear_kernel(SplitArgs a) {
       // the converged lanes together (a warp-uniform branch, no per-position
       // window test; taken for most chunks since evictions are rare)
       if (max(max(d0, d1), max(d2, d3)) <= Qc) {
-        // (measured: pays off for the fp64, full-solution and -- with the
-        // non-circular ring -- identity-tour int32 forms: C2 0.227 -> 0.215
-        // ms; column-table and generated int32 tours are faster with the
-        // per-position test: 0.247 vs 0.249, 0.412 vs 0.415 ms)
-        constexpr bool kSplitEvict =
-            !std::is_same<VT, int32_t>::value || FULL || (IDENT && SRC == kSrcTiled);
+        // (measured: pays off for every form since the non-circular ring and
+        // the 32-bit span -- C2 0.227 -> 0.212 ms, generated 0.415 -> 0.411,
+        // generated random tour 0.417 -> 0.406; random tiled tour neutral)
+        constexpr bool kSplitEvict = true;
         // the chunk's last window span: (load - front_l) <= Q plus four
         // demands <= Q each, so 32-bit arithmetic is exact while 5Q < 2^32
         // (int32 forms only: C2 0.215 -> 0.212 ms; the fp64 random-tour form
