@@ -179,6 +179,11 @@ struct scendp_ctx {
   std::vector<char> tours_blob;  // split tour tables resident at tours_dev
   std::vector<double> valid_costs;  // last cost matrix that passed validation
   const double* last_costs_ptr = nullptr;  // where the last validated matrix was
+  // the Poisson CDF resident in kScrCdf (make_gen_params)
+  double cdf_mean = -1.0;
+  int64_t cdf_hi = -1;
+  const double* cdf_dev = nullptr;
+  uint64_t cdf_gen = 0;
   void* tours_dev = nullptr;
   void tables_uploaded();
 };

@@ -220,10 +220,20 @@ GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_
   g.seed = d->seed;
   g.first_index = first_index;
   if (d->kind == SCENDP_DIST_POISSON) {
-    std::vector<double> cdf = poisson_table(d->mean, d->hi);
-    g.cdf_len = static_cast<int32_t>(cdf.size());
-    double* dev = static_cast<double*>(ctx->scratch_get(kScrCdf, cdf.size() * sizeof(double)));
-    ctx->copy(dev, cdf.data(), cdf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    // the table stays resident for the next call with the same (mean, hi)
+    // unless its scratch slot was reallocated or reused (tnormal's list)
+    const size_t len = static_cast<size_t>(d->hi) + 1;
+    double* dev = static_cast<double*>(ctx->scratch_get(kScrCdf, len * sizeof(double)));
+    if (!(ctx->cdf_mean == d->mean && ctx->cdf_hi == d->hi && ctx->cdf_dev == dev &&
+          ctx->cdf_gen == ctx->scratch_gen[kScrCdf])) {
+      std::vector<double> cdf = poisson_table(d->mean, d->hi);
+      ctx->copy(dev, cdf.data(), cdf.size() * sizeof(double), cudaMemcpyHostToDevice);
+      ctx->cdf_mean = d->mean;
+      ctx->cdf_hi = d->hi;
+      ctx->cdf_dev = dev;
+      ctx->cdf_gen = ctx->scratch_gen[kScrCdf];
+    }
+    g.cdf_len = static_cast<int32_t>(len);
     g.cdf = dev;
   }
   return g;
@@ -266,6 +276,7 @@ void launch_generate_tiled(scendp_ctx* ctx, const scendp_dist* d, uint64_t rows,
     check_dist(d);
     constexpr uint32_t kAmbCap = 4096;
     auto* amb = static_cast<char*>(ctx->scratch_get(kScrCdf, 16 + kAmbCap * 8ull));
+    ctx->cdf_dev = nullptr;  // the slot now holds tnormal's list, not a Poisson table
     CUDA_CHECK(cudaMemsetAsync(amb, 0, 16, ctx->stream));
     static const uint32_t force_every = [] {
       const char* e = std::getenv("SCENDP_TNORMAL_HOST_EVERY");
