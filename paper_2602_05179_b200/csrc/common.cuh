@@ -50,6 +50,7 @@ struct GenParams {
   uint32_t span32;     // span when it is < 2^32 (the common case), else 0
   const double* cdf;   // poisson: P[0..cdf_len-1], device
   int32_t cdf_len;
+  const int32_t* guide;  // poisson: guide[j] = min{k : cdf[k] >= j/64}, j = 0..64
   uint64_t seed;
   uint64_t first_index;
 };
@@ -113,7 +114,9 @@ __device__ __forceinline__ uint32_t draw_value(const GenParams& g, uint64_t x) {
   if (g.kind == SCENDP_DIST_UNIFORM) return uniform_draw(g, x);
   // next_unit: ((x >> 11) + 1) * 2^-53, exact in fp64
   const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
-  int32_t k = 0;
+  // the answer min{k : u <= cdf[k]} is >= guide[floor(64 u)] (cdf[k] >= u
+  // >= floor(64 u) / 64; both sides exact), so the scan starts there
+  int32_t k = __ldg(g.guide + static_cast<int>(u * 64.0));
   while (u > __ldg(g.cdf + k)) ++k;  // cdf[len-1] == 1.0 terminates
   return static_cast<uint32_t>(k);
 }

@@ -222,19 +222,31 @@ GenParams make_gen_params(scendp_ctx* ctx, const scendp_dist* d, uint64_t first_
   if (d->kind == SCENDP_DIST_POISSON) {
     // the table stays resident for the next call with the same (mean, hi)
     // unless its scratch slot was reallocated or reused (tnormal's list)
+    // table [len] doubles, then the 65-entry guide of draw_value
     const size_t len = static_cast<size_t>(d->hi) + 1;
-    double* dev = static_cast<double*>(ctx->scratch_get(kScrCdf, len * sizeof(double)));
-    if (!(ctx->cdf_mean == d->mean && ctx->cdf_hi == d->hi && ctx->cdf_dev == dev &&
+    const size_t bytes = len * sizeof(double) + 65 * sizeof(int32_t);
+    char* dev = static_cast<char*>(ctx->scratch_get(kScrCdf, bytes));
+    if (!(ctx->cdf_mean == d->mean && ctx->cdf_hi == d->hi &&
+          ctx->cdf_dev == reinterpret_cast<double*>(dev) &&
           ctx->cdf_gen == ctx->scratch_gen[kScrCdf])) {
       std::vector<double> cdf = poisson_table(d->mean, d->hi);
-      ctx->copy(dev, cdf.data(), cdf.size() * sizeof(double), cudaMemcpyHostToDevice);
+      std::vector<char> blob(bytes);
+      std::memcpy(blob.data(), cdf.data(), len * sizeof(double));
+      int32_t* guide = reinterpret_cast<int32_t*>(blob.data() + len * sizeof(double));
+      int32_t k = 0;
+      for (int j = 0; j <= 64; ++j) {
+        while (k + 1 < static_cast<int32_t>(len) && cdf[k] < j / 64.0) ++k;
+        guide[j] = k;
+      }
+      ctx->copy(dev, blob.data(), bytes, cudaMemcpyHostToDevice);
       ctx->cdf_mean = d->mean;
       ctx->cdf_hi = d->hi;
-      ctx->cdf_dev = dev;
+      ctx->cdf_dev = reinterpret_cast<double*>(dev);
       ctx->cdf_gen = ctx->scratch_gen[kScrCdf];
     }
     g.cdf_len = static_cast<int32_t>(len);
-    g.cdf = dev;
+    g.cdf = reinterpret_cast<const double*>(dev);
+    g.guide = reinterpret_cast<const int32_t*>(dev + len * sizeof(double));
   }
   return g;
 }
