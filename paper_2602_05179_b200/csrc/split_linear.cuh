@@ -346,6 +346,9 @@ __device__ __forceinline__ double2 ldtab2(const P* p) {
 template <bool FULL, int SRC, bool INTV, bool IDENT>
 __global__ void __launch_bounds__(k1_threads(INTV))
 split_linear_kernel(SplitArgs a) {
+  // the hand-off pass (launched programmatically dependent, see
+  // launch_overflow_pass) may start its CTAs now; they wait for this grid
+  asm volatile("griddepcontrol.launch_dependents;");
   using VT = typename std::conditional<INTV, int32_t, double>::type;
   constexpr int T = k1_threads(INTV);
   constexpr int kStep = kStepOf<T>;
