@@ -163,3 +163,36 @@ def test_long_horizons_dense_fallback(ctx, oracle, reference, H, U, full):
         a = got["agg"][c]
         assert (a["finite_count"], a["infeasible_count"]) == (fc, ic)
         assert abs(a["mean"] - mean) <= 1e-9 * abs(mean)
+
+
+@pytest.mark.parametrize("U,hi", [(300, 260), (100, 140), (200, 129), (20, 200)])
+def test_fp64_std_hold_large_demands(ctx, reference, U, hi):
+    """fp64 fast form with standard holding and demands on both sides of U
+    and of 128 (d = 128 and 129 exactly): shortage hold terms (rho h)*(-x)
+    for large -x, bit for bit against the reference."""
+    rng = np.random.default_rng(U + hi)
+    g, o = random_customer(rng, U=U, H=6, R=3, tab_hold=False, tab_del=False)
+    m = 900
+    dem = rng.integers(0, min(hi, 129), size=(m, 6)).astype(np.uint32)
+    big = rng.random(m) < 0.3
+    dem[big, rng.integers(0, 6, size=int(big.sum()))] = rng.integers(
+        100, hi + 1, size=int(big.sum())).astype(np.uint32)
+    dem[0, :] = 128
+    dem[1, 2] = 129
+    compare_one(ctx, reference, g, o, dem)
+
+
+def test_fp64_std_hold_multi_customer(ctx, reference):
+    """several fp64 standard-hold customers of different U (incl. 0) in one
+    cost-only launch, large demands."""
+    rng = np.random.default_rng(77)
+    H, m = 5, 1500
+    pairs = [random_customer(rng, U=int(u), H=H, R=2, tab_hold=False, tab_del=False)
+             for u in (3, 250, 64, 129, 0, 180)]
+    dem = rng.integers(0, 160, size=(m, len(pairs) * H)).astype(np.uint32)
+    got = ctx.dsirp_eval([p[0] for p in pairs], dem)
+    for c, (g, o) in enumerate(pairs):
+        sl = np.ascontiguousarray(dem[:, c * H:(c + 1) * H])
+        tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, sl)
+        np.testing.assert_array_equal(got["totals"][c], tot)
+        np.testing.assert_array_equal(got["evaluated"][c], ev)
