@@ -536,7 +536,10 @@ dsirp_fast_kernel(DsirpArgs a) {
   auto hold_of = [&](int x, int j) -> VT {
     if (htabular) return t_hold[j];
     if constexpr (INT) return hrI * j + nrhI * x;
-    else return __dmul_rn(x >= 0 ? h : rh, static_cast<double>(abs(x)));
+    // h*j + (rho h)*s with s = j - x: one of j, s is 0, so the FMA adds an
+    // exact +0 to (or scales +0 into) the single rounded product -- the same
+    // bits as __dmul_rn(x >= 0 ? h : rh, |x|), without the ALU selects
+    else return __fma_rn(h, static_cast<double>(j), __dmul_rn(rh, static_cast<double>(j - x)));
   };
   // aggregates: INT sums the scaled integer totals per thread (one exact
   // add per CTA and warp at the end); fp64 keeps a per-warp register
