@@ -196,3 +196,38 @@ def test_fp64_std_hold_multi_customer(ctx, reference):
         tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, sl)
         np.testing.assert_array_equal(got["totals"][c], tot)
         np.testing.assert_array_equal(got["evaluated"][c], ev)
+
+
+@pytest.mark.parametrize("h", [0.0, -0.0, 5e-324, 1e40])
+def test_fp64_hold_extremes(ctx, reference, h):
+    """fp64 fast form hold term fma(h, j, (rho h)*(j - x)) against the
+    reference's product at signed-zero, subnormal and huge holding costs
+    (non-dyadic delivery costs keep the call on the fp64 path)."""
+    rng = np.random.default_rng(31)
+    H, U = 6, 80
+    fixed, unit = rng.random((H, 3)) * 50, rng.random((H, 3)) * 2
+    g = Customer(U=U, I0=40, H=H, h=h, rho=1.7, fixed=fixed, unit=unit)
+    o = OCustomer(U, 40, H, h, 1.7, fixed=fixed, unit=unit)
+    dem = rng.integers(0, 70, size=(700, H)).astype(np.uint32)
+    compare_one(ctx, reference, g, o, dem)
+
+
+def test_fp64_hold_beyond_aggregate_range(ctx, reference):
+    """costs >= 2^192 (h = 1e300): per-scenario totals still bit-exact on the
+    fp64 fast form; the exact aggregate reports them as range_errors, not in
+    finite_count (include/scendp_cuda.h, scendp_agg_raw)."""
+    rng = np.random.default_rng(32)
+    H, U = 6, 80
+    fixed, unit = rng.random((H, 3)) * 50, rng.random((H, 3)) * 2
+    g = Customer(U=U, I0=40, H=H, h=1e300, rho=1.7, fixed=fixed, unit=unit)
+    o = OCustomer(U, 40, H, 1e300, 1.7, fixed=fixed, unit=unit)
+    dem = rng.integers(0, 70, size=(700, H)).astype(np.uint32)
+    tot, dl, q, ei, ro, ev, (mean, fc, ic) = reference.expected_cost(o, dem)
+    for full in (True, False):
+        got = ctx.dsirp_eval([g], dem, full=full)
+        np.testing.assert_array_equal(got["totals"][0], tot)
+        np.testing.assert_array_equal(got["evaluated"][0], ev)
+        a = got["agg"][0]
+        big = int(np.sum(np.isfinite(tot) & (tot >= 2.0 ** 192)))
+        assert big > 0
+        assert a["range_errors"] == big and a["finite_count"] + big == fc
